@@ -1,0 +1,926 @@
+// api.cu -- the C-ABI (include/mfx.h) over the device engine.
+//
+// Error text mirrors the reference exceptions word for word (graph.py:48-61,
+// dynamic.py:63-88, solver.py:79-84, 196-201, 244-250, 279-281) so the Python
+// shim can re-raise the same classes with the same messages.
+#include <limits.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <vector>
+
+#include "../../include/mfx.h"
+#include "engine.h"
+
+struct mfx_graph {
+  mfx::GraphObj g;
+};
+struct mfx_state {
+  mfx::StateObj s;
+  mfx::Ctrl *host_ctrl = nullptr;  // pinned mirror for async result download
+  long long *host_err = nullptr;   // pinned mirror of the batch error block
+  ~mfx_state() {
+    if (host_ctrl) cudaFreeHost(host_ctrl);
+    if (host_err) cudaFreeHost(host_err);
+  }
+};
+
+namespace mfx {
+
+thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+void count_launch(int k) { g_launches += k; }
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t _e = (x);                                                                 \
+    if (_e != cudaSuccess)                                                                \
+      return fail(MFX_CUDA_ERROR, "CUDA error %s at %s:%d: %s", cudaGetErrorName(_e),     \
+                  __FILE__, __LINE__, cudaGetErrorString(_e));                            \
+  } while (0)
+
+template <typename T>
+static void dfree(T *&p) {
+  if (p) cudaFree((void *)p);
+  p = nullptr;
+}
+
+Workspace::~Workspace() {
+  for (int q = 0; q < 2; ++q)
+    for (int b = 0; b < NBIN; ++b) dfree(F[q][b]);
+  for (int b = 0; b < NBIN; ++b) dfree(R[b]);
+  dfree(bases);
+  dfree(heavy);
+  dfree(mark);
+  dfree(stamp);
+  dfree(slot_first);
+  dfree(d_batch);
+  dfree(d_slot);
+  dfree(d_uv);
+  dfree(d_err);
+  dfree(d_red);
+}
+
+Topology::~Topology() {
+  cudaSetDevice(device);
+  dfree(off);
+  dfree(adj);
+  dfree(rev);
+  dfree(orig);
+  ws.~Workspace();
+  new (&ws) Workspace();
+  for (auto &e : ev)
+    if (e) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+GraphObj::~GraphObj() {
+  if (topo) cudaSetDevice(topo->device);
+  dfree(cap0);
+  dfree(pc);
+}
+
+StateObj::~StateObj() {
+  if (topo) cudaSetDevice(topo->device);
+  dfree(cf);
+  dfree(ex);
+  dfree(h);
+  dfree(ctrl);
+}
+
+cudaError_t ensure_workspace(Topology &t) {
+  Workspace &w = t.ws;
+  if (w.mark) return cudaSuccess;
+  size_t n = (size_t)(t.n > 0 ? t.n : 1);
+  w.n = t.n;
+  w.rcap = (int)(2 * n + 1024);
+  cudaError_t e;
+  for (int q = 0; q < 2; ++q)
+    for (int b = 0; b < NBIN; ++b)
+      if ((e = cudaMalloc(&w.F[q][b], sizeof(int) * n))) return e;
+  for (int b = 0; b < NBIN; ++b)
+    if ((e = cudaMalloc(&w.R[b], sizeof(int) * (size_t)w.rcap))) return e;
+  if ((e = cudaMalloc(&w.bases, sizeof(int) * n))) return e;
+  if ((e = cudaMalloc(&w.heavy, sizeof(int) * n))) return e;
+  if ((e = cudaMalloc(&w.stamp, sizeof(unsigned) * 4))) return e;
+  if ((e = cudaMemsetAsync(w.stamp, 0, sizeof(unsigned) * 4, t.stream))) return e;
+  if ((e = cudaMalloc(&w.slot_first, sizeof(int) * (size_t)(t.S > 0 ? t.S : 1)))) return e;
+  if ((e = cudaMemsetAsync(w.slot_first, 0x7f, sizeof(int) * (size_t)(t.S > 0 ? t.S : 1),
+                           t.stream)))
+    return e;
+  if ((e = cudaMalloc(&w.d_err, sizeof(long long) * 8))) return e;
+  if ((e = cudaMalloc(&w.d_red, sizeof(unsigned long long) * 64))) return e;
+  if ((e = cudaMalloc(&w.mark, sizeof(unsigned) * n))) return e;
+  return cudaMemsetAsync(w.mark, 0, sizeof(unsigned) * n, t.stream);
+}
+
+cudaError_t ensure_batch_capacity(Topology &t, int64_t k) {
+  Workspace &w = t.ws;
+  if (k <= w.kcap && w.d_batch) return cudaSuccess;
+  int64_t cap = k > 1024 ? k : 1024;
+  dfree(w.d_batch);
+  dfree(w.d_slot);
+  dfree(w.d_uv);
+  cudaError_t e;
+  if ((e = cudaMalloc(&w.d_batch, sizeof(int64_t) * 3 * (size_t)cap))) return e;
+  if ((e = cudaMalloc(&w.d_slot, sizeof(int) * (size_t)cap))) return e;
+  if ((e = cudaMalloc(&w.d_uv, sizeof(int) * 2 * (size_t)cap))) return e;
+  w.kcap = cap;
+  return cudaSuccess;
+}
+
+}  // namespace mfx
+
+using namespace mfx;
+
+// ---------------------------------------------------------------------------
+static int make_topology(int device, std::shared_ptr<Topology> &topo) {
+  int count = 0;
+  CK(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count)
+    return fail(MFX_VALUE_ERROR, "device %d out of range [0, %d)", device, count);
+  CK(cudaSetDevice(device));
+  topo = std::make_shared<Topology>();
+  topo->device = device;
+  CK(cudaStreamCreateWithFlags(&topo->stream, cudaStreamNonBlocking));
+  for (auto &e : topo->ev) CK(cudaEventCreate(&e));
+  CK(cudaDeviceGetAttribute(&topo->num_sms, cudaDevAttrMultiProcessorCount, device));
+  return MFX_OK;
+}
+
+// Choose the residual width and materialise cap0 / pair sums from int64 cap0.
+static int finish_graph(mfx_graph *G, int64_t *d_cap0_64, int force_wide) {
+  Topology &T = *G->g.topo;
+  unsigned long long *d_mx = nullptr, mx = 0;
+  CK(cudaMalloc(&d_mx, sizeof(unsigned long long)));
+  CK(pair_max_int64(T, d_cap0_64, d_mx));
+  CK(cudaMemcpyAsync(&mx, d_mx, sizeof(mx), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  cudaFree(d_mx);
+  T.cap_bytes = (!force_wide && mx < (1ull << 31)) ? 4 : 8;
+  size_t S = (size_t)(T.S > 0 ? T.S : 1);
+  CK(cudaMalloc(&G->g.cap0, S * T.cap_bytes));
+  CK(cudaMalloc(&G->g.pc, S * T.cap_bytes));
+  CK(launch_convert_cap(d_cap0_64, G->g.cap0, T.cap_bytes, T.S, T.stream));
+  CK(launch_refresh_pc(G->g));
+  CK(cudaStreamSynchronize(T.stream));
+  CK(ensure_workspace(T));
+  CK(cudaStreamSynchronize(T.stream));
+  return MFX_OK;
+}
+
+static int build_common(int64_t n, int64_t m, const int64_t *d_us, const int64_t *d_vs,
+                        const int64_t *d_caps, const int64_t *h_us, const int64_t *h_vs,
+                        const int64_t *h_caps, int device, int force_wide, mfx_graph **out) {
+  *out = nullptr;
+  if (n <= 0) return fail(MFX_GRAPH_ERROR, "vertex count must be positive, got %lld", (long long)n);
+  std::shared_ptr<Topology> topo;
+  int rc = make_topology(device, topo);
+  if (rc) return rc;
+  int64_t err[2];
+  int64_t *d_cap0 = nullptr;
+  CK(build_bicsr_device(n, m, d_us, d_vs, d_caps, *topo, &d_cap0, err, nullptr));
+  if (err[0]) {
+    if (d_cap0) cudaFree(d_cap0);
+    long long i = err[1];
+    auto val = [&](const int64_t *h, const int64_t *d) -> long long {
+      if (h) return h[i];
+      long long v = 0;
+      cudaMemcpy(&v, d + i, sizeof(v), cudaMemcpyDeviceToHost);
+      return v;
+    };
+    switch (err[0]) {
+      case 1: return fail(MFX_GRAPH_ERROR, "vertex count must be positive, got %lld", (long long)n);
+      case 2:
+        return fail(MFX_GRAPH_ERROR, "edge %lld: source vertex %lld out of range [0, %lld)", i,
+                    val(h_us, d_us), (long long)n);
+      case 3:
+        return fail(MFX_GRAPH_ERROR, "edge %lld: target vertex %lld out of range [0, %lld)", i,
+                    val(h_vs, d_vs), (long long)n);
+      case 4:
+        return fail(MFX_GRAPH_ERROR, "edge %lld: negative capacity %lld", i, val(h_caps, d_caps));
+      default:
+        return fail(MFX_VALUE_ERROR, "graph exceeds the int32 slot layout of one device");
+    }
+  }
+  mfx_graph *G = new mfx_graph();
+  G->g.topo = topo;
+  rc = finish_graph(G, d_cap0, force_wide);
+  cudaFree(d_cap0);
+  if (rc) {
+    delete G;
+    return rc;
+  }
+  *out = G;
+  return MFX_OK;
+}
+
+struct Staged {
+  void *p = nullptr;
+  ~Staged() {
+    if (p) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+int mfx_version(void) { return 1; }
+const char *mfx_last_error(void) { return g_last_error.c_str(); }
+int mfx_device_count(int *count) {
+  CK(cudaGetDeviceCount(count));
+  return MFX_OK;
+}
+int64_t mfx_launch_count(void) { return g_launches.load(); }
+
+int mfx_graph_build(int64_t n, int64_t m, const int64_t *us, const int64_t *vs,
+                    const int64_t *caps, int device, int force_wide, mfx_graph **out) {
+  if (n <= 0) return fail(MFX_GRAPH_ERROR, "vertex count must be positive, got %lld", (long long)n);
+  CK(cudaSetDevice(device));
+  Staged buf;
+  size_t M = (size_t)(m > 0 ? m : 1);
+  CK(cudaMalloc(&buf.p, 3 * M * sizeof(int64_t)));
+  int64_t *d = (int64_t *)buf.p;
+  if (m > 0) {
+    CK(cudaMemcpy(d, us, m * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d + M, vs, m * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d + 2 * M, caps, m * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  return build_common(n, m, d, d + M, d + 2 * M, us, vs, caps, device, force_wide, out);
+}
+
+int mfx_graph_build_device(int64_t n, int64_t m, const int64_t *d_us, const int64_t *d_vs,
+                           const int64_t *d_caps, int device, int force_wide, mfx_graph **out) {
+  return build_common(n, m, d_us, d_vs, d_caps, nullptr, nullptr, nullptr, device, force_wide, out);
+}
+
+int mfx_graph_from_bicsr(int64_t n, int64_t S, const int64_t *offsets, const int64_t *adj,
+                         const int64_t *rev, const int64_t *cap0, const uint8_t *is_original,
+                         int device, int force_wide, mfx_graph **out) {
+  *out = nullptr;
+  if (n <= 0) return fail(MFX_GRAPH_ERROR, "vertex count must be positive, got %lld", (long long)n);
+  if (S >= INT_MAX) return fail(MFX_VALUE_ERROR, "graph exceeds the int32 slot layout of one device");
+  std::shared_ptr<Topology> topo;
+  int rc = make_topology(device, topo);
+  if (rc) return rc;
+  size_t SS = (size_t)(S > 0 ? S : 1);
+  Staged b64, borig;
+  CK(cudaMalloc(&b64.p, sizeof(int64_t) * ((size_t)n + 1 + 3 * SS)));
+  CK(cudaMalloc(&borig.p, SS));
+  int64_t *d_off = (int64_t *)b64.p, *d_adj = d_off + n + 1, *d_rev = d_adj + SS,
+          *d_cap = d_rev + SS;
+  CK(cudaMemcpy(d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  if (S > 0) {
+    CK(cudaMemcpy(d_adj, adj, sizeof(int64_t) * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_rev, rev, sizeof(int64_t) * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_cap, cap0, sizeof(int64_t) * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(borig.p, is_original, S, cudaMemcpyHostToDevice));
+  }
+  CK(topology_from_bicsr(n, S, d_off, d_adj, d_rev, (const uint8_t *)borig.p, *topo));
+  long long mo = 0;
+  for (int64_t i = 0; i < S; ++i) mo += is_original[i] != 0;
+  topo->m_original = (int)mo;
+  mfx_graph *G = new mfx_graph();
+  G->g.topo = topo;
+  rc = finish_graph(G, d_cap, force_wide);
+  if (rc) {
+    delete G;
+    return rc;
+  }
+  *out = G;
+  return MFX_OK;
+}
+
+int mfx_graph_info_get(const mfx_graph *g, mfx_graph_info *info) {
+  const Topology &T = *g->g.topo;
+  info->n = T.n;
+  info->S = T.S;
+  info->m_original = T.m_original;
+  info->self_loops_dropped = T.diag[0];
+  info->parallel_edges_merged = T.diag[1];
+  info->reverse_stubs_added = T.diag[2];
+  info->cap_bytes = T.cap_bytes;
+  info->device = T.device;
+  return MFX_OK;
+}
+
+static int widen_download_i32(const int *d, int64_t *h, size_t cnt, cudaStream_t s) {
+  if (!h || cnt == 0) return MFX_OK;
+  std::vector<int> tmp(cnt);
+  CK(cudaMemcpyAsync(tmp.data(), d, sizeof(int) * cnt, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < cnt; ++i) h[i] = tmp[i];
+  return MFX_OK;
+}
+
+static int download_cap(const void *d, int cap_bytes, int64_t *h, size_t cnt, cudaStream_t s) {
+  if (!h || cnt == 0) return MFX_OK;
+  if (cap_bytes == 8) {
+    CK(cudaMemcpyAsync(h, d, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MFX_OK;
+  }
+  return widen_download_i32((const int *)d, h, cnt, s);
+}
+
+int mfx_graph_download(const mfx_graph *g, int64_t *offsets, int64_t *adj, int64_t *src,
+                       int64_t *rev, int64_t *cap0, uint8_t *is_original) {
+  const Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  int rc;
+  if ((rc = widen_download_i32(T.off, offsets, (size_t)T.n + 1, T.stream))) return rc;
+  if ((rc = widen_download_i32(T.adj, adj, (size_t)T.S, T.stream))) return rc;
+  if ((rc = widen_download_i32(T.rev, rev, (size_t)T.S, T.stream))) return rc;
+  if ((rc = download_cap(g->g.cap0, T.cap_bytes, cap0, (size_t)T.S, T.stream))) return rc;
+  if (is_original && T.S > 0) {
+    CK(cudaMemcpyAsync(is_original, T.orig, (size_t)T.S, cudaMemcpyDeviceToHost, T.stream));
+    CK(cudaStreamSynchronize(T.stream));
+  }
+  if (src && T.S > 0) {
+    Staged b;
+    CK(cudaMalloc(&b.p, sizeof(int64_t) * (size_t)T.S));
+    CK(download_src(T, (int64_t *)b.p));
+    CK(cudaMemcpyAsync(src, b.p, sizeof(int64_t) * (size_t)T.S, cudaMemcpyDeviceToHost, T.stream));
+    CK(cudaStreamSynchronize(T.stream));
+  }
+  return MFX_OK;
+}
+
+int mfx_graph_copy(const mfx_graph *g, mfx_graph **out) {
+  const Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  mfx_graph *G = new mfx_graph();
+  G->g.topo = g->g.topo;
+  size_t bytes = (size_t)(T.S > 0 ? T.S : 1) * T.cap_bytes;
+  cudaError_t e = cudaMalloc(&G->g.cap0, bytes);
+  if (!e) e = cudaMalloc(&G->g.pc, bytes);
+  if (!e) e = cudaMemcpyAsync(G->g.cap0, g->g.cap0, bytes, cudaMemcpyDeviceToDevice, T.stream);
+  if (!e) e = cudaMemcpyAsync(G->g.pc, g->g.pc, bytes, cudaMemcpyDeviceToDevice, T.stream);
+  if (!e) e = cudaStreamSynchronize(T.stream);
+  if (e) {
+    delete G;
+    CK(e);
+  }
+  *out = G;
+  return MFX_OK;
+}
+
+int mfx_graph_set_cap0(mfx_graph *g, const int64_t *cap0) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  if (T.S == 0) return MFX_OK;
+  if (T.cap_bytes == 4)
+    for (int64_t i = 0; i < T.S; ++i)
+      if (cap0[i] < 0 || cap0[i] >= (1ll << 30))
+        return fail(MFX_VALUE_ERROR, "capacity %lld does not fit the int32 residual storage",
+                    (long long)cap0[i]);
+  Staged b;
+  CK(cudaMalloc(&b.p, sizeof(int64_t) * (size_t)T.S));
+  CK(cudaMemcpy(b.p, cap0, sizeof(int64_t) * (size_t)T.S, cudaMemcpyHostToDevice));
+  CK(launch_convert_cap((const int64_t *)b.p, g->g.cap0, T.cap_bytes, T.S, T.stream));
+  CK(launch_refresh_pc(g->g));
+  CK(cudaStreamSynchronize(T.stream));
+  return MFX_OK;
+}
+
+int mfx_edge_indices(const mfx_graph *g, int64_t k, const int64_t *us, const int64_t *vs,
+                     int64_t *out) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  if (k <= 0) return MFX_OK;
+  CK(ensure_batch_capacity(T, k));
+  int64_t *d = T.ws.d_batch;
+  CK(cudaMemcpyAsync(d, us, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+  CK(cudaMemcpyAsync(d + k, vs, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+  CK(launch_edge_indices(g->g, k, d, d + k, d + 2 * k));
+  CK(cudaMemcpyAsync(out, d + 2 * k, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  return MFX_OK;
+}
+
+void mfx_graph_free(mfx_graph *g) { delete g; }
+
+// ---- state -------------------------------------------------------------------
+int mfx_state_create(const mfx_graph *g, int64_t source, int64_t sink, mfx_state **out) {
+  *out = nullptr;
+  const Topology &T = *g->g.topo;
+  if (source < 0 || source >= T.n)
+    return fail(MFX_VALUE_ERROR, "source %lld out of range [0, %d)", (long long)source, T.n);
+  if (sink < 0 || sink >= T.n)
+    return fail(MFX_VALUE_ERROR, "sink %lld out of range [0, %d)", (long long)sink, T.n);
+  CK(cudaSetDevice(T.device));
+  mfx_state *S = new mfx_state();
+  StateObj &st = S->s;
+  st.topo = g->g.topo;
+  st.s = (int)source;
+  st.t = (int)sink;
+  size_t SS = (size_t)(T.S > 0 ? T.S : 1);
+  cudaError_t e = cudaMalloc(&st.cf, SS * T.cap_bytes);
+  if (!e) e = cudaMalloc(&st.ex, sizeof(long long) * (size_t)T.n);
+  if (!e) e = cudaMalloc(&st.h, sizeof(int) * (size_t)T.n);
+  if (!e) e = cudaMalloc(&st.ctrl, sizeof(Ctrl));
+  if (!e) e = cudaMemsetAsync(st.ctrl, 0, sizeof(Ctrl), T.stream);
+  if (!e) e = cudaHostAlloc(&S->host_ctrl, sizeof(Ctrl), cudaHostAllocDefault);
+  if (!e) e = cudaHostAlloc(&S->host_err, sizeof(long long) * 8, cudaHostAllocDefault);
+  if (!e) e = launch_init_state(g->g, st);
+  if (!e) e = cudaStreamSynchronize(T.stream);
+  if (e) {
+    delete S;
+    CK(e);
+  }
+  *out = S;
+  return MFX_OK;
+}
+
+int mfx_state_copy(const mfx_state *st, mfx_state **out) {
+  const Topology &T = *st->s.topo;
+  CK(cudaSetDevice(T.device));
+  mfx_state *S = new mfx_state();
+  StateObj &d = S->s;
+  d.topo = st->s.topo;
+  d.s = st->s.s;
+  d.t = st->s.t;
+  d.excess_consistent = st->s.excess_consistent;
+  d.terminated_known = st->s.terminated_known;
+  size_t cfb = (size_t)(T.S > 0 ? T.S : 1) * T.cap_bytes;
+  cudaError_t e = cudaMalloc(&d.cf, cfb);
+  if (!e) e = cudaMalloc(&d.ex, sizeof(long long) * (size_t)T.n);
+  if (!e) e = cudaMalloc(&d.h, sizeof(int) * (size_t)T.n);
+  if (!e) e = cudaMalloc(&d.ctrl, sizeof(Ctrl));
+  if (!e) e = cudaHostAlloc(&S->host_ctrl, sizeof(Ctrl), cudaHostAllocDefault);
+  if (!e) e = cudaHostAlloc(&S->host_err, sizeof(long long) * 8, cudaHostAllocDefault);
+  if (!e) e = cudaMemcpyAsync(d.cf, st->s.cf, cfb, cudaMemcpyDeviceToDevice, T.stream);
+  if (!e) e = cudaMemcpyAsync(d.ex, st->s.ex, sizeof(long long) * T.n, cudaMemcpyDeviceToDevice, T.stream);
+  if (!e) e = cudaMemcpyAsync(d.h, st->s.h, sizeof(int) * T.n, cudaMemcpyDeviceToDevice, T.stream);
+  if (!e) e = cudaMemcpyAsync(d.ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToDevice, T.stream);
+  if (!e) e = cudaStreamSynchronize(T.stream);
+  if (e) {
+    delete S;
+    CK(e);
+  }
+  *out = S;
+  return MFX_OK;
+}
+
+int mfx_state_assign(mfx_state *dst, const mfx_state *src) {
+  if (dst->s.topo != src->s.topo)
+    return fail(MFX_VALUE_ERROR, "states belong to different graph topologies");
+  const Topology &T = *src->s.topo;
+  CK(cudaSetDevice(T.device));
+  size_t cfb = (size_t)(T.S > 0 ? T.S : 1) * T.cap_bytes;
+  CK(cudaMemcpyAsync(dst->s.cf, src->s.cf, cfb, cudaMemcpyDeviceToDevice, T.stream));
+  CK(cudaMemcpyAsync(dst->s.ex, src->s.ex, sizeof(long long) * T.n, cudaMemcpyDeviceToDevice, T.stream));
+  CK(cudaMemcpyAsync(dst->s.h, src->s.h, sizeof(int) * T.n, cudaMemcpyDeviceToDevice, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  dst->s.s = src->s.s;
+  dst->s.t = src->s.t;
+  dst->s.excess_consistent = src->s.excess_consistent;
+  dst->s.terminated_known = src->s.terminated_known;
+  return MFX_OK;
+}
+
+int mfx_state_upload(mfx_state *st, const int64_t *cf, const int64_t *excess,
+                     const int64_t *height) {
+  const Topology &T = *st->s.topo;
+  CK(cudaSetDevice(T.device));
+  if (cf && T.S > 0) {
+    if (T.cap_bytes == 8) {
+      CK(cudaMemcpy(st->s.cf, cf, sizeof(int64_t) * T.S, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<int> tmp((size_t)T.S);
+      for (int64_t i = 0; i < T.S; ++i) {
+        if (cf[i] < INT_MIN || cf[i] > INT_MAX)
+          return fail(MFX_VALUE_ERROR, "residual %lld does not fit the int32 residual storage",
+                      (long long)cf[i]);
+        tmp[i] = (int)cf[i];
+      }
+      CK(cudaMemcpy(st->s.cf, tmp.data(), sizeof(int) * T.S, cudaMemcpyHostToDevice));
+    }
+  }
+  if (excess) CK(cudaMemcpy(st->s.ex, excess, sizeof(int64_t) * T.n, cudaMemcpyHostToDevice));
+  if (height) {
+    std::vector<int> tmp((size_t)T.n);
+    for (int v = 0; v < T.n; ++v) tmp[v] = (int)height[v];
+    CK(cudaMemcpy(st->s.h, tmp.data(), sizeof(int) * T.n, cudaMemcpyHostToDevice));
+  }
+  st->s.excess_consistent = false;
+  st->s.terminated_known = false;
+  return MFX_OK;
+}
+
+int mfx_state_download(const mfx_state *st, int64_t *cf, int64_t *excess, int64_t *height) {
+  const Topology &T = *st->s.topo;
+  CK(cudaSetDevice(T.device));
+  int rc;
+  if ((rc = download_cap(st->s.cf, T.cap_bytes, cf, (size_t)T.S, T.stream))) return rc;
+  if (excess) {
+    CK(cudaMemcpyAsync(excess, st->s.ex, sizeof(int64_t) * T.n, cudaMemcpyDeviceToHost, T.stream));
+    CK(cudaStreamSynchronize(T.stream));
+  }
+  if ((rc = widen_download_i32(st->s.h, height, (size_t)T.n, T.stream))) return rc;
+  return MFX_OK;
+}
+
+void mfx_state_free(mfx_state *st) { delete st; }
+
+int mfx_saturate_source(mfx_state *st, const mfx_graph *g) {
+  const Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  CK(launch_saturate(g->g, st->s));
+  CK(cudaStreamSynchronize(T.stream));
+  st->s.terminated_known = false;
+  return MFX_OK;
+}
+
+int mfx_mask(const mfx_state *st, int which, uint8_t *out) {
+  const Topology &T = *st->s.topo;
+  CK(cudaSetDevice(T.device));
+  Staged b;
+  CK(cudaMalloc(&b.p, (size_t)T.n));
+  CK(launch_mask(st->s, which, (uint8_t *)b.p));
+  CK(cudaMemcpyAsync(out, b.p, (size_t)T.n, cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  return MFX_OK;
+}
+
+// ---- solver ------------------------------------------------------------------
+static unsigned long long operation_ceiling(long long n, long long m) {
+  // n^2 + n*E + 4 n^2 (n + E) (solver.py:37-44), saturated to 64 bits
+  long double c = (long double)n * n + (long double)n * m + 4.0L * n * n * (long double)(n + m);
+  if (c >= 1.8e19L) return ~0ull;
+  unsigned __int128 x = (unsigned __int128)n * n + (unsigned __int128)n * m +
+                        (unsigned __int128)4 * n * n * (unsigned __int128)(n + m);
+  return (unsigned long long)x;
+}
+
+static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &cfg) {
+  mfx_params d{};
+  if (!p) p = &d;
+  if (p->mode != 0 && p->mode != 1)
+    return fail(MFX_VALUE_ERROR, "mode must be one of ('data', 'topology'), got %d", p->mode);
+  if (p->kernel_cycles < 0)
+    return fail(MFX_VALUE_ERROR, "kernel_cycles must be >= 1 (or 0 for the default)");
+  long long kc = p->kernel_cycles;
+  if (kc == 0) kc = T.n > 0 ? (T.m_original + (long long)T.n - 1) / T.n : 1;
+  if (kc < 1) kc = 1;
+  if (kc > INT_MAX) kc = INT_MAX;
+  cfg.kc = (int)kc;
+  cfg.topology = p->mode;
+  cfg.max_waves = p->max_waves;
+  cfg.timeout_s = p->timeout_s > 0 ? p->timeout_s : 600.0;
+  cfg.blocks_per_sm = p->blocks_per_sm;
+  cfg.ceiling = operation_ceiling(T.n, T.m_original);
+  return MFX_OK;
+}
+
+static void fill_result(const mfx_state *st, mfx_result *r) {
+  const Ctrl &c = *st->host_ctrl;
+  r->flow = c.flow;
+  r->cut = c.cut;
+  r->rounds = (int64_t)c.rounds;
+  r->pushes = (int64_t)c.pushes;
+  r->relabels = (int64_t)c.relabels;
+  r->repairs = (int64_t)c.repairs;
+  r->bfs_levels = (int64_t)c.levels;
+  r->waves = (int64_t)c.waves;
+  r->bytes_alg = (int64_t)c.bytes;
+  r->ns_bfs = (double)c.phase_ns[PH_BFS];
+  r->ns_push = (double)c.phase_ns[PH_PUSH];
+  r->ns_repair = (double)c.phase_ns[PH_REPAIR];
+  r->status = c.status;
+}
+
+static int solve_status(const mfx_state *st, mfx_result *r) {
+  const Ctrl &c = *st->host_ctrl;
+  if (c.status == 6)
+    return fail(MFX_TIMEOUT, "device watchdog expired after %lld rounds", (long long)c.rounds);
+  if (c.status == 3)
+    return fail(MFX_SOLVER_ERROR,
+                "push/relabel count %llu exceeded the termination ceiling %llu; solver state is "
+                "likely corrupt",
+                c.pushes + c.relabels, c.ceiling);
+  if (r->flow != r->cut)
+    return fail(MFX_SOLVER_ERROR, "flow %lld does not match cut capacity %lld", (long long)r->flow,
+                (long long)r->cut);
+  return MFX_OK;
+}
+
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+int mfx_global_relabel(mfx_state *st, const mfx_graph *g, int dynamic_bases, int64_t *reached) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  SolveConfig cfg;
+  cfg.what = WHAT_BFS;
+  cfg.dyn_bases = dynamic_bases ? 1 : 0;
+  cfg.forbidden = dynamic_bases ? st->s.s : -1;
+  CK(launch_solve(g->g, st->s, cfg, nullptr));
+  CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  if (reached) *reached = st->host_ctrl->reached;
+  st->s.terminated_known = false;
+  return MFX_OK;
+}
+
+int mfx_solve_static(const mfx_graph *g, mfx_state *st, const mfx_params *p, mfx_result *r) {
+  Topology &T = *g->g.topo;
+  memset(r, 0, sizeof(*r));
+  if (st->s.s == st->s.t) return fail(MFX_VALUE_ERROR, "source and sink must differ");
+  if (st->s.topo != g->g.topo) return fail(MFX_VALUE_ERROR, "state belongs to another graph");
+  SolveConfig cfg;
+  int rc = resolve_config(T, p, cfg);
+  if (rc) return rc;
+  CK(cudaSetDevice(T.device));
+  cfg.what = WHAT_SOLVE;
+  cfg.dyn_bases = 1;
+  cfg.forbidden = st->s.s;
+  int launches = 0;
+  CK(cudaEventRecord(T.ev[0], T.stream));
+  CK(launch_init_state(g->g, st->s));
+  CK(launch_saturate(g->g, st->s));
+  launches += 1;
+  CK(cudaEventRecord(T.ev[1], T.stream));
+  CK(launch_solve(g->g, st->s, cfg, &launches));
+  CK(cudaEventRecord(T.ev[2], T.stream));
+  CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaEventRecord(T.ev[3], T.stream));
+  CK(cudaEventSynchronize(T.ev[3]));
+  CK(cudaGetLastError());
+  fill_result(st, r);
+  r->ms_update = ev_ms(T.ev[0], T.ev[1]);
+  r->ms_solve = ev_ms(T.ev[1], T.ev[2]);
+  r->ms_total = ev_ms(T.ev[0], T.ev[3]);
+  r->launches = launches;
+  st->s.terminated_known = r->status == 0;
+  return solve_status(st, r);
+}
+
+static int batch_error(const long long *err, int64_t k, const int64_t *h_us, const int64_t *h_vs,
+                       const int64_t *h_caps, const int64_t *d_us, const int64_t *d_vs,
+                       const int64_t *d_caps) {
+  auto get = [&](const int64_t *h, const int64_t *d, long long j) -> long long {
+    if (h) return h[j];
+    long long v = 0;
+    cudaMemcpy(&v, d + j, sizeof(v), cudaMemcpyDeviceToHost);
+    return v;
+  };
+  (void)k;
+  if (err[0] != LLONG_MAX) {
+    long long j = err[0];
+    return fail(MFX_BATCH_ERROR, "update %lld (%lld->%lld): negative capacity %lld", j,
+                get(h_us, d_us, j), get(h_vs, d_vs, j), get(h_caps, d_caps, j));
+  }
+  if (err[1] != LLONG_MAX) {
+    long long j = err[1];
+    return fail(MFX_BATCH_ERROR,
+                "update %lld targets edge %lld->%lld which is not an edge of the original graph",
+                j, get(h_us, d_us, j), get(h_vs, d_vs, j));
+  }
+  if (err[3] != LLONG_MAX) {
+    long long j = err[3];
+    return fail(MFX_BATCH_ERROR, "duplicate update for edge %lld->%lld", get(h_us, d_us, j),
+                get(h_vs, d_vs, j));
+  }
+  if (err[4] != LLONG_MAX) {
+    long long j = err[4];
+    return fail(MFX_VALUE_ERROR,
+                "update %lld (%lld->%lld): capacity %lld overflows the int32 residual storage; "
+                "rebuild the graph with wide capacities",
+                j, get(h_us, d_us, j), get(h_vs, d_vs, j), get(h_caps, d_caps, j));
+  }
+  return MFX_OK;
+}
+
+static int require_terminated(mfx_state *st, const char *what) {
+  if (st->s.terminated_known) return MFX_OK;
+  Topology &T = *st->s.topo;
+  CK(ensure_workspace(T));
+  unsigned long long cnt = 0;
+  CK(launch_count_active(st->s, T.ws.d_red));
+  CK(cudaMemcpyAsync(&cnt, T.ws.d_red, sizeof(cnt), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  if (cnt) return fail(MFX_SOLVER_ERROR, "%s requires a terminated solver state", what);
+  return MFX_OK;
+}
+
+static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *h_us,
+                                const int64_t *h_vs, const int64_t *h_caps, const int64_t *d_us,
+                                const int64_t *d_vs, const int64_t *d_caps, const mfx_params *p,
+                                mfx_result *r) {
+  Topology &T = *g->g.topo;
+  memset(r, 0, sizeof(*r));
+  if (st->s.topo != g->g.topo) return fail(MFX_VALUE_ERROR, "state belongs to another graph");
+  SolveConfig cfg;
+  int rc = resolve_config(T, p, cfg);
+  if (rc) return rc;
+  CK(cudaSetDevice(T.device));
+  if ((rc = require_terminated(st, "solve_dynamic"))) return rc;
+  CK(ensure_batch_capacity(T, k));
+  int launches = 0;
+  CK(cudaEventRecord(T.ev[0], T.stream));
+  if (h_us && k > 0) {  // host batch: stage it (part of the timed end-to-end call)
+    int64_t *d = T.ws.d_batch;
+    CK(cudaMemcpyAsync(d, h_us, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + k, h_vs, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + 2 * k, h_caps, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    d_us = d;
+    d_vs = d + k;
+    d_caps = d + 2 * k;
+  }
+  if (!st->s.excess_consistent) {  // uploaded state: full recompute_excess first
+    CK(launch_recompute_excess(g->g, st->s));
+    ++launches;
+  }
+  CK(launch_batch(g->g, &st->s, k, d_us, d_vs, d_caps, true, true, &launches));
+  CK(launch_saturate(g->g, st->s, T.ws.d_err));
+  ++launches;
+  CK(cudaEventRecord(T.ev[1], T.stream));
+  cfg.what = WHAT_SOLVE;
+  cfg.dyn_bases = 1;
+  cfg.forbidden = st->s.s;
+  cfg.gate = T.ws.d_err;
+  CK(launch_solve(g->g, st->s, cfg, &launches));
+  CK(cudaEventRecord(T.ev[2], T.stream));
+  CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaMemcpyAsync(st->host_err, T.ws.d_err, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
+                     T.stream));
+  CK(cudaEventRecord(T.ev[3], T.stream));
+  CK(cudaEventSynchronize(T.ev[3]));
+  CK(cudaGetLastError());
+  if ((rc = batch_error(st->host_err, k, h_us, h_vs, h_caps, d_us, d_vs, d_caps))) return rc;
+  fill_result(st, r);
+  r->updates = k;
+  r->ms_update = ev_ms(T.ev[0], T.ev[1]);
+  r->ms_solve = ev_ms(T.ev[1], T.ev[2]);
+  r->ms_total = ev_ms(T.ev[0], T.ev[3]);
+  r->launches = launches;
+  st->s.excess_consistent = true;
+  st->s.terminated_known = r->status == 0;
+  return solve_status(st, r);
+}
+
+int mfx_solve_dynamic(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us, const int64_t *vs,
+                      const int64_t *new_caps, const mfx_params *p, mfx_result *r) {
+  return solve_dynamic_common(g, st, k, us, vs, new_caps, nullptr, nullptr, nullptr, p, r);
+}
+
+int mfx_solve_dynamic_device(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *d_us,
+                             const int64_t *d_vs, const int64_t *d_caps, const mfx_params *p,
+                             mfx_result *r) {
+  return solve_dynamic_common(g, st, k, nullptr, nullptr, nullptr, d_us, d_vs, d_caps, p, r);
+}
+
+int mfx_apply_updates(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                      const int64_t *vs, const int64_t *new_caps) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  CK(ensure_batch_capacity(T, k));
+  int64_t *d = T.ws.d_batch;
+  if (k > 0) {
+    CK(cudaMemcpyAsync(d, us, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + k, vs, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + 2 * k, new_caps, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+  }
+  CK(launch_batch(g->g, st ? &st->s : nullptr, k, d, d + k, d + 2 * k, true, false, nullptr));
+  long long err[8];
+  CK(cudaMemcpyAsync(err, T.ws.d_err, sizeof(err), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  int rc = batch_error(err, k, us, vs, new_caps, nullptr, nullptr, nullptr);
+  if (rc) return rc;
+  if (st && k > 0) {
+    // apply_updates alone leaves excess stale until recompute_excess (dynamic.py:114-116)
+    st->s.excess_consistent = false;
+    st->s.terminated_known = false;
+  }
+  return MFX_OK;
+}
+
+int mfx_dynamic_prephase(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                         const int64_t *vs, const int64_t *new_caps) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  int rc;
+  if ((rc = require_terminated(st, "solve_dynamic"))) return rc;
+  CK(ensure_batch_capacity(T, k));
+  int64_t *d = T.ws.d_batch;
+  if (k > 0) {
+    CK(cudaMemcpyAsync(d, us, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + k, vs, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + 2 * k, new_caps, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+  }
+  if (!st->s.excess_consistent) CK(launch_recompute_excess(g->g, st->s));
+  CK(launch_batch(g->g, &st->s, k, d, d + k, d + 2 * k, true, true, nullptr));
+  CK(launch_saturate(g->g, st->s, T.ws.d_err));
+  long long err[8];
+  CK(cudaMemcpyAsync(err, T.ws.d_err, sizeof(err), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  if ((rc = batch_error(err, k, us, vs, new_caps, nullptr, nullptr, nullptr))) return rc;
+  st->s.excess_consistent = true;
+  st->s.terminated_known = false;
+  return MFX_OK;
+}
+
+int mfx_recompute_excess(mfx_state *st, const mfx_graph *g) {
+  const Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  CK(launch_recompute_excess(g->g, st->s));
+  CK(cudaStreamSynchronize(T.stream));
+  return MFX_OK;
+}
+
+int mfx_step(const mfx_graph *g, mfx_state *st, const mfx_params *p, int step, int dynamic_bases,
+             int64_t *active, mfx_result *r) {
+  Topology &T = *g->g.topo;
+  SolveConfig cfg;
+  int rc = resolve_config(T, p, cfg);
+  if (rc) return rc;
+  CK(cudaSetDevice(T.device));
+  cfg.dyn_bases = dynamic_bases ? 1 : 0;
+  cfg.forbidden = st->s.s;
+  cfg.reset_counters = (step & 0x10) != 0;  // first step of an instrumented solve
+  step &= 0xF;
+  if (step == 0) cfg.what = WHAT_BFS;
+  else if (step == 1) cfg.what = WHAT_ROUND;
+  else cfg.what = WHAT_FINAL;
+  int launches = 0;
+  CK(launch_solve(g->g, st->s, cfg, &launches));
+  CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  if (r) {
+    memset(r, 0, sizeof(*r));
+    fill_result(st, r);
+    r->launches = launches;
+  }
+  if (active) *active = st->host_ctrl->active;
+  st->s.terminated_known = false;
+  if (st->host_ctrl->status == 6) return fail(MFX_TIMEOUT, "device watchdog expired");
+  if (st->host_ctrl->status == 3)
+    return fail(MFX_SOLVER_ERROR,
+                "push/relabel count %llu exceeded the termination ceiling %llu; solver state is "
+                "likely corrupt",
+                st->host_ctrl->pushes + st->host_ctrl->relabels, st->host_ctrl->ceiling);
+  if (step == 2) st->s.terminated_known = true;
+  return MFX_OK;
+}
+
+int mfx_certificate(const mfx_state *st, const mfx_graph *g, int64_t *cut, uint8_t *a_mask) {
+  mfx_verify_report rep;
+  int rc;
+  if (cut) {
+    if ((rc = mfx_verify(st, g, &rep))) return rc;
+    *cut = rep.cut_capacity;
+  }
+  if (a_mask) return mfx_mask(st, 2, a_mask);
+  return MFX_OK;
+}
+
+int mfx_verify(const mfx_state *st, const mfx_graph *g, mfx_verify_report *rep) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  Staged b;
+  CK(cudaMalloc(&b.p, sizeof(long long) * 16));
+  CK(launch_verify(g->g, st->s, (long long *)b.p));
+  long long v[16];
+  CK(cudaMemcpyAsync(v, b.p, sizeof(v), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  rep->negative_cf = v[0];
+  rep->pair_violations = v[1];
+  rep->excess_mismatch = v[2];
+  rep->excess_sum = v[3];
+  rep->active_vertices = v[4];
+  rep->unsaturated_ab = v[5];
+  rep->loaded_ba = v[6];
+  rep->cut_capacity = v[7];
+  rep->flow_at_bases = v[8];
+  rep->source_in_b = v[9];
+  rep->sink_in_a = v[10];
+  rep->first_bad_slot = v[11] == LLONG_MAX ? -1 : v[11];
+  return MFX_OK;
+}
+
+int mfx_host_alloc(size_t bytes, void **ptr) {
+  CK(cudaHostAlloc(ptr, bytes ? bytes : 16, cudaHostAllocDefault));
+  return MFX_OK;
+}
+int mfx_host_free(void *ptr) {
+  CK(cudaFreeHost(ptr));
+  return MFX_OK;
+}
+void *mfx_graph_stream(const mfx_graph *g) { return (void *)g->g.topo->stream; }
+
+}  // extern "C"

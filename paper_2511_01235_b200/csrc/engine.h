@@ -1,0 +1,130 @@
+// engine.h -- host-side objects and internal launch entry points of libmfx.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <memory>
+#include <string>
+
+#include "mfx_internal.cuh"
+
+namespace mfx {
+
+constexpr int kFirstNone = 0x7f7f7f7f;  // byte-fill sentinel of Workspace::slot_first
+
+// Workspace for the persistent solve kernel, sized by (n, S); shared by every
+// state that lives on the same topology (calls are serialised per process).
+struct Workspace {
+  int n = 0;
+  int rcap = 0;
+  int *F[2][NBIN] = {};  // BFS frontiers (double buffered), capacity n per bin
+  int *R[NBIN] = {};     // round list (push waves + repair scope), capacity rcap per bin
+  int *bases = nullptr;  // last global relabel's base set, capacity n
+  int *heavy = nullptr;  // heavy rows scratch, capacity n
+  unsigned *mark = nullptr;  // wave stamps, n
+  unsigned *stamp = nullptr; // current wave stamp (1 word)
+  int *slot_first = nullptr; // batch duplicate detection, S (kept at kFirstNone)
+  // batch staging
+  int64_t kcap = 0;
+  int64_t *d_batch = nullptr;  // 3*kcap int64 (us, vs, caps)
+  int *d_slot = nullptr;       // kcap resolved slots
+  int *d_uv = nullptr;         // 2*kcap decomposed (u, v)
+  long long *d_err = nullptr;  // batch error block (8 x int64)
+  unsigned long long *d_red = nullptr;  // reduction scratch (64 x u64)
+  ~Workspace();
+};
+
+struct Topology {
+  int device = 0;
+  int n = 0;
+  int S = 0;
+  int m_original = 0;
+  int64_t diag[3] = {0, 0, 0};
+  int cap_bytes = 4;
+  int *off = nullptr, *adj = nullptr, *rev = nullptr;
+  uint8_t *orig = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  int num_sms = 0;
+  Workspace ws;
+  ~Topology();
+};
+
+struct GraphObj {
+  std::shared_ptr<Topology> topo;
+  void *cap0 = nullptr;  // CapT[S]
+  void *pc = nullptr;    // CapT[S]
+  ~GraphObj();
+};
+
+struct StateObj {
+  std::shared_ptr<Topology> topo;
+  int s = 0, t = 0;
+  void *cf = nullptr;        // CapT[S]
+  long long *ex = nullptr;   // int64[n]
+  int *h = nullptr;          // int32[n]
+  Ctrl *ctrl = nullptr;      // control block
+  bool excess_consistent = true;  // excess == sum_row(cf - cap0) known to hold
+  bool terminated_known = false;  // last op was a completed solve
+  ~StateObj();
+};
+
+// ---- solve kernel front-end (solve.cu) ------------------------------------
+enum What { WHAT_SOLVE = 0, WHAT_BFS = 1, WHAT_ROUND = 2, WHAT_FINAL = 3 };
+
+struct SolveConfig {
+  int what = WHAT_SOLVE;
+  int dyn_bases = 1;   // bases {t} U deficient (else {t})
+  int forbidden = -1;  // vertex never discovered (s in dynamic mode)
+  int kc = 1;
+  int max_waves = 0;
+  int topology = 0;
+  double timeout_s = 600.0;
+  int blocks_per_sm = 0;
+  unsigned long long ceiling = ~0ull;
+  bool reset_counters = true;
+  const long long *gate = nullptr;  // batch error block: skip the solve if the batch failed
+};
+
+cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg, int *launches);
+cudaError_t ensure_workspace(Topology &t);
+cudaError_t ensure_batch_capacity(Topology &t, int64_t k);
+
+// ---- state / batch kernels (state.cu) -------------------------------------
+cudaError_t launch_init_state(const GraphObj &g, StateObj &st);
+// gate: optional batch error block; the kernel is a no-op if the batch failed
+cudaError_t launch_saturate(const GraphObj &g, StateObj &st, const long long *gate = nullptr);
+cudaError_t launch_refresh_pc(const GraphObj &g);
+cudaError_t launch_mask(const StateObj &st, int which, uint8_t *d_out);
+cudaError_t launch_recompute_excess(const GraphObj &g, StateObj &st);
+cudaError_t launch_count_active(const StateObj &st, unsigned long long *d_out);
+// Batch: validate into ws.d_err (no mutation), then apply only if no error.
+// update_excess: move excess at repaired endpoints (fused solve_dynamic path);
+// false mirrors apply_updates alone, which leaves excess to recompute_excess.
+cudaError_t launch_batch(GraphObj &g, StateObj *st, int64_t k, const int64_t *d_us,
+                         const int64_t *d_vs, const int64_t *d_caps, bool apply,
+                         bool update_excess, int *launches);
+cudaError_t launch_edge_indices(const GraphObj &g, int64_t k, const int64_t *d_us,
+                                const int64_t *d_vs, int64_t *d_out);
+cudaError_t launch_verify(const GraphObj &g, const StateObj &st, long long *d_rep);
+cudaError_t launch_convert_cap(const int64_t *src, void *dst, int cap_bytes, int64_t cnt,
+                               cudaStream_t s);
+cudaError_t launch_widen_cap(const void *src, int64_t *dst, int cap_bytes, int64_t cnt,
+                             cudaStream_t s);
+cudaError_t pair_max_int64(const Topology &topo, const int64_t *d_cap0, unsigned long long *d_out);
+
+// ---- builder (build.cu) ---------------------------------------------------
+// Builds the topology and int64 cap0 on the device from device edge arrays.
+// Returns 0 or an error: kind in err[0] (1 n<=0, 2 src range, 3 dst range,
+// 4 negative cap), offending edge index in err[1].
+cudaError_t build_bicsr_device(int64_t n, int64_t m, const int64_t *d_us, const int64_t *d_vs,
+                               const int64_t *d_caps, Topology &topo, int64_t **d_cap0_out,
+                               int64_t err[2], int *launches);
+cudaError_t topology_from_bicsr(int64_t n, int64_t S, const int64_t *d_off, const int64_t *d_adj,
+                                const int64_t *d_rev, const uint8_t *d_orig, Topology &topo);
+cudaError_t download_src(const Topology &topo, int64_t *d_src);
+
+extern thread_local std::string g_last_error;
+void count_launch(int k = 1);
+
+}  // namespace mfx

@@ -1,0 +1,166 @@
+// mfx_internal.cuh -- device data layout, control block and shared device
+// helpers of the B200 max-flow engine.
+//
+// HBM layout (SoA, slot order identical to the reference build_bicsr: slots
+// sorted by (u, v), graph.py:143-171):
+//   topology (shared by graph copies, immutable):
+//     off  int32[n+1]   row offsets
+//     adj  int32[S]     head vertex of each slot
+//     rev  int32[S]     paired reverse slot
+//     orig uint8[S]     slot came from an input edge
+//   capacities (private per graph copy, mutated by batches):
+//     cap0 CapT[S]      capacity (0 on stubs)
+//     pc   CapT[S]      pair capacity cap0[i] + cap0[rev i]; since
+//                       cf[i] + cf[rev i] == pc[i] always (oracle.py:118),
+//                       the BFS reads the reverse residual as pc[i] - cf[i]
+//                       from u's own row instead of gathering cf[rev[i]].
+//   state (per SolverState):
+//     cf   CapT[S]      residual capacities
+//     ex   int64[n]     signed excess
+//     h    int32[n]     heights in [0, n]
+// CapT is int32 when every pair sum fits (the default), else int64.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mfx {
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int NBIN = 4;  // 0: thread/vertex, 1: warp/vertex, 2: CTA/vertex, 3: huge
+constexpr int kBin0Max = 16;
+constexpr int kBin1Max = 1024;
+constexpr int kBin2Max = 65536;
+
+__host__ __device__ inline int bin_of(int deg) {
+  return deg <= kBin0Max ? 0 : deg <= kBin1Max ? 1 : deg <= kBin2Max ? 2 : 3;
+}
+
+// ---- control block (one per state, device memory) ------------------------
+// live[] counters are appended to during a phase; the grid barrier's leader
+// (last arriving CTA) moves them into snap[] before releasing, so every CTA
+// reads identical, stable counts after the barrier.
+enum CtrIdx {
+  C_FNEXT = 0,   // [0..3]  next BFS frontier, per bin
+  C_RNEXT = 4,   // [4..7]  next push wave (round list), per bin
+  C_BASES = 8,   // bases list
+  C_HEAVY = 9,   // heavy rows (finalize)
+  C_NCTR = 16
+};
+
+enum Phase { PH_BFS = 0, PH_PUSH = 1, PH_REPAIR = 2, PH_FINAL = 3, PH_N = 4 };
+
+struct Ctrl {
+  unsigned int bar_count;
+  unsigned int bar_gen;
+  int abort;         // 1 = stop (status says why)
+  int status;        // 0 ok, 3 solver error (ceiling), 6 timeout
+  int live[C_NCTR];
+  int snap[C_NCTR];
+  unsigned long long deadline_ns;
+  unsigned long long last_ns;
+  unsigned long long phase_ns[PH_N];
+  unsigned long long ceiling;  // pushes + relabels bound (operation_ceiling)
+  // counters (flushed per round)
+  unsigned long long pushes, relabels, repairs, rounds, levels, waves;
+  unsigned long long bytes;
+  long long flow, cut;
+  long long active;   // active vertices found by the last global relabel
+  long long reached;  // vertices reached by the last global relabel
+  int overflow;
+  int pad;
+};
+
+// ---- small device helpers -------------------------------------------------
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// L2-coherent loads for arrays mutated during a phase (cf, ex, h): L1 is not
+// coherent and a persistent kernel keeps L1 lines across phases.
+__device__ __forceinline__ int ldcg(const int *p) { return __ldcg(p); }
+__device__ __forceinline__ long long ldcg(const long long *p) { return __ldcg(p); }
+
+__device__ __forceinline__ int atomic_add(int *p, int v) { return atomicAdd(p, v); }
+__device__ __forceinline__ long long atomic_add(long long *p, long long v) {
+  return (long long)atomicAdd((unsigned long long *)p, (unsigned long long)v);
+}
+__device__ __forceinline__ int atomic_exch(int *p, int v) { return atomicExch(p, v); }
+__device__ __forceinline__ long long atomic_exch(long long *p, long long v) {
+  return (long long)atomicExch((unsigned long long *)p, (unsigned long long)v);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-aggregated append of `v` to list `buf` at base + atomicAdd(counter):
+// one atomic per warp per call.  Safe under divergence (uses __activemask).
+__device__ __forceinline__ void warp_append(bool pred, int v, int *counter, int *buf, int base,
+                                            int cap, int *overflow) {
+  unsigned act = __activemask();
+  unsigned b = __ballot_sync(act, pred);
+  if (b == 0) return;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(b) - 1;
+  int pos0 = 0;
+  if (lane == leader) pos0 = atomicAdd(counter, __popc(b));
+  pos0 = __shfl_sync(act, pos0, leader);
+  if (pred) {
+    int p = base + pos0 + __popc(b & lanemask_lt());
+    if (p < cap) buf[p] = v;
+    else *overflow = 1;
+  }
+}
+
+// Per-bin warp-aggregated append (the bin is a function of the vertex degree).
+__device__ __forceinline__ void warp_append_binned(bool pred, int v, int bin, int *counters,
+                                                   int *const *bufs, const int *bases, int cap,
+                                                   int *overflow) {
+  unsigned act = __activemask();
+  if (__ballot_sync(act, pred) == 0) return;
+#pragma unroll
+  for (int b = 0; b < NBIN; ++b) {
+    bool p = pred && bin == b;
+    unsigned m = __ballot_sync(act, p);
+    if (m == 0) continue;
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(m) - 1;
+    int pos0 = 0;
+    if (lane == leader) pos0 = atomicAdd(counters + b, __popc(m));
+    pos0 = __shfl_sync(act, pos0, leader);
+    if (p) {
+      int pos = bases[b] + pos0 + __popc(m & lanemask_lt());
+      if (pos < cap) bufs[b][pos] = v;
+      else *overflow = 1;
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+}  // namespace mfx

@@ -1,0 +1,734 @@
+// solve.cu -- the persistent cooperative push-relabel solve kernel.
+//
+// One launch runs the whole round loop of the reference _push_rounds
+// (solver.py:204-241) on the device:
+//
+//   loop:  global relabel (frontier BFS from the bases, kernels.py:168-215)
+//          -> active set compacted during discovery (state.py:62-67)
+//          -> exit when empty (solver.py:221-222: device-side convergence)
+//          -> push phase: waves of bounded push/relabel (kernels.py:19-67)
+//             over the live active list; a vertex that becomes active during
+//             a wave joins the next wave (excess moves several
+//             hops per global relabel instead of one)
+//          -> repair of steep edges (kernels.py:70-93) over every vertex
+//             processed in the round
+//   finalize: flow = sum of excess over the bases (dynamic.py:141-143),
+//             cut = sum cap0 over A->B slots, A = {h == n} (solver.py:178-184)
+//
+// Work is binned by degree at append time: thread / warp / CTA per vertex,
+// and grid-wide expansion for huge rows (s and t of the grid config have
+// ~2.1 M slots).  Phases are separated by a software grid barrier whose last
+// arriving CTA snapshots the append counters, checks the watchdog and the
+// operation ceiling, so every loop decision is taken on identical values.
+#include <cooperative_groups.h>
+#include <limits.h>
+#include <stdio.h>
+
+#include "engine.h"
+
+namespace mfx {
+
+template <typename CapT>
+struct SolveArgs {
+  int n;
+  int s, t;
+  int forbidden;
+  int dyn_bases;
+  int kc;
+  int max_waves;
+  int topology;
+  int what;
+  int rcap;
+  const int *__restrict__ off;
+  const int *__restrict__ adj;
+  const int *__restrict__ rev;
+  const CapT *__restrict__ cap0;
+  const CapT *__restrict__ pc;
+  CapT *cf;
+  long long *ex;
+  int *h;
+  int *F0[NBIN];
+  int *F1[NBIN];
+  int *R[NBIN];
+  int *bases;
+  int *heavy;
+  unsigned *mark;
+  unsigned *stamp;  // persistent wave stamp shared by all states of the topology
+  Ctrl *ctrl;
+  const long long *gate;  // batch error block (dynamic solves), may be null
+};
+
+// algorithmic bytes per event, CapT-dependent
+template <typename CapT>
+struct Bytes {
+  static constexpr int kVertex = 20;                          // off(2x4) + h 4 + ex 8
+  static constexpr int kSlot = 8 + (int)sizeof(CapT);         // adj + cf + h[v]
+  static constexpr int kBfsSlot = 8 + 2 * (int)sizeof(CapT);  // adj + cf + pc + h[v]
+  static constexpr int kPush = 2 * (int)sizeof(CapT) + 16 + 4;
+  static constexpr int kDisc = 8;
+};
+
+struct Local {
+  unsigned long long pushes = 0, relabels = 0, repairs = 0, bytes = 0;
+};
+
+// ---------------------------------------------------------------------------
+// grid barrier with a leader action
+// ---------------------------------------------------------------------------
+struct Sync {
+  unsigned gen;
+  int *s_snap;  // smem copy of ctrl->snap after the last barrier
+  int *s_abort;
+};
+
+__device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, unsigned acc_mask,
+                                       unsigned clear_mask, int phase) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile Ctrl *vc = c;
+    __threadfence();
+    unsigned prev = atomicAdd(&c->bar_count, 1u);
+    if (prev == gridDim.x - 1) {
+      vc->bar_count = 0;
+      for (int i = 0; i < C_NCTR; ++i) {
+        unsigned bit = 1u << i;
+        if (clear_mask & bit) vc->snap[i] = 0;
+        if (snap_mask & bit) {
+          vc->snap[i] = vc->live[i];
+          vc->live[i] = 0;
+        } else if (acc_mask & bit) {
+          vc->snap[i] = vc->snap[i] + vc->live[i];
+          vc->live[i] = 0;
+        }
+      }
+      unsigned long long now = globaltimer();
+      vc->phase_ns[phase] = vc->phase_ns[phase] + (now - vc->last_ns);
+      vc->last_ns = now;
+      if (!vc->abort) {
+        if (now > vc->deadline_ns) {
+          vc->abort = 1;
+          vc->status = 6;
+        } else if (vc->pushes + vc->relabels > vc->ceiling) {
+          vc->abort = 1;
+          vc->status = 3;
+        }
+      }
+      __threadfence();
+      st_release_u32(&c->bar_gen, sy.gen + 1);
+    } else {
+      unsigned spins = 0;
+      while (ld_acquire_u32(&c->bar_gen) == sy.gen) {
+        __nanosleep(40);
+        if ((++spins & 0xFFFFu) == 0) {
+          // escape hatch: a CTA is stuck far past the watchdog; give up so the
+          // launch terminates instead of hanging the device.
+          if (globaltimer() > vc->deadline_ns + 30ull * 1000000000ull) {
+            vc->abort = 1;
+            vc->status = 6;
+            break;
+          }
+        }
+      }
+    }
+    sy.gen += 1;
+    for (int i = 0; i < C_NCTR; ++i) sy.s_snap[i] = vc->snap[i];
+    *sy.s_abort = vc->abort;
+  }
+  __syncthreads();
+}
+
+// block-wide sum, result valid in thread 0
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T *scratch) {
+  v = warp_sum(v);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  T r = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kWarps; ++i) r += scratch[i];
+  return r;
+}
+
+__device__ void flush_counters(Ctrl *c, Local &lc, unsigned long long *scr) {
+  unsigned long long p = block_sum(lc.pushes, scr);
+  if (threadIdx.x == 0 && p) atomicAdd(&c->pushes, p);
+  unsigned long long r = block_sum(lc.relabels, scr);
+  if (threadIdx.x == 0 && r) atomicAdd(&c->relabels, r);
+  unsigned long long q = block_sum(lc.repairs, scr);
+  if (threadIdx.x == 0 && q) atomicAdd(&c->repairs, q);
+  unsigned long long b = block_sum(lc.bytes, scr);
+  if (threadIdx.x == 0 && b) atomicAdd(&c->bytes, b);
+  lc = Local();
+}
+
+// ---------------------------------------------------------------------------
+// global relabel (kernels.py:168-215) as a level-synchronous frontier BFS
+// ---------------------------------------------------------------------------
+template <typename CapT>
+struct Kern {
+  const SolveArgs<CapT> &a;
+  Sync &sy;
+  Local &lc;
+  int gtid, gthreads, gwarp, gwarps, lane;
+
+  __device__ Kern(const SolveArgs<CapT> &a_, Sync &sy_, Local &lc_) : a(a_), sy(sy_), lc(lc_) {
+    gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    gthreads = gridDim.x * blockDim.x;
+    lane = threadIdx.x & 31;
+    gwarp = gtid >> 5;
+    gwarps = gthreads >> 5;
+  }
+
+  __device__ __forceinline__ int deg(int v) const { return __ldg(a.off + v + 1) - __ldg(a.off + v); }
+
+  // Discovery of v at level L+1 through slot i of frontier vertex u.
+  __device__ __forceinline__ void discover_slot(int i, int L, int *const *Fn, const int *rbase,
+                                                const int *zero) {
+    const int n = a.n;
+    int v = __ldg(a.adj + i);
+    bool disc = false;
+    if (v != a.forbidden && ldcg(a.h + v) == n) {
+      CapT r = __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i));
+      if (r > 0) disc = atomicCAS(a.h + v, n, L + 1) == n;
+    }
+    int b = 0;
+    bool act = false;
+    if (disc) {
+      b = bin_of(deg(v));
+      act = !a.topology && v != a.s && v != a.t && ldcg(a.ex + v) > 0;
+      lc.bytes += Bytes<CapT>::kDisc;
+    }
+    warp_append_binned(disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, n, &a.ctrl->overflow);
+    warp_append_binned(act, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap, &a.ctrl->overflow);
+  }
+
+  // returns the number of BFS levels; the active set is left in R (wave 0)
+  __device__ int bfs() {
+    const int n = a.n;
+    __shared__ int zero[NBIN];
+    __shared__ int rb[NBIN];
+    if (threadIdx.x < NBIN) zero[threadIdx.x] = 0;
+    __syncthreads();
+    // reset + seed bases (kernels.py:184-193); topology mode seeds wave 0
+    for (int v = gtid; v < n; v += gthreads) {
+      bool base = v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0);
+      if (v == a.forbidden) base = false;
+      a.h[v] = base ? 0 : n;
+      int b = base ? bin_of(deg(v)) : 0;
+      warp_append_binned(base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n, &a.ctrl->overflow);
+      warp_append(base, v, a.ctrl->live + C_BASES, a.bases, 0, n, &a.ctrl->overflow);
+      bool topo = a.topology && v != a.s && v != a.t;
+      int tb = topo ? bin_of(deg(v)) : 0;
+      warp_append_binned(topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap,
+                         &a.ctrl->overflow);
+    }
+    lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
+    const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
+    grid_sync(a.ctrl, sy, fmask | (1u << C_BASES), rmask, rmask, PH_BFS);
+    long long reached = 0;
+    int L = 0;
+    for (;;) {
+      int cnt[NBIN];
+      int tot = 0;
+      for (int b = 0; b < NBIN; ++b) {
+        cnt[b] = sy.s_snap[C_FNEXT + b];
+        if (cnt[b] > n) cnt[b] = n;
+        tot += cnt[b];
+      }
+      if (tot == 0 || *sy.s_abort) break;
+      reached += tot;
+      if (threadIdx.x < NBIN) rb[threadIdx.x] = sy.s_snap[C_RNEXT + threadIdx.x];
+      __syncthreads();
+      int *const *Fc = (L & 1) ? a.F1 : a.F0;
+      int *const *Fn = (L & 1) ? a.F0 : a.F1;
+      // bin 0: thread per vertex
+      for (int j = gtid; j < cnt[0]; j += gthreads) {
+        int u = Fc[0][j];
+        int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
+        for (int i = lo; i < hi; ++i) discover_slot(i, L, Fn, rb, zero);
+      }
+      // bin 1: warp per vertex
+      for (int j = gwarp; j < cnt[1]; j += gwarps) {
+        int u = Fc[1][j];
+        int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        if (lane == 0)
+          lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
+        for (int i = lo + lane; i < hi; i += 32) discover_slot(i, L, Fn, rb, zero);
+      }
+      // bin 2: CTA per vertex
+      for (int j = blockIdx.x; j < cnt[2]; j += gridDim.x) {
+        int u = Fc[2][j];
+        int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        if (threadIdx.x == 0)
+          lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) discover_slot(i, L, Fn, rb, zero);
+      }
+      // bin 3: whole grid per vertex
+      for (int j = 0; j < cnt[3]; ++j) {
+        int u = Fc[3][j];
+        int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        if (gtid == 0)
+          lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
+        for (int i = lo + gtid; i < hi; i += gthreads) discover_slot(i, L, Fn, rb, zero);
+      }
+      grid_sync(a.ctrl, sy, fmask, rmask, 0, PH_BFS);
+      ++L;
+    }
+    if (gtid == 0) {
+      a.ctrl->levels += L;
+      a.ctrl->reached = reached;
+    }
+    return L;
+  }
+
+  // -------------------------------------------------------------------------
+  // push phase (kernels.py:19-67) with in-phase re-activation
+  // -------------------------------------------------------------------------
+  // Append v to the next wave once (stamp dedupe).  Single thread.
+  __device__ __forceinline__ void activate_one(int v, unsigned stamp, const int *nbase) {
+    if (atomicMax(a.mark + v, stamp) >= stamp) return;
+    int b = bin_of(deg(v));
+    int p = nbase[b] + atomicAdd(a.ctrl->live + C_RNEXT + b, 1);
+    if (p < a.rcap) a.R[b][p] = v;
+    else a.ctrl->overflow = 1;
+  }
+
+  // Warp-aggregated variant for thread-per-vertex code (divergent callers).
+  __device__ __forceinline__ void activate_agg(bool pred, int v, unsigned stamp, const int *nbase) {
+    int b = 0;
+    if (pred) {
+      pred = atomicMax(a.mark + v, stamp) < stamp;
+      if (pred) b = bin_of(deg(v));
+    }
+    warp_append_binned(pred, v, b, a.ctrl->live + C_RNEXT, a.R, nbase, a.rcap, &a.ctrl->overflow);
+  }
+
+  // Push d along slot i from u to v; returns the previous excess of v.
+  __device__ __forceinline__ long long push_slot(int u, int i, int v, long long d) {
+    atomic_add(a.cf + i, (CapT)(-d));
+    atomic_add(a.cf + __ldg(a.rev + i), (CapT)d);
+    atomic_add(a.ex + u, -d);
+    lc.pushes++;
+    lc.bytes += Bytes<CapT>::kPush;
+    return atomic_add(a.ex + v, d);
+  }
+
+  __device__ void push_thread(int u, unsigned stamp, const int *nbase) {
+    const int n = a.n;
+    int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+    int hu = ldcg(a.h + u);
+    for (int cnt = 0; cnt < a.kc; ++cnt) {
+      long long eu = ldcg(a.ex + u);
+      lc.bytes += Bytes<CapT>::kVertex;
+      if (eu <= 0 || hu >= n) break;
+      int bh = INT_MAX, bi = -1;
+      for (int i = lo; i < hi; ++i) {
+        if (ldcg((const CapT *)(a.cf + i)) > 0) {
+          int hv = ldcg(a.h + __ldg(a.adj + i));
+          if (hv < bh) {
+            bh = hv;
+            bi = i;
+          }
+        }
+      }
+      lc.bytes += (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
+      if (bi < 0) {  // no residual out-edge: nothing can ever leave u
+        hu = n;
+        a.h[u] = n;
+        lc.relabels++;
+        break;
+      }
+      if (hu > bh) {
+        long long c = (long long)ldcg((const CapT *)(a.cf + bi));
+        long long d = eu < c ? eu : c;
+        int v = __ldg(a.adj + bi);
+        long long old = push_slot(u, bi, v, d);
+        activate_agg(old <= 0 && old + d > 0 && v != a.s && v != a.t, v, stamp, nbase);
+      } else {
+        hu = bh + 1 > n ? n : bh + 1;
+        a.h[u] = hu;
+        lc.relabels++;
+      }
+    }
+    activate_agg(hu < n && ldcg(a.ex + u) > 0, u, stamp, nbase);
+  }
+
+  // warp per vertex: lanes scan slots, (height, slot) argmin by shuffle
+  __device__ void push_warp(int u, unsigned stamp, const int *nbase) {
+    const int n = a.n;
+    int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+    int hu = __shfl_sync(0xffffffffu, lane == 0 ? ldcg(a.h + u) : 0, 0);
+    for (int cnt = 0; cnt < a.kc; ++cnt) {
+      long long eu = __shfl_sync(0xffffffffu, lane == 0 ? ldcg(a.ex + u) : 0ll, 0);
+      if (eu <= 0 || hu >= n) break;
+      unsigned long long best = ~0ull;
+      for (int i = lo + lane; i < hi; i += 32) {
+        if (ldcg((const CapT *)(a.cf + i)) > 0) {
+          unsigned long long key =
+              ((unsigned long long)(unsigned)ldcg(a.h + __ldg(a.adj + i)) << 32) | (unsigned)(i - lo);
+          best = key < best ? key : best;
+        }
+      }
+      best = warp_min_u64(best);
+      if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
+      if (best == ~0ull) {
+        hu = n;
+        if (lane == 0) {
+          a.h[u] = n;
+          lc.relabels++;
+        }
+        break;
+      }
+      int bh = (int)(best >> 32);
+      int bi = lo + (int)(best & 0xFFFFFFFFu);
+      if (hu > bh) {
+        if (lane == 0) {
+          long long c = (long long)ldcg((const CapT *)(a.cf + bi));
+          long long d = eu < c ? eu : c;
+          int v = __ldg(a.adj + bi);
+          long long old = push_slot(u, bi, v, d);
+          if (old <= 0 && old + d > 0 && v != a.s && v != a.t) activate_one(v, stamp, nbase);
+        }
+        __syncwarp();
+      } else {
+        hu = bh + 1 > n ? n : bh + 1;
+        if (lane == 0) {
+          a.h[u] = hu;
+          lc.relabels++;
+        }
+      }
+    }
+    if (lane == 0 && hu < n && ldcg(a.ex + u) > 0) activate_one(u, stamp, nbase);
+    __syncwarp();
+  }
+
+  // CTA per vertex
+  __device__ void push_block(int u, unsigned stamp, const int *nbase) {
+    const int n = a.n;
+    __shared__ unsigned long long wbest[kWarps];
+    __shared__ long long s_eu;
+    __shared__ int s_hu;
+    int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+    __syncthreads();
+    if (threadIdx.x == 0) s_hu = ldcg(a.h + u);
+    __syncthreads();
+    int hu = s_hu;
+    for (int cnt = 0; cnt < a.kc; ++cnt) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_eu = ldcg(a.ex + u);
+      __syncthreads();
+      long long eu = s_eu;
+      if (eu <= 0 || hu >= n) break;
+      unsigned long long best = ~0ull;
+      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        if (ldcg((const CapT *)(a.cf + i)) > 0) {
+          unsigned long long key =
+              ((unsigned long long)(unsigned)ldcg(a.h + __ldg(a.adj + i)) << 32) | (unsigned)(i - lo);
+          best = key < best ? key : best;
+        }
+      }
+      best = warp_min_u64(best);
+      if (lane == 0) wbest[threadIdx.x >> 5] = best;
+      __syncthreads();
+      best = ~0ull;
+      for (int w = 0; w < kWarps; ++w) best = wbest[w] < best ? wbest[w] : best;
+      if (threadIdx.x == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
+      if (best == ~0ull) {
+        hu = n;
+        if (threadIdx.x == 0) {
+          a.h[u] = n;
+          lc.relabels++;
+        }
+        break;
+      }
+      int bh = (int)(best >> 32);
+      int bi = lo + (int)(best & 0xFFFFFFFFu);
+      if (hu > bh) {
+        if (threadIdx.x == 0) {
+          long long c = (long long)ldcg((const CapT *)(a.cf + bi));
+          long long d = eu < c ? eu : c;
+          int v = __ldg(a.adj + bi);
+          long long old = push_slot(u, bi, v, d);
+          if (old <= 0 && old + d > 0 && v != a.s && v != a.t) activate_one(v, stamp, nbase);
+        }
+      } else {
+        hu = bh + 1 > n ? n : bh + 1;
+        if (threadIdx.x == 0) {
+          a.h[u] = hu;
+          lc.relabels++;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && hu < n && ldcg(a.ex + u) > 0) activate_one(u, stamp, nbase);
+    __syncthreads();
+  }
+
+  // -------------------------------------------------------------------------
+  // repair (kernels.py:70-93): saturate steep residual edges h(u) > h(v)+1
+  // -------------------------------------------------------------------------
+  __device__ __forceinline__ void repair_slot(int u, int hu, int i) {
+    if (ldcg((const CapT *)(a.cf + i)) > 0) {
+      int v = __ldg(a.adj + i);
+      if (hu > ldcg(a.h + v) + 1) {
+        CapT amt = atomic_exch(a.cf + i, (CapT)0);
+        if (amt > 0) {
+          atomic_add(a.cf + __ldg(a.rev + i), amt);
+          atomic_add(a.ex + u, -(long long)amt);
+          atomic_add(a.ex + v, (long long)amt);
+          lc.repairs++;
+          lc.bytes += Bytes<CapT>::kPush;
+        }
+      }
+    }
+  }
+
+  __device__ void repair(const int *end) {
+    for (int j = gtid; j < end[0]; j += gthreads) {
+      int u = a.R[0][j];
+      int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+      int hu = ldcg(a.h + u);
+      lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
+      for (int i = lo; i < hi; ++i) repair_slot(u, hu, i);
+    }
+    for (int j = gwarp; j < end[1]; j += gwarps) {
+      int u = a.R[1][j];
+      int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+      int hu = ldcg(a.h + u);
+      if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
+      for (int i = lo + lane; i < hi; i += 32) repair_slot(u, hu, i);
+    }
+    for (int b = 2; b < NBIN; ++b) {
+      for (int j = blockIdx.x; j < end[b]; j += gridDim.x) {
+        int u = a.R[b][j];
+        int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        int hu = ldcg(a.h + u);
+        if (threadIdx.x == 0)
+          lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) repair_slot(u, hu, i);
+      }
+    }
+  }
+
+  // one round's push phase + repair; wave 0 = the active list in R
+  __device__ void push_round(unsigned &stamp, unsigned long long *scr) {
+    __shared__ int nbase[NBIN];
+    int base[NBIN], cnt[NBIN];
+    for (int b = 0; b < NBIN; ++b) {
+      base[b] = 0;
+      cnt[b] = sy.s_snap[C_RNEXT + b];
+    }
+    int waves = 0;
+    for (;;) {
+      unsigned next = ++stamp;
+      __syncthreads();
+      if (threadIdx.x < NBIN) nbase[threadIdx.x] = base[threadIdx.x] + cnt[threadIdx.x];
+      __syncthreads();
+      int lim[NBIN];
+      for (int b = 0; b < NBIN; ++b) {
+        lim[b] = base[b] + cnt[b];
+        if (lim[b] > a.rcap) lim[b] = a.rcap;
+      }
+      for (int j = base[0] + gtid; j < lim[0]; j += gthreads) push_thread(a.R[0][j], next, nbase);
+      for (int j = base[1] + gwarp; j < lim[1]; j += gwarps) push_warp(a.R[1][j], next, nbase);
+      for (int b = 2; b < NBIN; ++b)
+        for (int j = base[b] + blockIdx.x; j < lim[b]; j += gridDim.x)
+          push_block(a.R[b][j], next, nbase);
+      flush_counters(a.ctrl, lc, scr);
+      grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_PUSH);
+      ++waves;
+      int tot = 0;
+      for (int b = 0; b < NBIN; ++b) {
+        base[b] = base[b] + cnt[b];
+        cnt[b] = sy.s_snap[C_RNEXT + b];
+        tot += cnt[b];
+      }
+      if (tot == 0 || waves >= a.max_waves || *sy.s_abort) break;
+    }
+    int end[NBIN];
+    for (int b = 0; b < NBIN; ++b) {
+      end[b] = base[b] + cnt[b];
+      if (end[b] > a.rcap) end[b] = a.rcap;
+    }
+    repair(end);
+    flush_counters(a.ctrl, lc, scr);
+    if (gtid == 0) {
+      a.ctrl->waves += waves;
+      a.ctrl->rounds += 1;
+    }
+    // the barrier also clears the wave counters left by the last wave
+    grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_REPAIR);
+  }
+
+  // -------------------------------------------------------------------------
+  // flow (dynamic.py:141-143) and cut certificate (solver.py:178-184)
+  // -------------------------------------------------------------------------
+  __device__ void finalize(long long *scr) {
+    const int n = a.n;
+    long long f = 0;
+    int nb = sy.s_snap[C_BASES];
+    for (int j = gtid; j < nb; j += gthreads) f += ldcg(a.ex + a.bases[j]);
+    f = block_sum(f, scr);
+    if (threadIdx.x == 0 && f) atomicAdd((unsigned long long *)&a.ctrl->flow, (unsigned long long)f);
+    long long c = 0;
+    for (int u = gtid; u < n; u += gthreads) {
+      if (ldcg(a.h + u) != n) continue;
+      int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+      if (hi - lo > 64) {
+        int p = atomicAdd(a.ctrl->live + C_HEAVY, 1);
+        a.heavy[p] = u;
+        continue;
+      }
+      for (int i = lo; i < hi; ++i)
+        if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
+    }
+    grid_sync(a.ctrl, sy, 1u << C_HEAVY, 0, 0, PH_FINAL);
+    int nh = sy.s_snap[C_HEAVY];
+    for (int j = blockIdx.x; j < nh; j += gridDim.x) {
+      int u = a.heavy[j];
+      int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
+        if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
+    }
+    c = block_sum(c, scr);
+    if (threadIdx.x == 0 && c) atomicAdd((unsigned long long *)&a.ctrl->cut, (unsigned long long)c);
+  }
+};
+
+template <typename CapT>
+__global__ void __launch_bounds__(kBlock, 4) solve_kernel(const __grid_constant__ SolveArgs<CapT> a) {
+  __shared__ int s_snap[C_NCTR];
+  __shared__ int s_abort;
+  __shared__ unsigned long long scr[kWarps];
+  if (a.gate && (a.gate[0] != LLONG_MAX || a.gate[1] != LLONG_MAX || a.gate[3] != LLONG_MAX ||
+                 a.gate[4] != LLONG_MAX))
+    return;  // the batch was rejected: state untouched, nothing to solve
+  Sync sy;
+  Local lc;
+  if (threadIdx.x == 0) {
+    volatile Ctrl *vc = a.ctrl;
+    sy.gen = vc->bar_gen;
+    for (int i = 0; i < C_NCTR; ++i) s_snap[i] = vc->snap[i];
+    s_abort = vc->abort;
+  }
+  sy.s_snap = s_snap;
+  sy.s_abort = &s_abort;
+  __syncthreads();
+  Kern<CapT> k(a, sy, lc);
+  unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
+  if (a.what == WHAT_BFS) {
+    k.bfs();
+    if (k.gtid == 0) a.ctrl->active = (long long)(s_snap[C_RNEXT] + s_snap[C_RNEXT + 1] +
+                                                  s_snap[C_RNEXT + 2] + s_snap[C_RNEXT + 3]);
+    flush_counters(a.ctrl, lc, scr);
+    return;
+  }
+  if (a.what == WHAT_ROUND) {
+    k.push_round(stamp, scr);
+    if (k.gtid == 0) *a.stamp = stamp;
+    return;
+  }
+  if (a.what == WHAT_SOLVE) {
+    for (;;) {
+      k.bfs();
+      int act = s_snap[C_RNEXT] + s_snap[C_RNEXT + 1] + s_snap[C_RNEXT + 2] + s_snap[C_RNEXT + 3];
+      if (k.gtid == 0) a.ctrl->active = act;
+      if (act == 0 || s_abort) break;
+      k.push_round(stamp, scr);
+      if (s_abort) break;
+    }
+    if (k.gtid == 0) *a.stamp = stamp;
+    flush_counters(a.ctrl, lc, scr);
+    if (s_abort) return;
+  }
+  k.finalize((long long *)scr);
+}
+
+__global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long ceiling,
+                                  int reset_counters) {
+  unsigned long long now = globaltimer();
+  c->deadline_ns = now + (unsigned long long)(timeout_s * 1e9);
+  c->last_ns = now;
+  c->bar_count = 0;
+  c->abort = 0;
+  c->status = 0;
+  c->overflow = 0;
+  c->ceiling = ceiling;
+  for (int i = 0; i < C_NCTR; ++i) c->live[i] = 0;
+  c->flow = 0;
+  c->cut = 0;
+  if (reset_counters) {
+    for (int i = 0; i < PH_N; ++i) c->phase_ns[i] = 0;
+    c->pushes = c->relabels = c->repairs = c->rounds = c->levels = c->waves = c->bytes = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename CapT>
+static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveConfig &cfg,
+                                  int *launches) {
+  Topology &T = *g.topo;
+  cudaError_t e = ensure_workspace(T);
+  if (e != cudaSuccess) return e;
+  Workspace &W = T.ws;
+  SolveArgs<CapT> a;
+  a.n = T.n;
+  a.s = st.s;
+  a.t = st.t;
+  a.forbidden = cfg.forbidden;
+  a.dyn_bases = cfg.dyn_bases;
+  a.kc = cfg.kc;
+  a.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1 << 30;
+  a.topology = cfg.topology;
+  a.what = cfg.what;
+  a.rcap = W.rcap;
+  a.off = T.off;
+  a.adj = T.adj;
+  a.rev = T.rev;
+  a.cap0 = (const CapT *)g.cap0;
+  a.pc = (const CapT *)g.pc;
+  a.cf = (CapT *)st.cf;
+  a.ex = st.ex;
+  a.h = st.h;
+  for (int b = 0; b < NBIN; ++b) {
+    a.F0[b] = W.F[0][b];
+    a.F1[b] = W.F[1][b];
+    a.R[b] = W.R[b];
+  }
+  a.bases = W.bases;
+  a.heavy = W.heavy;
+  a.mark = W.mark;
+  a.stamp = W.stamp;
+  a.ctrl = st.ctrl;
+  a.gate = cfg.gate;
+
+  ctrl_begin_kernel<<<1, 1, 0, T.stream>>>(st.ctrl, cfg.timeout_s, cfg.ceiling,
+                                          cfg.reset_counters ? 1 : 0);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  static int occ_cache[2] = {0, 0};
+  int &occ = occ_cache[sizeof(CapT) == 8];
+  if (occ == 0) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, solve_kernel<CapT>, kBlock, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  int bps = occ;
+  if (cfg.blocks_per_sm > 0 && cfg.blocks_per_sm < bps) bps = cfg.blocks_per_sm;
+  dim3 grid(T.num_sms * bps), block(kBlock);
+  void *args[] = {(void *)&a};
+  e = cudaLaunchCooperativeKernel((const void *)solve_kernel<CapT>, grid, block, args, 0, T.stream);
+  if (launches) *launches += 2;
+  count_launch(2);
+  return e;
+}
+
+cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg, int *launches) {
+  if (g.topo->cap_bytes == 8) return launch_solve_t<long long>(g, st, cfg, launches);
+  return launch_solve_t<int>(g, st, cfg, launches);
+}
+
+}  // namespace mfx

@@ -1,0 +1,65 @@
+"""CPU-side checks of the C-ABI boundary: libmfx.so loads without a GPU and
+exports every function include/mfx.h declares, and the ctypes signature table
+covers exactly those functions."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mfx.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    names = re.findall(r"\b(mfx_[a-z0-9_]+)\s*\(", text)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2511_01235_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        import __graft_entry__
+        __graft_entry__.build()
+    return _lib.load()
+
+
+def test_header_declares_the_hot_path():
+    names = declared_functions()
+    for must in ("mfx_graph_build", "mfx_solve_static", "mfx_solve_dynamic",
+                 "mfx_global_relabel", "mfx_apply_updates", "mfx_verify"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_ctypes_table_matches_header():
+    from paper_2511_01235_b200 import _lib
+    assert sorted(_lib.SIGNATURES) == declared_functions()
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    from paper_2511_01235_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    arches = set(re.findall(r"sm_\d+a?", out))
+    assert arches == {"sm_100a"}, arches
+
+
+def test_no_cpu_fallback_when_library_missing(tmp_path, monkeypatch):
+    from paper_2511_01235_b200 import _lib
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "absent.so"))
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(_lib.LibraryMissing):
+        _lib.load()
+
+
+def test_version_and_launch_counter(lib):
+    assert lib.mfx_version() == 1
+    assert lib.mfx_launch_count() >= 0
