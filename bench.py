@@ -1,0 +1,452 @@
+"""Benchmark: dynamic max-flow ms per update batch (vs a GPU static re-solve)
+and static max-flow edges/s on config C2 of BASELINE.json (2048x2048
+4-neighbour grid with terminal edges, batches of 10,000 mixed updates).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one chained dynamic batch through solve_dynamic.  ``value`` times K
+steps with the batches already resident in HBM (CUDA events on the engine's
+stream, max over ranks); ``e2e`` times K further chained steps through the
+public Python API from pinned host arrays (H2D of the batch and D2H of the
+result inside the timed region).  ``--impl reference`` runs the unmodified
+reference package (baseline/_ref, numba) on the host cores instead, or the C
+oracle port when the reference is not installed.
+
+N > 1: one process per GPU (torchrun); the grid config does not partition,
+so every rank runs an independent replica ("replicas only").
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dynamic maxflow ms per update batch vs static recompute; static maxflow edges/s"
+CONFIG_NAME = "C2"
+GRID_W = GRID_H = 2048
+BATCH = 10_000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--grid", type=int, default=GRID_W, help="grid side (C2: 2048)")
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=150.0)
+    ap.add_argument("--max-waves", type=int, default=0)
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no e2e / cpu baseline / re-solve legs")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_setup(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+        pg = dist
+    return rank, world, local, pg
+
+
+def barrier(pg, local):
+    if pg is not None:
+        import torch
+        if torch.cuda.is_available():
+            pg.barrier(device_ids=[local])
+        else:
+            pg.barrier()
+
+
+def max_over_ranks(pg, x: float, local: int) -> float:
+    if pg is None:
+        return x
+    import torch
+    dev = f"cuda:{local}" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the
+    timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+                "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+                "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+                "display_clock_setting": 0x100,
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for k, bit in names.items():
+                            if r & bit and k != "gpu_idle":
+                                self.reasons.add(k)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.05)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        busy = [s for s in self.samples if s > 0]
+        return {"sm_mhz": float(statistics.median(busy)) if busy else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per solve-kernel launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_solve_kernel.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def make_instance(side):
+    from paper_2511_01235_b200 import gen
+    us, vs, caps, s, t = gen.grid_graph(side, side, seed=0)
+    return side * side + 2, us, vs, caps, s, t
+
+
+def make_chain(n, el_us, el_vs, el_caps, s, t, count, k, seed0):
+    """`count` chained batches: each drawn from the capacities left by the
+    previous one (fast_batch: reference generate_batch semantics)."""
+    from paper_2511_01235_b200 import gen
+    caps = el_caps.copy()
+    out = []
+    for i in range(count):
+        bu, bv, bc, pick = gen.fast_batch(n, el_us, el_vs, caps, s, t, k, "mixed", seed0 + i)
+        caps[pick] = bc
+        out.append((bu, bv, bc))
+    return out
+
+
+def bench_ours(args, rank, world, local, pg):
+    import torch
+
+    import paper_2511_01235_b200 as mfx
+    from paper_2511_01235_b200 import _lib
+
+    dev = local
+    torch.cuda.set_device(dev)
+    n, us, vs, caps, s, t = make_instance(args.grid)
+    # graph build (not part of the metric, reported)
+    t0 = time.perf_counter()
+    g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps), device=dev)
+    build_s = time.perf_counter() - t0
+    params = mfx.SolverParams(max_waves=args.max_waves)
+    # static solve: warm once, then time
+    res = mfx.solve_static(g, s, t, params)
+    static_runs = []
+    for _ in range(1 if args.profile else 2):
+        res = mfx.solve_static(g, s, t, params)
+        static_runs.append(res.device["ms_total"])
+    static_ms = min(static_runs)
+    static_flow = res.flow_value
+    m_orig = g.m_original
+    st = res.state
+    el = g.to_edge_list()
+    W, K = args.warmup, args.steps
+    chain = make_chain(n, el.us, el.vs, el.caps, s, t, W + 2 * K, args.batch, 1000 * rank)
+    # device-resident batches for the `value` leg
+    dbat = []
+    for bu, bv, bc in chain[:W + K]:
+        dbat.append(tuple(torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev}")
+                          for a in (bu, bv, bc)))
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(_lib.load().mfx_graph_stream(g.handle), device=dev)
+    for i in range(W):
+        bu, bv, bc = dbat[i]
+        mfx.solve_dynamic_device(st, g, bu.numel(), bu.data_ptr(), bv.data_ptr(), bc.data_ptr(), params)
+
+    flows, rounds, solve_ms, bytes_alg, pushes, levels, waves = [], [], [], [], [], [], []
+    launches0 = mfx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        barrier(pg, local)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(W, W + K):
+            bu, bv, bc = dbat[i]
+            r = mfx.solve_dynamic_device(st, g, bu.numel(), bu.data_ptr(), bv.data_ptr(),
+                                         bc.data_ptr(), params)
+            flows.append(r.flow_value)
+            rounds.append(r.rounds)
+            solve_ms.append(r.device["ms_solve"])
+            bytes_alg.append(r.device["bytes_alg"])
+            pushes.append(r.pushes)
+            levels.append(r.device["bfs_levels"])
+            waves.append(r.device["waves"])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(pg, local)
+    launches = mfx.launch_count() - launches0
+    elapsed_ms = ev0.elapsed_time(ev1)
+    elapsed_ms = max_over_ranks(pg, elapsed_ms, local)
+    ms_per_step = elapsed_ms / K
+
+    out = {"elapsed_ms": elapsed_ms, "ms_per_step": ms_per_step, "flows": flows,
+           "rounds": rounds, "solve_ms": solve_ms, "bytes_alg": bytes_alg, "launches": launches,
+           "clocks": clk.summary(), "static_ms": static_ms, "static_flow": static_flow,
+           "m_orig": m_orig, "n": n, "S": g.m, "build_s": build_s, "pushes": pushes,
+           "levels": levels, "waves": waves, "cap_bytes": g.cap_bytes}
+    if args.profile:
+        return out
+
+    # ---- e2e: public API, pinned host batches, H2D + D2H in the timed region
+    pinned = []
+    for bu, bv, bc in chain[W + K:]:
+        hb = [mfx.HostBuffer(bu.size) for _ in range(3)]
+        for h, a in zip(hb, (bu, bv, bc)):
+            h.array[:] = a
+        pinned.append(hb)
+    barrier(pg, local)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_flows = []
+    for hb in pinned:
+        r = mfx.solve_dynamic(st, g, mfx.UpdateBatch(hb[0].array, hb[1].array, hb[2].array), params)
+        e2e_flows.append(r.flow_value)  # D2H of the result struct happened inside the call
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    barrier(pg, local)
+    e2e_ms = max_over_ranks(pg, e2e_ms, local)
+    out["e2e_ms_per_step"] = e2e_ms / K
+    out["e2e_h2d"] = 3 * 8 * args.batch
+    # D2H per call: the device control block (296 B) + the batch error block (64 B)
+    out["e2e_d2h"] = 296 + 64
+    out["e2e_flows"] = e2e_flows
+
+    # ---- GPU static re-solve on the updated capacities (the comparison point)
+    st2 = mfx.init_residuals(g, s, t)
+    rs = []
+    for _ in range(2):
+        rr = mfx.resolve_static(g, st2, params)
+        rs.append(rr.device["ms_total"])
+    out["resolve_ms"] = min(rs)
+    out["resolve_flow"] = rr.flow_value
+    assert rr.flow_value == e2e_flows[-1], (rr.flow_value, e2e_flows[-1])
+    rep = mfx.verify_gpu(st, g, e2e_flows[-1])
+    assert rep.ok, rep.problems
+    out["verified"] = True
+
+    # ---- CPU baseline sample: the C oracle (1 thread), one batch of the same
+    # workload from the GPU's terminated state (rank 0, N = 1 only)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_sample(g, st, s, t, n, chain, args)
+    return out
+
+
+def cpu_sample(g, st, s, t, n, chain, args):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    og = O.OracleGraph(n, g.m, g.offsets.copy(), g.adj.copy(), g.src.copy(), g.rev.copy(),
+                       g.cap0.copy(), g.is_original.copy(), (0, 0, 0))
+    ost = O.OracleState(st.cf.copy(), st.excess.copy(), st.height.copy(), s, t)
+    from paper_2511_01235_b200 import gen
+    el_caps = og.cap0[og.is_original]
+    bu, bv, bc, _ = gen.fast_batch(n, og.src[og.is_original], og.adj[og.is_original], el_caps, s,
+                                   t, args.batch, "mixed", 99991)
+    t0 = time.perf_counter()
+    r = O.solve_dynamic(og, ost, bu, bv, bc)
+    dt = time.perf_counter() - t0
+    return {"value": dt * 1e3, "unit": "ms/batch", "cores": 1, "kind": "port",
+            "sample": f"1 batch of {args.batch} mixed updates on the {args.grid}^2 grid (C oracle, "
+                      f"deterministic schedule) continuing from the GPU's terminated state; "
+                      f"flow {r.flow}, {r.rounds} rounds"}
+
+
+# ---------------------------------------------------------------------------
+def bench_reference(args, rank, world):
+    """Reference arm: the unmodified reference package on the host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    cores = os.cpu_count() or 1
+    try:
+        import dynmaxflow as ref
+        kind = "reference"
+    except Exception:
+        ref = None
+        kind = "port"
+    n, us, vs, caps, s, t = make_instance(args.grid)
+    K = args.steps
+    if ref is not None:
+        params = ref.SolverParams(threads=cores)
+        # warm the numba JIT on a tiny instance (reference bench protocol)
+        tg, ts, tt = ref.random_graph(50, 300, seed=0)
+        ref.solve_static(ref.build_bicsr(tg), ts, tt, params)
+        csr = ref.build_bicsr(ref.EdgeListGraph(n, us, vs, caps))
+        t0 = time.perf_counter()
+        prior = ref.solve_static(csr, s, t, params)
+        static_s = time.perf_counter() - t0
+        el = csr.to_edge_list()
+        chain = make_chain(n, el.us, el.vs, el.caps, s, t, K, args.batch, 0)
+        st, g = prior.state, csr
+        times = []
+        tb = time.perf_counter()
+        for bu, bv, bc in chain:
+            t0 = time.perf_counter()
+            r = ref.solve_dynamic(st, g, ref.UpdateBatch(bu, bv, bc), params)
+            times.append(time.perf_counter() - t0)
+            st, g = r.state, r.graph
+            if time.perf_counter() - tb > args.cpu_budget_s:
+                break
+        m_orig = csr.m_original
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        og = O.build_bicsr(n, us, vs, caps)
+        t0 = time.perf_counter()
+        _, ost = O.solve_static(og, s, t)
+        static_s = time.perf_counter() - t0
+        el_us, el_vs = og.src[og.is_original], og.adj[og.is_original]
+        chain = make_chain(n, el_us, el_vs, og.cap0[og.is_original], s, t, K, args.batch, 0)
+        times = []
+        tb = time.perf_counter()
+        for bu, bv, bc in chain:
+            t0 = time.perf_counter()
+            O.solve_dynamic(og, ost, bu, bv, bc)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() - tb > args.cpu_budget_s:
+                break
+        m_orig = og.m_original
+        cores = 1
+    ms = 1e3 * sum(times) / len(times)
+    sample = (f"{len(times)} chained batches of {args.batch} mixed updates on the "
+              f"{args.grid}^2 grid after a static solve of {static_s:.1f} s "
+              f"(time budget {args.cpu_budget_s:.0f} s)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/batch",
+        "n_gpus": world, "steps": len(times), "warmup": 0, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": config_block(args, world),
+        "static_maxflow_edges_per_s": round(m_orig / static_s, 1), "static_ms": round(1e3 * static_s, 1),
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/batch", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, world):
+    return {"workload": f"C2: {args.grid}x{args.grid} 4-neighbour grid + terminal edge per pixel "
+                        f"(caps U[1,100], seed 0), chained batches of {args.batch} mixed updates "
+                        f"(bias 10)",
+            "graph": f"grid{args.grid}", "batch_updates": args.batch,
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (Bi-CSR + state ~0.8 GB > 126 MB L2)"}
+
+
+def main():
+    args = parse()
+    rank, world, local, pg = dist_setup(args)
+    if args.impl == "reference":
+        if rank == 0:
+            bench_reference(args, rank, world)
+        return
+    out = bench_ours(args, rank, world, local, pg)
+    if rank != 0:
+        return
+    K = args.steps
+    peak, peak_kind = load_peaks()
+    solve_ms_tot = sum(out["solve_ms"])
+    achieved = (sum(out["bytes_alg"]) / 1e9) / (solve_ms_tot / 1e3) if solve_ms_tot > 0 else 0.0
+    traffic = load_traffic()
+    value = out["elapsed_ms"] / (K * world)
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "ms/batch", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(out["ms_per_step"], 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": config_block(args, world),
+        "static_maxflow_edges_per_s": round(out["m_orig"] / (out["static_ms"] / 1e3), 1),
+        "static_ms": round(out["static_ms"], 3),
+        "gpu_static_resolve_ms": round(out.get("resolve_ms", float("nan")), 3),
+        "dynamic_speedup_vs_gpu_static_resolve": (round(out["resolve_ms"] / out["ms_per_step"], 2)
+                                                  if "resolve_ms" in out else None),
+        "flow_static": out["static_flow"], "flows": out["flows"][:3] + ["..."],
+        "rounds_per_batch": round(float(np.mean(out["rounds"])), 2),
+        "gpu_launches": out["launches"],
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_source": peak_kind,
+                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                     "kernel": "mfx::solve_kernel (persistent, one launch per batch)",
+                     "bytes_alg_per_launch": int(np.mean(out["bytes_alg"])),
+                     "kernel_ms_per_launch": round(solve_ms_tot / K, 4)},
+        "clocks": out["clocks"],
+    }
+    if "e2e_ms_per_step" in out:
+        line["e2e"] = {"value": round(out["e2e_ms_per_step"] / world, 4), "unit": "ms/batch",
+                       "h2d_bytes_per_step": out["e2e_h2d"], "d2h_bytes_per_step": out["e2e_d2h"]}
+    if "cpu_baseline" in out:
+        line["cpu_baseline"] = out["cpu_baseline"]
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

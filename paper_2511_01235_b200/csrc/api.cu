@@ -6,6 +6,7 @@
 #include <limits.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -578,7 +579,9 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.kc = (int)kc;
   cfg.topology = p->mode;
   cfg.max_waves = p->max_waves;
-  cfg.timeout_s = p->timeout_s > 0 ? p->timeout_s : 600.0;
+  double tmo = 600.0;
+  if (const char *env = getenv("MFX_TIMEOUT_S")) tmo = atof(env) > 0 ? atof(env) : tmo;
+  cfg.timeout_s = p->timeout_s > 0 ? p->timeout_s : tmo;
   cfg.blocks_per_sm = p->blocks_per_sm;
   cfg.ceiling = operation_ceiling(T.n, T.m_original);
   return MFX_OK;

@@ -45,6 +45,7 @@ enum CtrIdx {
   C_RNEXT = 4,   // [4..7]  next push wave (round list), per bin
   C_BASES = 8,   // bases list
   C_HEAVY = 9,   // heavy rows (finalize)
+  C_ACTIVE = 10, // active vertices discovered by the global relabel
   C_NCTR = 16
 };
 

@@ -197,9 +197,15 @@ struct Kern {
     bool act = false;
     if (disc) {
       b = bin_of(deg(v));
-      act = !a.topology && v != a.s && v != a.t && ldcg(a.ex + v) > 0;
+      act = v != a.s && v != a.t && ldcg(a.ex + v) > 0;
       lc.bytes += Bytes<CapT>::kDisc;
     }
+    {  // count active discoveries (the convergence test, state.py:62-67)
+      unsigned am = __activemask();
+      unsigned bal = __ballot_sync(am, act);
+      if (bal && (threadIdx.x & 31) == __ffs(bal) - 1) atomicAdd(a.ctrl->live + C_ACTIVE, __popc(bal));
+    }
+    if (a.topology) act = false;  // topology mode seeded every vertex already
     warp_append_binned(disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, n, &a.ctrl->overflow);
     warp_append_binned(act, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap, &a.ctrl->overflow);
   }
@@ -226,7 +232,8 @@ struct Kern {
     }
     lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
     const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
-    grid_sync(a.ctrl, sy, fmask | (1u << C_BASES), rmask, rmask, PH_BFS);
+    const unsigned amask = 1u << C_ACTIVE;
+    grid_sync(a.ctrl, sy, fmask | (1u << C_BASES), rmask | amask, rmask | amask, PH_BFS);
     long long reached = 0;
     int L = 0;
     for (;;) {
@@ -274,7 +281,7 @@ struct Kern {
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i = lo + gtid; i < hi; i += gthreads) discover_slot(i, L, Fn, rb, zero);
       }
-      grid_sync(a.ctrl, sy, fmask, rmask, 0, PH_BFS);
+      grid_sync(a.ctrl, sy, fmask, rmask | amask, 0, PH_BFS);
       ++L;
     }
     if (gtid == 0) {
@@ -621,8 +628,7 @@ __global__ void __launch_bounds__(kBlock, 4) solve_kernel(const __grid_constant_
   unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
   if (a.what == WHAT_BFS) {
     k.bfs();
-    if (k.gtid == 0) a.ctrl->active = (long long)(s_snap[C_RNEXT] + s_snap[C_RNEXT + 1] +
-                                                  s_snap[C_RNEXT + 2] + s_snap[C_RNEXT + 3]);
+    if (k.gtid == 0) a.ctrl->active = (long long)s_snap[C_ACTIVE];
     flush_counters(a.ctrl, lc, scr);
     return;
   }
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__(kBlock, 4) solve_kernel(const __grid_constant_
   if (a.what == WHAT_SOLVE) {
     for (;;) {
       k.bfs();
-      int act = s_snap[C_RNEXT] + s_snap[C_RNEXT + 1] + s_snap[C_RNEXT + 2] + s_snap[C_RNEXT + 3];
+      int act = s_snap[C_ACTIVE];
       if (k.gtid == 0) a.ctrl->active = act;
       if (act == 0 || s_abort) break;
       k.push_round(stamp, scr);

@@ -43,7 +43,7 @@ class SolverParams:
     ignored: the device schedule is always massively parallel and the flow
     value does not depend on it.  Device knobs: ``max_waves`` (push waves per
     round before the next global relabel, 0 = until the active list drains),
-    ``timeout_s`` (device watchdog), ``blocks_per_sm`` (persistent grid).
+    ``timeout_s`` (device watchdog; 0 = $MFX_TIMEOUT_S or 600 s), ``blocks_per_sm`` (persistent grid).
     """
 
     kernel_cycles: int = 0
@@ -52,7 +52,7 @@ class SolverParams:
     threads: int = 0
     instrument: Optional[Callable] = None
     max_waves: int = 0
-    timeout_s: float = 600.0
+    timeout_s: float = 0.0
     blocks_per_sm: int = 0
 
     def resolve_threads(self) -> int:

@@ -3,6 +3,9 @@ import sys
 
 import pytest
 
+# fail fast instead of hanging the device if a solve ever stops converging
+os.environ.setdefault("MFX_TIMEOUT_S", "60")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for p in (ROOT, os.path.join(ROOT, "oracle")):
     if p not in sys.path:
