@@ -59,6 +59,8 @@ typedef struct {
     double timeout_s;      /* device watchdog for one solve; 0 -> 600 s            */
     int32_t blocks_per_sm; /* persistent-grid occupancy; 0 -> auto                 */
     int32_t flags;         /* reserved, 0                                          */
+    int32_t wave_mult;     /* auto wave budget = wave_mult * BFS levels + wave_add */
+    int32_t wave_add;      /*   (0, 0 -> 2, 16); used when max_waves == 0          */
 } mfx_params;
 
 /* FlowResult (solver.py:108-118) plus device counters. */

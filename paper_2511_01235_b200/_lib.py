@@ -36,7 +36,8 @@ class GraphInfo(ctypes.Structure):
 
 class Params(ctypes.Structure):
     _fields_ = [("kernel_cycles", i64), ("mode", i32), ("max_waves", i32),
-                ("timeout_s", ctypes.c_double), ("blocks_per_sm", i32), ("flags", i32)]
+                ("timeout_s", ctypes.c_double), ("blocks_per_sm", i32), ("flags", i32),
+                ("wave_mult", i32), ("wave_add", i32)]
 
 
 class Result(ctypes.Structure):

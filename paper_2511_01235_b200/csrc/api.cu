@@ -579,6 +579,10 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.kc = (int)kc;
   cfg.topology = p->mode;
   cfg.max_waves = p->max_waves;
+  if (p->wave_mult > 0 || p->wave_add > 0) {
+    cfg.wave_mult = p->wave_mult;
+    cfg.wave_add = p->wave_add;
+  }
   double tmo = 600.0;
   if (const char *env = getenv("MFX_TIMEOUT_S")) tmo = atof(env) > 0 ? atof(env) : tmo;
   cfg.timeout_s = p->timeout_s > 0 ? p->timeout_s : tmo;

@@ -78,6 +78,8 @@ struct SolveConfig {
   int forbidden = -1;  // vertex never discovered (s in dynamic mode)
   int kc = 1;
   int max_waves = 0;
+  int wave_mult = 2;  // auto wave budget per round: wave_mult * BFS levels + wave_add
+  int wave_add = 16;
   int topology = 0;
   double timeout_s = 600.0;
   int blocks_per_sm = 0;

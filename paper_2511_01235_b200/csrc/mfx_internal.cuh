@@ -69,7 +69,7 @@ struct Ctrl {
   long long active;   // active vertices found by the last global relabel
   long long reached;  // vertices reached by the last global relabel
   int overflow;
-  int pad;
+  int last_levels;  // BFS levels of the last global relabel
 };
 
 // ---- small device helpers -------------------------------------------------

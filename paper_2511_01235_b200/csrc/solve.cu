@@ -35,7 +35,9 @@ struct SolveArgs {
   int forbidden;
   int dyn_bases;
   int kc;
-  int max_waves;
+  int max_waves;  // > 0: fixed waves per round; 0: wave_mult * BFS levels + wave_add
+  int wave_mult;
+  int wave_add;
   int topology;
   int what;
   int rcap;
@@ -286,6 +288,7 @@ struct Kern {
     }
     if (gtid == 0) {
       a.ctrl->levels += L;
+      a.ctrl->last_levels = L;
       a.ctrl->reached = reached;
     }
     return L;
@@ -521,7 +524,7 @@ struct Kern {
   }
 
   // one round's push phase + repair; wave 0 = the active list in R
-  __device__ void push_round(unsigned &stamp, unsigned long long *scr) {
+  __device__ void push_round(unsigned &stamp, unsigned long long *scr, int max_waves) {
     __shared__ int nbase[NBIN];
     int base[NBIN], cnt[NBIN];
     for (int b = 0; b < NBIN; ++b) {
@@ -553,7 +556,7 @@ struct Kern {
         cnt[b] = sy.s_snap[C_RNEXT + b];
         tot += cnt[b];
       }
-      if (tot == 0 || waves >= a.max_waves || *sy.s_abort) break;
+      if (tot == 0 || waves >= max_waves || *sy.s_abort) break;
     }
     int end[NBIN];
     for (int b = 0; b < NBIN; ++b) {
@@ -633,17 +636,17 @@ __global__ void __launch_bounds__(kBlock, 4) solve_kernel(const __grid_constant_
     return;
   }
   if (a.what == WHAT_ROUND) {
-    k.push_round(stamp, scr);
+    k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * (int)((volatile Ctrl *)a.ctrl)->last_levels + a.wave_add);
     if (k.gtid == 0) *a.stamp = stamp;
     return;
   }
   if (a.what == WHAT_SOLVE) {
     for (;;) {
-      k.bfs();
+      int L = k.bfs();
       int act = s_snap[C_ACTIVE];
       if (k.gtid == 0) a.ctrl->active = act;
       if (act == 0 || s_abort) break;
-      k.push_round(stamp, scr);
+      k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
       if (s_abort) break;
     }
     if (k.gtid == 0) *a.stamp = stamp;
@@ -687,7 +690,9 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.forbidden = cfg.forbidden;
   a.dyn_bases = cfg.dyn_bases;
   a.kc = cfg.kc;
-  a.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1 << 30;
+  a.max_waves = cfg.max_waves;
+  a.wave_mult = cfg.wave_mult;
+  a.wave_add = cfg.wave_add;
   a.topology = cfg.topology;
   a.what = cfg.what;
   a.rcap = W.rcap;

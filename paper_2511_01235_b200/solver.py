@@ -54,6 +54,8 @@ class SolverParams:
     max_waves: int = 0
     timeout_s: float = 0.0
     blocks_per_sm: int = 0
+    wave_mult: int = 0
+    wave_add: int = 0
 
     def resolve_threads(self) -> int:
         return 1
@@ -74,7 +76,8 @@ class SolverParams:
         if self.kernel_cycles < 0:
             raise ValueError("kernel_cycles must be >= 1 (or 0 for the default)")
         return L.Params(int(self.kernel_cycles), MODES.index(self.mode), int(self.max_waves),
-                        float(self.timeout_s), int(self.blocks_per_sm), 0)
+                        float(self.timeout_s), int(self.blocks_per_sm), 0,
+                        int(self.wave_mult), int(self.wave_add))
 
 
 @dataclass
