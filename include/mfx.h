@@ -174,6 +174,11 @@ int mfx_certificate(const mfx_state *st, const mfx_graph *g, int64_t *cut, uint8
 /* Device-side constraint checks on the flow of a terminated state. */
 int mfx_verify(const mfx_state *st, const mfx_graph *g, mfx_verify_report *rep);
 
+/* Diagnostics: cost of one software grid barrier of the persistent solve
+ * kernel (iters barriers in one launch, CUDA-event timed). */
+int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_per_sm,
+                      double *ns_per_barrier);
+
 /* ---- host memory helpers (pinned staging for end-to-end timing) -------- */
 int mfx_host_alloc(size_t bytes, void **ptr);
 int mfx_host_free(void *ptr);

@@ -102,6 +102,8 @@ SIGNATURES = {
                                 p_i64, ctypes.POINTER(Result)]),
     "mfx_certificate": (ctypes.c_int, [vp, vp, p_i64, p_u8]),
     "mfx_verify": (ctypes.c_int, [vp, vp, ctypes.POINTER(VerifyReport)]),
+    "mfx_bench_barrier": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_double)]),
     "mfx_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(vp)]),
     "mfx_host_free": (ctypes.c_int, [vp]),
     "mfx_graph_stream": (vp, [vp]),

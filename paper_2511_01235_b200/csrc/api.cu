@@ -66,6 +66,7 @@ Workspace::~Workspace() {
   dfree(heavy);
   dfree(mark);
   dfree(stamp);
+  dfree(vbin);
   dfree(slot_first);
   dfree(d_batch);
   dfree(d_slot);
@@ -123,6 +124,8 @@ cudaError_t ensure_workspace(Topology &t) {
     return e;
   if ((e = cudaMalloc(&w.d_err, sizeof(long long) * 8))) return e;
   if ((e = cudaMalloc(&w.d_red, sizeof(unsigned long long) * 64))) return e;
+  if ((e = cudaMalloc(&w.vbin, n))) return e;
+  if ((e = launch_vbin(t, w.vbin))) return e;
   if ((e = cudaMalloc(&w.mark, sizeof(unsigned) * n))) return e;
   return cudaMemsetAsync(w.mark, 0, sizeof(unsigned) * n, t.stream);
 }
@@ -917,6 +920,23 @@ int mfx_verify(const mfx_state *st, const mfx_graph *g, mfx_verify_report *rep) 
   rep->source_in_b = v[9];
   rep->sink_in_a = v[10];
   rep->first_bad_slot = v[11] == LLONG_MAX ? -1 : v[11];
+  return MFX_OK;
+}
+
+int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_per_sm,
+                      double *ns_per_barrier) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  SolveConfig cfg;
+  cfg.what = WHAT_BARRIER;
+  cfg.kc = iters;
+  cfg.blocks_per_sm = blocks_per_sm;
+  CK(launch_solve(g->g, st->s, cfg, nullptr));  // warm-up
+  CK(cudaEventRecord(T.ev[0], T.stream));
+  CK(launch_solve(g->g, st->s, cfg, nullptr));
+  CK(cudaEventRecord(T.ev[1], T.stream));
+  CK(cudaEventSynchronize(T.ev[1]));
+  *ns_per_barrier = 1e6 * ev_ms(T.ev[0], T.ev[1]) / (iters > 0 ? iters : 1);
   return MFX_OK;
 }
 

@@ -23,6 +23,7 @@ struct Workspace {
   int *heavy = nullptr;  // heavy rows scratch, capacity n
   unsigned *mark = nullptr;  // wave stamps, n
   unsigned *stamp = nullptr; // current wave stamp (1 word)
+  uint8_t *vbin = nullptr;   // degree class per vertex, n
   int *slot_first = nullptr; // batch duplicate detection, S (kept at kFirstNone)
   // batch staging
   int64_t kcap = 0;
@@ -70,7 +71,7 @@ struct StateObj {
 };
 
 // ---- solve kernel front-end (solve.cu) ------------------------------------
-enum What { WHAT_SOLVE = 0, WHAT_BFS = 1, WHAT_ROUND = 2, WHAT_FINAL = 3 };
+enum What { WHAT_SOLVE = 0, WHAT_BFS = 1, WHAT_ROUND = 2, WHAT_FINAL = 3, WHAT_BARRIER = 4 };
 
 struct SolveConfig {
   int what = WHAT_SOLVE;
@@ -94,6 +95,7 @@ cudaError_t ensure_batch_capacity(Topology &t, int64_t k);
 
 // ---- state / batch kernels (state.cu) -------------------------------------
 cudaError_t launch_init_state(const GraphObj &g, StateObj &st);
+cudaError_t launch_vbin(const Topology &t, uint8_t *vbin);
 // gate: optional batch error block; the kernel is a no-op if the batch failed
 cudaError_t launch_saturate(const GraphObj &g, StateObj &st, const long long *gate = nullptr);
 cudaError_t launch_refresh_pc(const GraphObj &g);

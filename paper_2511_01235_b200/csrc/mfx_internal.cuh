@@ -28,7 +28,7 @@ namespace mfx {
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int NBIN = 4;  // 0: thread/vertex, 1: warp/vertex, 2: CTA/vertex, 3: huge
-constexpr int kBin0Max = 16;
+constexpr int kBin0Max = 8;
 constexpr int kBin1Max = 1024;
 constexpr int kBin2Max = 65536;
 

@@ -44,6 +44,7 @@ struct SolveArgs {
   const int *__restrict__ off;
   const int *__restrict__ adj;
   const int *__restrict__ rev;
+  const uint8_t *__restrict__ vbin;  // degree class of every vertex (bin_of(deg))
   const CapT *__restrict__ cap0;
   const CapT *__restrict__ pc;
   CapT *cf;
@@ -183,9 +184,23 @@ struct Kern {
     gwarps = gthreads >> 5;
   }
 
-  __device__ __forceinline__ int deg(int v) const { return __ldg(a.off + v + 1) - __ldg(a.off + v); }
+  __device__ __forceinline__ int vbin(int v) const { return __ldg(a.vbin + v); }
 
-  // Discovery of v at level L+1 through slot i of frontier vertex u.
+  // Appends for a discovery decision: next frontier, active list, active count.
+  __device__ __forceinline__ void discover_post(bool disc, int v, int b, bool act, int *const *Fn,
+                                                const int *rbase, const int *zero) {
+    {  // count active discoveries (the convergence test, state.py:62-67)
+      unsigned am = __activemask();
+      unsigned bal = __ballot_sync(am, act);
+      if (bal && (threadIdx.x & 31) == __ffs(bal) - 1) atomicAdd(a.ctrl->live + C_ACTIVE, __popc(bal));
+    }
+    if (a.topology) act = false;  // topology mode seeded every vertex already
+    warp_append_binned(disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, a.n, &a.ctrl->overflow);
+    warp_append_binned(act, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap, &a.ctrl->overflow);
+  }
+
+  // Discovery of v at level L+1 through slot i of a frontier vertex: the
+  // reverse residual cf[rev i] is read as pc[i] - cf[i] (same row).
   __device__ __forceinline__ void discover_slot(int i, int L, int *const *Fn, const int *rbase,
                                                 const int *zero) {
     const int n = a.n;
@@ -198,18 +213,46 @@ struct Kern {
     int b = 0;
     bool act = false;
     if (disc) {
-      b = bin_of(deg(v));
+      b = vbin(v);
       act = v != a.s && v != a.t && ldcg(a.ex + v) > 0;
       lc.bytes += Bytes<CapT>::kDisc;
     }
-    {  // count active discoveries (the convergence test, state.py:62-67)
-      unsigned am = __activemask();
-      unsigned bal = __ballot_sync(am, act);
-      if (bal && (threadIdx.x & 31) == __ffs(bal) - 1) atomicAdd(a.ctrl->live + C_ACTIVE, __popc(bal));
+    discover_post(disc, v, b, act, Fn, rbase, zero);
+  }
+
+  // Thread-per-vertex expansion for rows of <= kBin0Max slots: every load of
+  // the row is issued before any result is consumed (ILP instead of a
+  // dependent chain per slot).
+  __device__ __forceinline__ void expand_thread(int u, int L, int *const *Fn, const int *rbase,
+                                                const int *zero) {
+    const int n = a.n;
+    int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
+    lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kBfsSlot;
+    int vv[kBin0Max], hv[kBin0Max];
+    CapT rr[kBin0Max];
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) vv[k] = k < d ? __ldg(a.adj + lo + k) : -1;
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k)
+      hv[k] = (k < d && vv[k] != a.forbidden) ? ldcg(a.h + vv[k]) : -1;
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k)
+      rr[k] = hv[k] == n ? __ldg(a.pc + lo + k) - (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
+    bool disc[kBin0Max];
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) disc[k] = rr[k] > 0 && atomicCAS(a.h + vv[k], n, L + 1) == n;
+    int bb[kBin0Max];
+    bool act[kBin0Max];
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) {
+      bb[k] = disc[k] ? vbin(vv[k]) : 0;
+      act[k] = disc[k] && vv[k] != a.s && vv[k] != a.t && ldcg(a.ex + vv[k]) > 0;
     }
-    if (a.topology) act = false;  // topology mode seeded every vertex already
-    warp_append_binned(disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, n, &a.ctrl->overflow);
-    warp_append_binned(act, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap, &a.ctrl->overflow);
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) {
+      if (disc[k]) lc.bytes += Bytes<CapT>::kDisc;
+      discover_post(disc[k], vv[k], bb[k], act[k], Fn, rbase, zero);
+    }
   }
 
   // returns the number of BFS levels; the active set is left in R (wave 0)
@@ -224,11 +267,11 @@ struct Kern {
       bool base = v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0);
       if (v == a.forbidden) base = false;
       a.h[v] = base ? 0 : n;
-      int b = base ? bin_of(deg(v)) : 0;
+      int b = base ? vbin(v) : 0;
       warp_append_binned(base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n, &a.ctrl->overflow);
       warp_append(base, v, a.ctrl->live + C_BASES, a.bases, 0, n, &a.ctrl->overflow);
       bool topo = a.topology && v != a.s && v != a.t;
-      int tb = topo ? bin_of(deg(v)) : 0;
+      int tb = topo ? vbin(v) : 0;
       warp_append_binned(topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap,
                          &a.ctrl->overflow);
     }
@@ -253,12 +296,7 @@ struct Kern {
       int *const *Fc = (L & 1) ? a.F1 : a.F0;
       int *const *Fn = (L & 1) ? a.F0 : a.F1;
       // bin 0: thread per vertex
-      for (int j = gtid; j < cnt[0]; j += gthreads) {
-        int u = Fc[0][j];
-        int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
-        lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i = lo; i < hi; ++i) discover_slot(i, L, Fn, rb, zero);
-      }
+      for (int j = gtid; j < cnt[0]; j += gthreads) expand_thread(Fc[0][j], L, Fn, rb, zero);
       // bin 1: warp per vertex
       for (int j = gwarp; j < cnt[1]; j += gwarps) {
         int u = Fc[1][j];
@@ -300,7 +338,7 @@ struct Kern {
   // Append v to the next wave once (stamp dedupe).  Single thread.
   __device__ __forceinline__ void activate_one(int v, unsigned stamp, const int *nbase) {
     if (atomicMax(a.mark + v, stamp) >= stamp) return;
-    int b = bin_of(deg(v));
+    int b = vbin(v);
     int p = nbase[b] + atomicAdd(a.ctrl->live + C_RNEXT + b, 1);
     if (p < a.rcap) a.R[b][p] = v;
     else a.ctrl->overflow = 1;
@@ -311,7 +349,7 @@ struct Kern {
     int b = 0;
     if (pred) {
       pred = atomicMax(a.mark + v, stamp) < stamp;
-      if (pred) b = bin_of(deg(v));
+      if (pred) b = vbin(v);
     }
     warp_append_binned(pred, v, b, a.ctrl->live + C_RNEXT, a.R, nbase, a.rcap, &a.ctrl->overflow);
   }
@@ -326,39 +364,62 @@ struct Kern {
     return atomic_add(a.ex + v, d);
   }
 
+  // Thread per vertex (rows of <= kBin0Max slots).  The row (head, residual,
+  // head height) is loaded once with all loads in flight, then up to KC
+  // push/relabel steps run on that register snapshot: cf only grows under
+  // concurrent pushes and only this thread lowers it, so snapshot - own
+  // pushes is a safe lower bound; stale neighbour heights are the lock-free
+  // algorithm's tolerated race.
   __device__ void push_thread(int u, unsigned stamp, const int *nbase) {
     const int n = a.n;
-    int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+    int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
     int hu = ldcg(a.h + u);
+    long long eu = ldcg(a.ex + u);
+    lc.bytes += Bytes<CapT>::kVertex;
+    if (eu <= 0 || hu >= n) return;
+    int vv[kBin0Max], hh[kBin0Max];
+    CapT cc[kBin0Max];
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) {
+      vv[k] = k < d ? __ldg(a.adj + lo + k) : 0;
+      cc[k] = k < d ? (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
+    }
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) hh[k] = cc[k] > 0 ? ldcg(a.h + vv[k]) : INT_MAX;
+    lc.bytes += (unsigned long long)d * Bytes<CapT>::kSlot;
     for (int cnt = 0; cnt < a.kc; ++cnt) {
-      long long eu = ldcg(a.ex + u);
-      lc.bytes += Bytes<CapT>::kVertex;
       if (eu <= 0 || hu >= n) break;
-      int bh = INT_MAX, bi = -1;
-      for (int i = lo; i < hi; ++i) {
-        if (ldcg((const CapT *)(a.cf + i)) > 0) {
-          int hv = ldcg(a.h + __ldg(a.adj + i));
-          if (hv < bh) {
-            bh = hv;
-            bi = i;
-          }
+      int bh = INT_MAX, bk = -1;  // first minimum in slot order (kernels.py:40-48)
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k)
+        if (cc[k] > 0 && hh[k] < bh) {
+          bh = hh[k];
+          bk = k;
         }
-      }
-      lc.bytes += (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-      if (bi < 0) {  // no residual out-edge: nothing can ever leave u
+      if (bk < 0) {  // no residual out-edge: nothing can ever leave u
         hu = n;
         a.h[u] = n;
         lc.relabels++;
         break;
       }
       if (hu > bh) {
-        long long c = (long long)ldcg((const CapT *)(a.cf + bi));
-        long long d = eu < c ? eu : c;
-        int v = __ldg(a.adj + bi);
-        long long old = push_slot(u, bi, v, d);
-        activate_agg(old <= 0 && old + d > 0 && v != a.s && v != a.t, v, stamp, nbase);
+        CapT c = 0;
+        int v = 0;
+#pragma unroll
+        for (int k = 0; k < kBin0Max; ++k)
+          if (k == bk) {
+            c = cc[k];
+            v = vv[k];
+          }
+        long long dd = eu < (long long)c ? eu : (long long)c;
+#pragma unroll
+        for (int k = 0; k < kBin0Max; ++k)
+          if (k == bk) cc[k] -= (CapT)dd;
+        eu -= dd;
+        long long old = push_slot(u, lo + bk, v, dd);
+        activate_agg(old <= 0 && old + dd > 0 && v != a.s && v != a.t, v, stamp, nbase);
       } else {
-        hu = bh + 1 > n ? n : bh + 1;
+        hu = bh + 1 > n ? n : bh + 1;  // relabel from the snapshot
         a.h[u] = hu;
         lc.relabels++;
       }
@@ -609,7 +670,10 @@ struct Kern {
 };
 
 template <typename CapT>
-__global__ void __launch_bounds__(kBlock, 4) solve_kernel(const __grid_constant__ SolveArgs<CapT> a) {
+#ifndef MFX_MIN_BLOCKS
+#define MFX_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS) solve_kernel(const __grid_constant__ SolveArgs<CapT> a) {
   __shared__ int s_snap[C_NCTR];
   __shared__ int s_abort;
   __shared__ unsigned long long scr[kWarps];
@@ -628,6 +692,10 @@ __global__ void __launch_bounds__(kBlock, 4) solve_kernel(const __grid_constant_
   sy.s_abort = &s_abort;
   __syncthreads();
   Kern<CapT> k(a, sy, lc);
+  if (a.what == WHAT_BARRIER) {  // barrier latency microbenchmark (kc iterations)
+    for (int i = 0; i < a.kc && !s_abort; ++i) grid_sync(a.ctrl, sy, 0, 0, 0, PH_FINAL);
+    return;
+  }
   unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
   if (a.what == WHAT_BFS) {
     k.bfs();
@@ -699,6 +767,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.off = T.off;
   a.adj = T.adj;
   a.rev = T.rev;
+  a.vbin = W.vbin;
   a.cap0 = (const CapT *)g.cap0;
   a.pc = (const CapT *)g.pc;
   a.cf = (CapT *)st.cf;

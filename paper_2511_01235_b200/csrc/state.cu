@@ -86,6 +86,18 @@ cudaError_t launch_init_state(const GraphObj &g, StateObj &st) {
   return e;
 }
 
+__global__ void vbin_kernel(const int *off, int n, uint8_t *vbin) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    vbin[v] = (uint8_t)bin_of(off[v + 1] - off[v]);
+}
+
+cudaError_t launch_vbin(const Topology &t, uint8_t *vbin) {
+  if (t.n == 0) return cudaSuccess;
+  vbin_kernel<<<grid_for(t.n, t.num_sms), kBlock, 0, t.stream>>>(t.off, t.n, vbin);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 __global__ void mask_kernel(const long long *ex, const int *h, int n, int s, int t, int which,
                             uint8_t *out) {

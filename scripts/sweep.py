@@ -52,12 +52,22 @@ def main():
     ap.add_argument("--batch", type=int, default=10000)
     ap.add_argument("--batches", type=int, default=3)
     ap.add_argument("--knobs", nargs="+", default=[""])
+    ap.add_argument("--barrier", action="store_true")
     args = ap.parse_args()
     n, us, vs, caps, s, t = instance(args.graph, args.side, args.scale)
     t0 = time.perf_counter()
     g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps))
     print(f"# {args.graph} n={n} S={g.m} m_orig={g.m_original} build {time.perf_counter()-t0:.2f}s "
           f"cap_bytes={g.cap_bytes}", flush=True)
+    if args.barrier:
+        import ctypes
+        from paper_2511_01235_b200 import _lib
+        st = mfx.init_residuals(g, s, t)
+        for bps in (1, 2, 3, 4):
+            ns = ctypes.c_double()
+            _lib.check(_lib.load().mfx_bench_barrier(g.handle, st.handle, 20000, bps,
+                                                     ctypes.byref(ns)))
+            print(f"# grid barrier: {bps} CTA/SM -> {ns.value:.0f} ns", flush=True)
     el = g.to_edge_list()
     chain = []
     c = el.caps.copy()
