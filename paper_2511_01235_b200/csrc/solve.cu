@@ -82,50 +82,65 @@ struct Sync {
   unsigned gen;
   int *s_snap;  // smem copy of ctrl->snap after the last barrier
   int *s_abort;
+  unsigned long long deadline, ceiling;  // read once at kernel start
+  unsigned long long t_last;             // block 0: phase timing
+  unsigned long long ph[PH_N];
 };
 
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned *p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Arrival is an acq_rel RMW on the counter (releases this CTA's writes, which
+// bar.sync made visible to thread 0; the last arriver acquires everyone's);
+// the release store of the generation publishes the leader's snapshot.
+// No full fences on the critical path.
 __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, unsigned acc_mask,
                                        unsigned clear_mask, int phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile Ctrl *vc = c;
-    __threadfence();
-    unsigned prev = atomicAdd(&c->bar_count, 1u);
+    unsigned prev = atom_add_acq_rel(&c->bar_count, 1u);
     if (prev == gridDim.x - 1) {
-      vc->bar_count = 0;
+      const unsigned rd = snap_mask | acc_mask;
+      int lv[C_NCTR], sv[C_NCTR];
+#pragma unroll
+      for (int i = 0; i < C_NCTR; ++i) {  // all loads in flight together
+        lv[i] = (rd >> i & 1) ? vc->live[i] : 0;
+        sv[i] = ((acc_mask & ~clear_mask & ~snap_mask) >> i & 1) ? vc->snap[i] : 0;
+      }
+      unsigned long long p = vc->pushes, r = vc->relabels;
+      int ab = vc->abort;
+#pragma unroll
       for (int i = 0; i < C_NCTR; ++i) {
-        unsigned bit = 1u << i;
-        if (clear_mask & bit) vc->snap[i] = 0;
-        if (snap_mask & bit) {
-          vc->snap[i] = vc->live[i];
+        if (rd >> i & 1) {
+          vc->snap[i] = lv[i] + sv[i];
           vc->live[i] = 0;
-        } else if (acc_mask & bit) {
-          vc->snap[i] = vc->snap[i] + vc->live[i];
-          vc->live[i] = 0;
+        } else if (clear_mask >> i & 1) {
+          vc->snap[i] = 0;
         }
       }
-      unsigned long long now = globaltimer();
-      vc->phase_ns[phase] = vc->phase_ns[phase] + (now - vc->last_ns);
-      vc->last_ns = now;
-      if (!vc->abort) {
-        if (now > vc->deadline_ns) {
+      if (!ab) {
+        if (globaltimer() > sy.deadline) {
           vc->abort = 1;
           vc->status = 6;
-        } else if (vc->pushes + vc->relabels > vc->ceiling) {
+        } else if (p + r > sy.ceiling) {
           vc->abort = 1;
           vc->status = 3;
         }
       }
-      __threadfence();
+      vc->bar_count = 0;
       st_release_u32(&c->bar_gen, sy.gen + 1);
     } else {
       unsigned spins = 0;
       while (ld_acquire_u32(&c->bar_gen) == sy.gen) {
-        __nanosleep(40);
+        __nanosleep(20);
         if ((++spins & 0xFFFFu) == 0) {
           // escape hatch: a CTA is stuck far past the watchdog; give up so the
           // launch terminates instead of hanging the device.
-          if (globaltimer() > vc->deadline_ns + 30ull * 1000000000ull) {
+          if (globaltimer() > sy.deadline + 30ull * 1000000000ull) {
             vc->abort = 1;
             vc->status = 6;
             break;
@@ -134,8 +149,18 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
       }
     }
     sy.gen += 1;
-    for (int i = 0; i < C_NCTR; ++i) sy.s_snap[i] = vc->snap[i];
-    *sy.s_abort = vc->abort;
+    int snapv[C_NCTR];
+#pragma unroll
+    for (int i = 0; i < C_NCTR; ++i) snapv[i] = vc->snap[i];
+    int ab = vc->abort;
+#pragma unroll
+    for (int i = 0; i < C_NCTR; ++i) sy.s_snap[i] = snapv[i];
+    *sy.s_abort = ab;
+    if (blockIdx.x == 0) {
+      unsigned long long now = globaltimer();
+      sy.ph[phase] += now - sy.t_last;
+      sy.t_last = now;
+    }
   }
   __syncthreads();
 }
@@ -296,10 +321,10 @@ struct Kern {
       int *const *Fc = (L & 1) ? a.F1 : a.F0;
       int *const *Fn = (L & 1) ? a.F0 : a.F1;
       // bin 0: thread per vertex
-      for (int j = gtid; j < cnt[0]; j += gthreads) expand_thread(Fc[0][j], L, Fn, rb, zero);
+      for (int j = gtid; j < cnt[0]; j += gthreads) expand_thread(ldcg(Fc[0] + j), L, Fn, rb, zero);
       // bin 1: warp per vertex
       for (int j = gwarp; j < cnt[1]; j += gwarps) {
-        int u = Fc[1][j];
+        int u = ldcg(Fc[1] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         if (lane == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
@@ -307,7 +332,7 @@ struct Kern {
       }
       // bin 2: CTA per vertex
       for (int j = blockIdx.x; j < cnt[2]; j += gridDim.x) {
-        int u = Fc[2][j];
+        int u = ldcg(Fc[2] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         if (threadIdx.x == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
@@ -315,7 +340,7 @@ struct Kern {
       }
       // bin 3: whole grid per vertex
       for (int j = 0; j < cnt[3]; ++j) {
-        int u = Fc[3][j];
+        int u = ldcg(Fc[3] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         if (gtid == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
@@ -559,14 +584,14 @@ struct Kern {
 
   __device__ void repair(const int *end) {
     for (int j = gtid; j < end[0]; j += gthreads) {
-      int u = a.R[0][j];
+      int u = ldcg(a.R[0] + j);
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int hu = ldcg(a.h + u);
       lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
       for (int i = lo; i < hi; ++i) repair_slot(u, hu, i);
     }
     for (int j = gwarp; j < end[1]; j += gwarps) {
-      int u = a.R[1][j];
+      int u = ldcg(a.R[1] + j);
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int hu = ldcg(a.h + u);
       if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
@@ -574,7 +599,7 @@ struct Kern {
     }
     for (int b = 2; b < NBIN; ++b) {
       for (int j = blockIdx.x; j < end[b]; j += gridDim.x) {
-        int u = a.R[b][j];
+        int u = ldcg(a.R[b] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         int hu = ldcg(a.h + u);
         if (threadIdx.x == 0)
@@ -603,11 +628,11 @@ struct Kern {
         lim[b] = base[b] + cnt[b];
         if (lim[b] > a.rcap) lim[b] = a.rcap;
       }
-      for (int j = base[0] + gtid; j < lim[0]; j += gthreads) push_thread(a.R[0][j], next, nbase);
-      for (int j = base[1] + gwarp; j < lim[1]; j += gwarps) push_warp(a.R[1][j], next, nbase);
+      for (int j = base[0] + gtid; j < lim[0]; j += gthreads) push_thread(ldcg(a.R[0] + j), next, nbase);
+      for (int j = base[1] + gwarp; j < lim[1]; j += gwarps) push_warp(ldcg(a.R[1] + j), next, nbase);
       for (int b = 2; b < NBIN; ++b)
         for (int j = base[b] + blockIdx.x; j < lim[b]; j += gridDim.x)
-          push_block(a.R[b][j], next, nbase);
+          push_block(ldcg(a.R[b] + j), next, nbase);
       flush_counters(a.ctrl, lc, scr);
       grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_PUSH);
       ++waves;
@@ -641,7 +666,7 @@ struct Kern {
     const int n = a.n;
     long long f = 0;
     int nb = sy.s_snap[C_BASES];
-    for (int j = gtid; j < nb; j += gthreads) f += ldcg(a.ex + a.bases[j]);
+    for (int j = gtid; j < nb; j += gthreads) f += ldcg(a.ex + ldcg(a.bases + j));
     f = block_sum(f, scr);
     if (threadIdx.x == 0 && f) atomicAdd((unsigned long long *)&a.ctrl->flow, (unsigned long long)f);
     long long c = 0;
@@ -659,7 +684,7 @@ struct Kern {
     grid_sync(a.ctrl, sy, 1u << C_HEAVY, 0, 0, PH_FINAL);
     int nh = sy.s_snap[C_HEAVY];
     for (int j = blockIdx.x; j < nh; j += gridDim.x) {
-      int u = a.heavy[j];
+      int u = ldcg(a.heavy + j);
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
         if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
@@ -685,43 +710,50 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS) solve_kernel(const __g
   if (threadIdx.x == 0) {
     volatile Ctrl *vc = a.ctrl;
     sy.gen = vc->bar_gen;
+    sy.deadline = vc->deadline_ns;
+    sy.ceiling = vc->ceiling;
     for (int i = 0; i < C_NCTR; ++i) s_snap[i] = vc->snap[i];
     s_abort = vc->abort;
+    sy.t_last = globaltimer();
+    for (int i = 0; i < PH_N; ++i) sy.ph[i] = 0;
   }
   sy.s_snap = s_snap;
   sy.s_abort = &s_abort;
   __syncthreads();
   Kern<CapT> k(a, sy, lc);
+  unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
   if (a.what == WHAT_BARRIER) {  // barrier latency microbenchmark (kc iterations)
     for (int i = 0; i < a.kc && !s_abort; ++i) grid_sync(a.ctrl, sy, 0, 0, 0, PH_FINAL);
-    return;
-  }
-  unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
-  if (a.what == WHAT_BFS) {
+  } else if (a.what == WHAT_BFS) {
     k.bfs();
     if (k.gtid == 0) a.ctrl->active = (long long)s_snap[C_ACTIVE];
     flush_counters(a.ctrl, lc, scr);
-    return;
-  }
-  if (a.what == WHAT_ROUND) {
-    k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * (int)((volatile Ctrl *)a.ctrl)->last_levels + a.wave_add);
+  } else if (a.what == WHAT_ROUND) {
+    int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
+    k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
     if (k.gtid == 0) *a.stamp = stamp;
-    return;
-  }
-  if (a.what == WHAT_SOLVE) {
-    for (;;) {
-      int L = k.bfs();
-      int act = s_snap[C_ACTIVE];
-      if (k.gtid == 0) a.ctrl->active = act;
-      if (act == 0 || s_abort) break;
-      k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
-      if (s_abort) break;
+  } else {
+    bool final = true;
+    if (a.what == WHAT_SOLVE) {
+      for (;;) {
+        int L = k.bfs();
+        int act = s_snap[C_ACTIVE];
+        if (k.gtid == 0) a.ctrl->active = act;
+        if (act == 0 || s_abort) break;
+        k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
+        if (s_abort) break;
+      }
+      if (k.gtid == 0) *a.stamp = stamp;
+      flush_counters(a.ctrl, lc, scr);
+      final = !s_abort;
     }
-    if (k.gtid == 0) *a.stamp = stamp;
-    flush_counters(a.ctrl, lc, scr);
-    if (s_abort) return;
+    if (final) k.finalize((long long *)scr);
   }
-  k.finalize((long long *)scr);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // device phase times (block 0's view)
+    unsigned long long now = globaltimer();
+    sy.ph[PH_FINAL] += now - sy.t_last;
+    for (int i = 0; i < PH_N; ++i) a.ctrl->phase_ns[i] += sy.ph[i];
+  }
 }
 
 __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long ceiling,
