@@ -255,17 +255,19 @@ struct Kern {
     lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kBfsSlot;
     int vv[kBin0Max], hv[kBin0Max];
     CapT rr[kBin0Max];
+    // round 1: heads and reverse residuals of the whole row (same cache lines)
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) vv[k] = k < d ? __ldg(a.adj + lo + k) : -1;
+    for (int k = 0; k < kBin0Max; ++k) {
+      vv[k] = k < d ? __ldg(a.adj + lo + k) : -1;
+      rr[k] = k < d ? __ldg(a.pc + lo + k) - (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
+    }
+    // round 2: head heights, only across residual slots
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k)
-      hv[k] = (k < d && vv[k] != a.forbidden) ? ldcg(a.h + vv[k]) : -1;
-#pragma unroll
-    for (int k = 0; k < kBin0Max; ++k)
-      rr[k] = hv[k] == n ? __ldg(a.pc + lo + k) - (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
+      hv[k] = (rr[k] > 0 && vv[k] != a.forbidden) ? ldcg(a.h + vv[k]) : -1;
     bool disc[kBin0Max];
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) disc[k] = rr[k] > 0 && atomicCAS(a.h + vv[k], n, L + 1) == n;
+    for (int k = 0; k < kBin0Max; ++k) disc[k] = hv[k] == n && atomicCAS(a.h + vv[k], n, L + 1) == n;
     int bb[kBin0Max];
     bool act[kBin0Max];
 #pragma unroll
@@ -402,16 +404,25 @@ struct Kern {
     long long eu = ldcg(a.ex + u);
     lc.bytes += Bytes<CapT>::kVertex;
     if (eu <= 0 || hu >= n) return;
-    int vv[kBin0Max], hh[kBin0Max];
+    int vv[kBin0Max], hh[kBin0Max], rv[kBin0Max];
     CapT cc[kBin0Max];
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) {
       vv[k] = k < d ? __ldg(a.adj + lo + k) : 0;
+      rv[k] = k < d ? __ldg(a.rev + lo + k) : 0;
       cc[k] = k < d ? (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
     }
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) hh[k] = cc[k] > 0 ? ldcg(a.h + vv[k]) : INT_MAX;
     lc.bytes += (unsigned long long)d * Bytes<CapT>::kSlot;
+    // Each slot is pushed at most once per visit (a push either saturates it
+    // or exhausts u), so the old head excess per slot fits in registers and
+    // the activation tests wait for all atomics together after the loop.
+    long long oldv[kBin0Max];
+    unsigned pushed = 0;
+    long long e_after = eu;  // u's excess after its last push (fresh, from the atomic)
+    bool own_atomic = false;
+    long long own_old = 0, own_d = 0;
     for (int cnt = 0; cnt < a.kc; ++cnt) {
       if (eu <= 0 || hu >= n) break;
       int bh = INT_MAX, bk = -1;  // first minimum in slot order (kernels.py:40-48)
@@ -428,28 +439,35 @@ struct Kern {
         break;
       }
       if (hu > bh) {
-        CapT c = 0;
-        int v = 0;
 #pragma unroll
         for (int k = 0; k < kBin0Max; ++k)
           if (k == bk) {
-            c = cc[k];
-            v = vv[k];
+            long long dd = eu < (long long)cc[k] ? eu : (long long)cc[k];
+            cc[k] -= (CapT)dd;
+            eu -= dd;
+            atomic_add(a.cf + lo + k, (CapT)(-dd));
+            atomic_add(a.cf + rv[k], (CapT)dd);
+            own_old = atomic_add(a.ex + u, -dd);
+            own_d = dd;
+            oldv[k] = atomic_add(a.ex + vv[k], dd);
+            pushed |= 1u << k;
           }
-        long long dd = eu < (long long)c ? eu : (long long)c;
-#pragma unroll
-        for (int k = 0; k < kBin0Max; ++k)
-          if (k == bk) cc[k] -= (CapT)dd;
-        eu -= dd;
-        long long old = push_slot(u, lo + bk, v, dd);
-        activate_agg(old <= 0 && old + dd > 0 && v != a.s && v != a.t, v, stamp, nbase);
+        own_atomic = true;
+        lc.pushes++;
+        lc.bytes += Bytes<CapT>::kPush;
       } else {
         hu = bh + 1 > n ? n : bh + 1;  // relabel from the snapshot
         a.h[u] = hu;
         lc.relabels++;
       }
     }
-    activate_agg(hu < n && ldcg(a.ex + u) > 0, u, stamp, nbase);
+    if (own_atomic) e_after = own_old - own_d;
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) {
+      bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
+      activate_agg(p, vv[k], stamp, nbase);
+    }
+    activate_agg(hu < n && e_after > 0, u, stamp, nbase);
   }
 
   // warp per vertex: lanes scan slots, (height, slot) argmin by shuffle
@@ -583,12 +601,33 @@ struct Kern {
   }
 
   __device__ void repair(const int *end) {
-    for (int j = gtid; j < end[0]; j += gthreads) {
+    for (int j = gtid; j < end[0]; j += gthreads) {  // thread per row, loads batched
       int u = ldcg(a.R[0] + j);
-      int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+      int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
       int hu = ldcg(a.h + u);
-      lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-      for (int i = lo; i < hi; ++i) repair_slot(u, hu, i);
+      lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kSlot;
+      int vv[kBin0Max], hv[kBin0Max];
+      CapT cc[kBin0Max];
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) {
+        vv[k] = k < d ? __ldg(a.adj + lo + k) : 0;
+        cc[k] = k < d ? (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
+      }
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) hv[k] = cc[k] > 0 ? ldcg(a.h + vv[k]) : INT_MAX - 1;
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) {
+        if (cc[k] > 0 && hu > hv[k] + 1) {
+          CapT amt = atomic_exch(a.cf + lo + k, (CapT)0);
+          if (amt > 0) {
+            atomic_add(a.cf + __ldg(a.rev + lo + k), amt);
+            atomic_add(a.ex + u, -(long long)amt);
+            atomic_add(a.ex + vv[k], (long long)amt);
+            lc.repairs++;
+            lc.bytes += Bytes<CapT>::kPush;
+          }
+        }
+      }
     }
     for (int j = gwarp; j < end[1]; j += gwarps) {
       int u = ldcg(a.R[1] + j);
@@ -696,7 +735,7 @@ struct Kern {
 
 template <typename CapT>
 #ifndef MFX_MIN_BLOCKS
-#define MFX_MIN_BLOCKS 3
+#define MFX_MIN_BLOCKS 2
 #endif
 __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS) solve_kernel(const __grid_constant__ SolveArgs<CapT> a) {
   __shared__ int s_snap[C_NCTR];
