@@ -15,18 +15,22 @@
 //   finalize: flow = sum of excess over the bases (dynamic.py:141-143),
 //             cut = sum cap0 over A->B slots, A = {h == n} (solver.py:178-184)
 //
-// Work is binned by degree at append time: thread / warp / CTA per vertex,
-// and grid-wide expansion for huge rows (s and t of the grid config have
-// ~2.1 M slots).  Phases are separated by a software grid barrier whose last
-// arriving CTA snapshots the append counters, checks the watchdog and the
+// Work is binned by degree (vbin): thread / warp / CTA per vertex, and
+// grid-wide expansion for huge rows (s and t of the grid config have ~2.1 M
+// slots).  Every loop that appends to a work list is warp-uniform, so the
+// appends of a warp are staged in shared memory and published 32 at a time
+// with one atomic (the per-list counters are the hottest addresses of the
+// whole solve).  Phases are separated by a software grid barrier whose last
+// arriving CTA snapshots the append counters and checks the watchdog and the
 // operation ceiling, so every loop decision is taken on identical values.
-#include <cooperative_groups.h>
 #include <limits.h>
 #include <stdio.h>
 
 #include "engine.h"
 
 namespace mfx {
+
+constexpr unsigned FULL = 0xffffffffu;
 
 template <typename CapT>
 struct SolveArgs {
@@ -73,6 +77,14 @@ struct Bytes {
 
 struct Local {
   unsigned long long pushes = 0, relabels = 0, repairs = 0, bytes = 0;
+};
+
+// per-warp staging queues in shared memory: q0 = next frontier (bin 0),
+// q1 = next push wave / active list (bin 0)
+constexpr int kWQ = 64;
+struct WarpQ {
+  int cnt[2];
+  int item[2][kWQ];
 };
 
 // ---------------------------------------------------------------------------
@@ -191,49 +203,125 @@ __device__ void flush_counters(Ctrl *c, Local &lc, unsigned long long *scr) {
   lc = Local();
 }
 
-// ---------------------------------------------------------------------------
-// global relabel (kernels.py:168-215) as a level-synchronous frontier BFS
-// ---------------------------------------------------------------------------
+// inclusive warp scan (full warp)
+__device__ __forceinline__ long long warp_incl_scan(long long v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long w = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += w;
+  }
+  return v;
+}
+
 template <typename CapT>
 struct Kern {
   const SolveArgs<CapT> &a;
   Sync &sy;
   Local &lc;
-  int gtid, gthreads, gwarp, gwarps, lane;
+  WarpQ *q;  // this warp's staging queues
+  int gtid, gthreads, gwarp, gwarps, lane, wib;
+  int act_cnt;  // active discoveries counted by this lane in the current level
 
-  __device__ Kern(const SolveArgs<CapT> &a_, Sync &sy_, Local &lc_) : a(a_), sy(sy_), lc(lc_) {
+  __device__ Kern(const SolveArgs<CapT> &a_, Sync &sy_, Local &lc_, WarpQ *wq)
+      : a(a_), sy(sy_), lc(lc_) {
     gtid = blockIdx.x * blockDim.x + threadIdx.x;
     gthreads = gridDim.x * blockDim.x;
     lane = threadIdx.x & 31;
+    wib = threadIdx.x >> 5;
     gwarp = gtid >> 5;
     gwarps = gthreads >> 5;
+    q = wq + wib;
+    act_cnt = 0;
   }
 
   __device__ __forceinline__ int vbin(int v) const { return __ldg(a.vbin + v); }
 
-  // Appends for a discovery decision: next frontier, active list, active count.
-  __device__ __forceinline__ void discover_post(bool disc, int v, int b, bool act, int *const *Fn,
-                                                const int *rbase, const int *zero) {
-    {  // count active discoveries (the convergence test, state.py:62-67)
-      unsigned am = __activemask();
-      unsigned bal = __ballot_sync(am, act);
-      if (bal && (threadIdx.x & 31) == __ffs(bal) - 1) atomicAdd(a.ctrl->live + C_ACTIVE, __popc(bal));
+  // ---- warp-synchronous list appends (every lane of the warp must call) ----
+  __device__ __forceinline__ void stage(int qi, bool pred, int v, int *counter, int *buf, int base,
+                                        int cap) {
+    unsigned b = __ballot_sync(FULL, pred);
+    if (b == 0) return;
+    int c = q->cnt[qi];
+    if (pred) q->item[qi][c + __popc(b & lanemask_lt())] = v;
+    c += __popc(b);
+    __syncwarp();
+    if (c >= 32) {  // publish 32 staged items with one atomic
+      int g = 0;
+      if (lane == 0) g = atomicAdd(counter, 32);
+      g = __shfl_sync(FULL, g, 0);
+      int p = base + g + lane;
+      if (p < cap) buf[p] = q->item[qi][lane];
+      else a.ctrl->overflow = 1;
+      __syncwarp();
+      if (lane < c - 32) q->item[qi][lane] = q->item[qi][lane + 32];
+      c -= 32;
     }
-    if (a.topology) act = false;  // topology mode seeded every vertex already
-    warp_append_binned(disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, a.n, &a.ctrl->overflow);
-    warp_append_binned(act, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap, &a.ctrl->overflow);
+    __syncwarp();
+    if (lane == 0) q->cnt[qi] = c;
+    __syncwarp();
   }
 
-  // Discovery of v at level L+1 through slot i of a frontier vertex: the
-  // reverse residual cf[rev i] is read as pc[i] - cf[i] (same row).
-  __device__ __forceinline__ void discover_slot(int i, int L, int *const *Fn, const int *rbase,
-                                                const int *zero) {
+  __device__ __forceinline__ void stage_flush(int qi, int *counter, int *buf, int base, int cap) {
+    int c = q->cnt[qi];
+    if (c == 0) return;
+    int g = 0;
+    if (lane == 0) g = atomicAdd(counter, c);
+    g = __shfl_sync(FULL, g, 0);
+    if (lane < c) {
+      int p = base + g + lane;
+      if (p < cap) buf[p] = q->item[qi][lane];
+      else a.ctrl->overflow = 1;
+    }
+    __syncwarp();
+    if (lane == 0) q->cnt[qi] = 0;
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ void direct(bool pred, int v, int *counter, int *buf, int base, int cap) {
+    unsigned b = __ballot_sync(FULL, pred);
+    if (b == 0) return;
+    int leader = __ffs(b) - 1;
+    int g = 0;
+    if (lane == leader) g = atomicAdd(counter, __popc(b));
+    g = __shfl_sync(FULL, g, leader);
+    if (pred) {
+      int p = base + g + __popc(b & lanemask_lt());
+      if (p < cap) buf[p] = v;
+      else a.ctrl->overflow = 1;
+    }
+  }
+
+  // bin 0 through the staging queue, bins 1..3 (rare) directly
+  __device__ __forceinline__ void append_binned(int qi, bool pred, int v, int bin, int *counters,
+                                                int *const *bufs, const int *bases, int cap) {
+    stage(qi, pred && bin == 0, v, counters, bufs[0], bases[0], cap);
+    if (__any_sync(FULL, pred && bin != 0)) {
+#pragma unroll
+      for (int b = 1; b < NBIN; ++b)
+        direct(pred && bin == b, v, counters + b, bufs[b], bases[b], cap);
+    }
+  }
+
+  // =========================================================================
+  // global relabel (kernels.py:168-215) as a level-synchronous frontier BFS
+  // =========================================================================
+  __device__ __forceinline__ void discover_post(bool disc, int v, int b, bool act, int *const *Fn,
+                                                const int *rbase, const int *zero) {
+    act_cnt += act;
+    append_binned(0, disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, a.n);
+    append_binned(1, act && !a.topology, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap);
+  }
+
+  // Discovery through slot i (valid lanes only) of a frontier vertex: the
+  // reverse residual cf[rev i] is read as pc[i] - cf[i] from the same row.
+  __device__ __forceinline__ void discover_slot(bool valid, int i, int L, int *const *Fn,
+                                                const int *rbase, const int *zero) {
     const int n = a.n;
-    int v = __ldg(a.adj + i);
+    int v = valid ? __ldg(a.adj + i) : 0;
     bool disc = false;
-    if (v != a.forbidden && ldcg(a.h + v) == n) {
+    if (valid && v != a.forbidden) {
       CapT r = __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i));
-      if (r > 0) disc = atomicCAS(a.h + v, n, L + 1) == n;
+      if (r > 0 && ldcg(a.h + v) == n) disc = atomicCAS(a.h + v, n, L + 1) == n;
     }
     int b = 0;
     bool act = false;
@@ -248,22 +336,24 @@ struct Kern {
   // Thread-per-vertex expansion for rows of <= kBin0Max slots: every load of
   // the row is issued before any result is consumed (ILP instead of a
   // dependent chain per slot).
-  __device__ __forceinline__ void expand_thread(int u, int L, int *const *Fn, const int *rbase,
-                                                const int *zero) {
+  __device__ __forceinline__ void expand_thread(bool valid, int u, int L, int *const *Fn,
+                                                const int *rbase, const int *zero) {
     const int n = a.n;
-    int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
-    lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kBfsSlot;
+    int lo = 0, d = 0;
+    if (valid) {
+      lo = __ldg(a.off + u);
+      d = __ldg(a.off + u + 1) - lo;
+      lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kBfsSlot;
+    }
     int vv[kBin0Max], hv[kBin0Max];
     CapT rr[kBin0Max];
-    // round 1: heads and reverse residuals of the whole row (same cache lines)
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) {
+    for (int k = 0; k < kBin0Max; ++k) {  // heads + reverse residuals of the row
       vv[k] = k < d ? __ldg(a.adj + lo + k) : -1;
       rr[k] = k < d ? __ldg(a.pc + lo + k) - (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
     }
-    // round 2: head heights, only across residual slots
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k)
+    for (int k = 0; k < kBin0Max; ++k)  // head heights across residual slots only
       hv[k] = (rr[k] > 0 && vv[k] != a.forbidden) ? ldcg(a.h + vv[k]) : -1;
     bool disc[kBin0Max];
 #pragma unroll
@@ -282,6 +372,14 @@ struct Kern {
     }
   }
 
+  __device__ void level_flush(int *const *Fn, const int *rbase) {
+    stage_flush(0, a.ctrl->live + C_FNEXT, Fn[0], 0, a.n);
+    stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], rbase[0], a.rcap);
+    int c = warp_sum(act_cnt);
+    if (lane == 0 && c) atomicAdd(a.ctrl->live + C_ACTIVE, c);
+    act_cnt = 0;
+  }
+
   // returns the number of BFS levels; the active set is left in R (wave 0)
   __device__ int bfs() {
     const int n = a.n;
@@ -290,18 +388,20 @@ struct Kern {
     if (threadIdx.x < NBIN) zero[threadIdx.x] = 0;
     __syncthreads();
     // reset + seed bases (kernels.py:184-193); topology mode seeds wave 0
-    for (int v = gtid; v < n; v += gthreads) {
-      bool base = v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0);
+    for (int v0 = gwarp * 32; v0 < n; v0 += gwarps * 32) {
+      int v = v0 + lane;
+      bool valid = v < n;
+      bool base = valid && (v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0));
       if (v == a.forbidden) base = false;
-      a.h[v] = base ? 0 : n;
+      if (valid) a.h[v] = base ? 0 : n;
       int b = base ? vbin(v) : 0;
-      warp_append_binned(base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n, &a.ctrl->overflow);
-      warp_append(base, v, a.ctrl->live + C_BASES, a.bases, 0, n, &a.ctrl->overflow);
-      bool topo = a.topology && v != a.s && v != a.t;
+      append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
+      direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
+      bool topo = valid && a.topology && v != a.s && v != a.t;
       int tb = topo ? vbin(v) : 0;
-      warp_append_binned(topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap,
-                         &a.ctrl->overflow);
+      append_binned(1, topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap);
     }
+    level_flush(a.F0, zero);
     lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
     const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
     const unsigned amask = 1u << C_ACTIVE;
@@ -322,15 +422,19 @@ struct Kern {
       __syncthreads();
       int *const *Fc = (L & 1) ? a.F1 : a.F0;
       int *const *Fn = (L & 1) ? a.F0 : a.F1;
-      // bin 0: thread per vertex
-      for (int j = gtid; j < cnt[0]; j += gthreads) expand_thread(ldcg(Fc[0] + j), L, Fn, rb, zero);
+      // bin 0: thread per vertex (warp-uniform trip count)
+      for (int j0 = gwarp * 32; j0 < cnt[0]; j0 += gwarps * 32) {
+        int j = j0 + lane;
+        bool valid = j < cnt[0];
+        expand_thread(valid, valid ? ldcg(Fc[0] + j) : 0, L, Fn, rb, zero);
+      }
       // bin 1: warp per vertex
       for (int j = gwarp; j < cnt[1]; j += gwarps) {
         int u = ldcg(Fc[1] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         if (lane == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i = lo + lane; i < hi; i += 32) discover_slot(i, L, Fn, rb, zero);
+        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, L, Fn, rb, zero);
       }
       // bin 2: CTA per vertex
       for (int j = blockIdx.x; j < cnt[2]; j += gridDim.x) {
@@ -338,7 +442,10 @@ struct Kern {
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         if (threadIdx.x == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) discover_slot(i, L, Fn, rb, zero);
+        for (int i0 = lo; i0 < hi; i0 += blockDim.x) {
+          int i = i0 + threadIdx.x;
+          discover_slot(i < hi, i, L, Fn, rb, zero);
+        }
       }
       // bin 3: whole grid per vertex
       for (int j = 0; j < cnt[3]; ++j) {
@@ -346,8 +453,12 @@ struct Kern {
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         if (gtid == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i = lo + gtid; i < hi; i += gthreads) discover_slot(i, L, Fn, rb, zero);
+        for (int i0 = lo + gwarp * 32; i0 < hi; i0 += gthreads) {
+          int i = i0 + lane;
+          discover_slot(i < hi, i, L, Fn, rb, zero);
+        }
       }
+      level_flush(Fn, rb);
       grid_sync(a.ctrl, sy, fmask, rmask | amask, 0, PH_BFS);
       ++L;
     }
@@ -359,51 +470,38 @@ struct Kern {
     return L;
   }
 
-  // -------------------------------------------------------------------------
+  // =========================================================================
   // push phase (kernels.py:19-67) with in-phase re-activation
-  // -------------------------------------------------------------------------
-  // Append v to the next wave once (stamp dedupe).  Single thread.
-  __device__ __forceinline__ void activate_one(int v, unsigned stamp, const int *nbase) {
-    if (atomicMax(a.mark + v, stamp) >= stamp) return;
-    int b = vbin(v);
-    int p = nbase[b] + atomicAdd(a.ctrl->live + C_RNEXT + b, 1);
-    if (p < a.rcap) a.R[b][p] = v;
-    else a.ctrl->overflow = 1;
-  }
-
-  // Warp-aggregated variant for thread-per-vertex code (divergent callers).
-  __device__ __forceinline__ void activate_agg(bool pred, int v, unsigned stamp, const int *nbase) {
+  // =========================================================================
+  // Append v to the next wave once (stamp dedupe).  Warp-synchronous.
+  __device__ __forceinline__ void activate(bool pred, int v, unsigned stamp, const int *nbase) {
     int b = 0;
     if (pred) {
       pred = atomicMax(a.mark + v, stamp) < stamp;
       if (pred) b = vbin(v);
     }
-    warp_append_binned(pred, v, b, a.ctrl->live + C_RNEXT, a.R, nbase, a.rcap, &a.ctrl->overflow);
+    append_binned(1, pred, v, b, a.ctrl->live + C_RNEXT, a.R, nbase, a.rcap);
   }
 
-  // Push d along slot i from u to v; returns the previous excess of v.
-  __device__ __forceinline__ long long push_slot(int u, int i, int v, long long d) {
-    atomic_add(a.cf + i, (CapT)(-d));
-    atomic_add(a.cf + __ldg(a.rev + i), (CapT)d);
-    atomic_add(a.ex + u, -d);
-    lc.pushes++;
-    lc.bytes += Bytes<CapT>::kPush;
-    return atomic_add(a.ex + v, d);
-  }
-
-  // Thread per vertex (rows of <= kBin0Max slots).  The row (head, residual,
-  // head height) is loaded once with all loads in flight, then up to KC
-  // push/relabel steps run on that register snapshot: cf only grows under
-  // concurrent pushes and only this thread lowers it, so snapshot - own
-  // pushes is a safe lower bound; stale neighbour heights are the lock-free
-  // algorithm's tolerated race.
-  __device__ void push_thread(int u, unsigned stamp, const int *nbase) {
+  // Thread per vertex (rows of <= kBin0Max slots).  The row (head, reverse
+  // slot, residual, head height) is loaded once with all loads in flight,
+  // then up to KC push/relabel steps run on that register snapshot: cf only
+  // grows under concurrent pushes and only this thread lowers it, so
+  // snapshot - own pushes is a safe lower bound; stale neighbour heights are
+  // the lock-free algorithm's tolerated race.
+  __device__ void push_thread(bool valid, int u, unsigned stamp, const int *nbase) {
     const int n = a.n;
-    int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
-    int hu = ldcg(a.h + u);
-    long long eu = ldcg(a.ex + u);
-    lc.bytes += Bytes<CapT>::kVertex;
-    if (eu <= 0 || hu >= n) return;
+    int lo = 0, d = 0, hu = n;
+    long long eu = 0;
+    if (valid) {
+      lo = __ldg(a.off + u);
+      d = __ldg(a.off + u + 1) - lo;
+      hu = ldcg(a.h + u);
+      eu = ldcg(a.ex + u);
+      lc.bytes += Bytes<CapT>::kVertex;
+    }
+    const bool live = eu > 0 && hu < n;
+    if (!live) d = 0;
     int vv[kBin0Max], hh[kBin0Max], rv[kBin0Max];
     CapT cc[kBin0Max];
 #pragma unroll
@@ -420,170 +518,200 @@ struct Kern {
     // the activation tests wait for all atomics together after the loop.
     long long oldv[kBin0Max];
     unsigned pushed = 0;
-    long long e_after = eu;  // u's excess after its last push (fresh, from the atomic)
+    long long e_after = eu;  // u's excess after its last push (from the atomic)
     bool own_atomic = false;
     long long own_old = 0, own_d = 0;
-    for (int cnt = 0; cnt < a.kc; ++cnt) {
-      if (eu <= 0 || hu >= n) break;
-      int bh = INT_MAX, bk = -1;  // first minimum in slot order (kernels.py:40-48)
-#pragma unroll
-      for (int k = 0; k < kBin0Max; ++k)
-        if (cc[k] > 0 && hh[k] < bh) {
-          bh = hh[k];
-          bk = k;
-        }
-      if (bk < 0) {  // no residual out-edge: nothing can ever leave u
-        hu = n;
-        a.h[u] = n;
-        lc.relabels++;
-        break;
-      }
-      if (hu > bh) {
+    if (live) {
+      for (int cnt = 0; cnt < a.kc; ++cnt) {
+        if (eu <= 0 || hu >= n) break;
+        int bh = INT_MAX, bk = -1;  // first minimum in slot order (kernels.py:40-48)
 #pragma unroll
         for (int k = 0; k < kBin0Max; ++k)
-          if (k == bk) {
-            long long dd = eu < (long long)cc[k] ? eu : (long long)cc[k];
-            cc[k] -= (CapT)dd;
-            eu -= dd;
-            atomic_add(a.cf + lo + k, (CapT)(-dd));
-            atomic_add(a.cf + rv[k], (CapT)dd);
-            own_old = atomic_add(a.ex + u, -dd);
-            own_d = dd;
-            oldv[k] = atomic_add(a.ex + vv[k], dd);
-            pushed |= 1u << k;
+          if (cc[k] > 0 && hh[k] < bh) {
+            bh = hh[k];
+            bk = k;
           }
-        own_atomic = true;
-        lc.pushes++;
-        lc.bytes += Bytes<CapT>::kPush;
-      } else {
-        hu = bh + 1 > n ? n : bh + 1;  // relabel from the snapshot
-        a.h[u] = hu;
-        lc.relabels++;
+        if (bk < 0) {  // no residual out-edge: nothing can ever leave u
+          hu = n;
+          a.h[u] = n;
+          lc.relabels++;
+          break;
+        }
+        if (hu > bh) {
+#pragma unroll
+          for (int k = 0; k < kBin0Max; ++k)
+            if (k == bk) {
+              long long dd = eu < (long long)cc[k] ? eu : (long long)cc[k];
+              cc[k] -= (CapT)dd;
+              eu -= dd;
+              atomic_add(a.cf + lo + k, (CapT)(-dd));
+              atomic_add(a.cf + rv[k], (CapT)dd);
+              own_old = atomic_add(a.ex + u, -dd);
+              own_d = dd;
+              oldv[k] = atomic_add(a.ex + vv[k], dd);
+              pushed |= 1u << k;
+            }
+          own_atomic = true;
+          lc.pushes++;
+          lc.bytes += Bytes<CapT>::kPush;
+        } else {
+          hu = bh + 1 > n ? n : bh + 1;  // relabel from the snapshot
+          a.h[u] = hu;
+          lc.relabels++;
+        }
       }
     }
     if (own_atomic) e_after = own_old - own_d;
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) {
       bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
-      activate_agg(p, vv[k], stamp, nbase);
+      activate(p, vv[k], stamp, nbase);
     }
-    activate_agg(hu < n && e_after > 0, u, stamp, nbase);
+    activate(live && hu < n && e_after > 0, u, stamp, nbase);
   }
 
-  // warp per vertex: lanes scan slots, (height, slot) argmin by shuffle
-  __device__ void push_warp(int u, unsigned stamp, const int *nbase) {
+  // Cooperative push for rows of more than kBin0Max slots, by a group of G
+  // threads (a warp, or the whole CTA).  One scan finds the lowest residual
+  // neighbour height bh (first minimum by slot order, kernels.py:40-48);
+  // the excess is then pushed across every admissible slot at height bh in
+  // slot order (ordered prefix sum of the residuals), which is what
+  // successive KC steps would do while bh stays the minimum, in one pass.
+  template <int G>
+  __device__ void push_coop(int u, unsigned stamp, const int *nbase, long long *s_red) {
     const int n = a.n;
+    const int tid = G == 32 ? lane : threadIdx.x;
     int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
-    int hu = __shfl_sync(0xffffffffu, lane == 0 ? ldcg(a.h + u) : 0, 0);
+    int hu;
+    long long eu;
+    if (G == 32) {
+      hu = __shfl_sync(FULL, lane == 0 ? ldcg(a.h + u) : 0, 0);
+      eu = __shfl_sync(FULL, lane == 0 ? ldcg(a.ex + u) : 0ll, 0);
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_red[0] = ldcg(a.h + u);
+        s_red[1] = ldcg(a.ex + u);
+      }
+      __syncthreads();
+      hu = (int)s_red[0];
+      eu = s_red[1];
+    }
+    bool any_push = false;
+    long long last_old = 0, last_total = 0;
     for (int cnt = 0; cnt < a.kc; ++cnt) {
-      long long eu = __shfl_sync(0xffffffffu, lane == 0 ? ldcg(a.ex + u) : 0ll, 0);
       if (eu <= 0 || hu >= n) break;
+      // ---- pass 1: (height, slot) argmin over residual slots, 4-way ILP
       unsigned long long best = ~0ull;
-      for (int i = lo + lane; i < hi; i += 32) {
-        if (ldcg((const CapT *)(a.cf + i)) > 0) {
-          unsigned long long key =
-              ((unsigned long long)(unsigned)ldcg(a.h + __ldg(a.adj + i)) << 32) | (unsigned)(i - lo);
-          best = key < best ? key : best;
+      for (int i0 = lo + tid; i0 < hi; i0 += 4 * G) {
+        CapT c4[4];
+        int v4[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          int i = i0 + r * G;
+          c4[r] = i < hi ? (CapT)ldcg((const CapT *)(a.cf + i)) : (CapT)0;
+          v4[r] = i < hi ? __ldg(a.adj + i) : 0;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (c4[r] > 0) {
+            unsigned long long key = ((unsigned long long)(unsigned)ldcg(a.h + v4[r]) << 32) |
+                                     (unsigned)(i0 + r * G - lo);
+            best = key < best ? key : best;
+          }
         }
       }
       best = warp_min_u64(best);
-      if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-      if (best == ~0ull) {
+      if (G > 32) {
+        __syncthreads();
+        if (lane == 0) s_red[wib] = (long long)best;
+        __syncthreads();
+        best = ~0ull;
+        for (int w = 0; w < G / 32; ++w) best = (unsigned long long)s_red[w] < best ? (unsigned long long)s_red[w] : best;
+      }
+      if (tid == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
+      if (best == ~0ull) {  // no residual out-edge
         hu = n;
-        if (lane == 0) {
+        if (tid == 0) {
           a.h[u] = n;
           lc.relabels++;
         }
         break;
       }
       int bh = (int)(best >> 32);
-      int bi = lo + (int)(best & 0xFFFFFFFFu);
-      if (hu > bh) {
-        if (lane == 0) {
-          long long c = (long long)ldcg((const CapT *)(a.cf + bi));
-          long long d = eu < c ? eu : c;
-          int v = __ldg(a.adj + bi);
-          long long old = push_slot(u, bi, v, d);
-          if (old <= 0 && old + d > 0 && v != a.s && v != a.t) activate_one(v, stamp, nbase);
-        }
-        __syncwarp();
-      } else {
+      if (hu <= bh) {  // relabel from the scan snapshot
         hu = bh + 1 > n ? n : bh + 1;
-        if (lane == 0) {
+        if (tid == 0) {
           a.h[u] = hu;
           lc.relabels++;
         }
+        continue;
       }
+      // ---- pass 2: push along slots at height bh, ordered by slot
+      int first = lo + (int)(best & 0xFFFFFFFFu);
+      long long carry = 0;  // residual of admissible slots before this chunk
+      for (int i0 = first - ((first - lo) % G); i0 < hi && carry < eu; i0 += G) {
+        int i = i0 + tid;
+        long long c = 0;
+        int v = 0;
+        if (i < hi && i >= first) {
+          c = (long long)ldcg((const CapT *)(a.cf + i));
+          if (c > 0) {
+            v = __ldg(a.adj + i);
+            if (ldcg(a.h + v) != bh) c = 0;
+          }
+        }
+        long long incl = warp_incl_scan(c, lane), tot;
+        if (G > 32) {
+          __syncthreads();
+          if (lane == 31) s_red[wib] = incl;
+          __syncthreads();
+          long long before = 0;
+          tot = 0;
+          for (int w = 0; w < G / 32; ++w) {
+            long long x = s_red[w];
+            if (w < wib) before += x;
+            tot += x;
+          }
+          incl += before;
+        } else {
+          tot = __shfl_sync(FULL, incl, 31);
+        }
+        long long room = eu - carry - (incl - c);
+        long long amt = room <= 0 ? 0 : (room < c ? room : c);
+        bool act = false;
+        if (amt > 0) {
+          atomic_add(a.cf + i, (CapT)(-amt));
+          atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
+          long long old = atomic_add(a.ex + v, amt);
+          act = old <= 0 && v != a.s && v != a.t;
+          lc.pushes++;
+          lc.bytes += Bytes<CapT>::kPush;
+        }
+        activate(act, v, stamp, nbase);
+        carry += tot;
+      }
+      long long moved = carry < eu ? carry : eu;
+      if (tid == 0 && moved > 0) {
+        last_old = atomic_add(a.ex + u, -moved);
+        last_total = moved;
+      }
+      any_push = any_push || moved > 0;
+      eu -= moved;
+      if (G > 32) __syncthreads();
     }
-    if (lane == 0 && hu < n && ldcg(a.ex + u) > 0) activate_one(u, stamp, nbase);
-    __syncwarp();
+    // self re-activation from the fresh value returned by the last atomic
+    bool self = false;
+    if (tid == 0) {
+      long long e_after = any_push ? last_old - last_total : eu;
+      self = hu < n && e_after > 0;
+    }
+    if (G == 32 || wib == 0) activate(self, u, stamp, nbase);
+    if (G > 32) __syncthreads();
   }
 
-  // CTA per vertex
-  __device__ void push_block(int u, unsigned stamp, const int *nbase) {
-    const int n = a.n;
-    __shared__ unsigned long long wbest[kWarps];
-    __shared__ long long s_eu;
-    __shared__ int s_hu;
-    int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
-    __syncthreads();
-    if (threadIdx.x == 0) s_hu = ldcg(a.h + u);
-    __syncthreads();
-    int hu = s_hu;
-    for (int cnt = 0; cnt < a.kc; ++cnt) {
-      __syncthreads();
-      if (threadIdx.x == 0) s_eu = ldcg(a.ex + u);
-      __syncthreads();
-      long long eu = s_eu;
-      if (eu <= 0 || hu >= n) break;
-      unsigned long long best = ~0ull;
-      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        if (ldcg((const CapT *)(a.cf + i)) > 0) {
-          unsigned long long key =
-              ((unsigned long long)(unsigned)ldcg(a.h + __ldg(a.adj + i)) << 32) | (unsigned)(i - lo);
-          best = key < best ? key : best;
-        }
-      }
-      best = warp_min_u64(best);
-      if (lane == 0) wbest[threadIdx.x >> 5] = best;
-      __syncthreads();
-      best = ~0ull;
-      for (int w = 0; w < kWarps; ++w) best = wbest[w] < best ? wbest[w] : best;
-      if (threadIdx.x == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-      if (best == ~0ull) {
-        hu = n;
-        if (threadIdx.x == 0) {
-          a.h[u] = n;
-          lc.relabels++;
-        }
-        break;
-      }
-      int bh = (int)(best >> 32);
-      int bi = lo + (int)(best & 0xFFFFFFFFu);
-      if (hu > bh) {
-        if (threadIdx.x == 0) {
-          long long c = (long long)ldcg((const CapT *)(a.cf + bi));
-          long long d = eu < c ? eu : c;
-          int v = __ldg(a.adj + bi);
-          long long old = push_slot(u, bi, v, d);
-          if (old <= 0 && old + d > 0 && v != a.s && v != a.t) activate_one(v, stamp, nbase);
-        }
-      } else {
-        hu = bh + 1 > n ? n : bh + 1;
-        if (threadIdx.x == 0) {
-          a.h[u] = hu;
-          lc.relabels++;
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && hu < n && ldcg(a.ex + u) > 0) activate_one(u, stamp, nbase);
-    __syncthreads();
-  }
-
-  // -------------------------------------------------------------------------
+  // =========================================================================
   // repair (kernels.py:70-93): saturate steep residual edges h(u) > h(v)+1
-  // -------------------------------------------------------------------------
+  // =========================================================================
   __device__ __forceinline__ void repair_slot(int u, int hu, int i) {
     if (ldcg((const CapT *)(a.cf + i)) > 0) {
       int v = __ldg(a.adj + i);
@@ -651,6 +779,7 @@ struct Kern {
   // one round's push phase + repair; wave 0 = the active list in R
   __device__ void push_round(unsigned &stamp, unsigned long long *scr, int max_waves) {
     __shared__ int nbase[NBIN];
+    __shared__ long long s_red[kWarps + 2];
     int base[NBIN], cnt[NBIN];
     for (int b = 0; b < NBIN; ++b) {
       base[b] = 0;
@@ -667,11 +796,16 @@ struct Kern {
         lim[b] = base[b] + cnt[b];
         if (lim[b] > a.rcap) lim[b] = a.rcap;
       }
-      for (int j = base[0] + gtid; j < lim[0]; j += gthreads) push_thread(ldcg(a.R[0] + j), next, nbase);
-      for (int j = base[1] + gwarp; j < lim[1]; j += gwarps) push_warp(ldcg(a.R[1] + j), next, nbase);
+      for (int j0 = base[0] + gwarp * 32; j0 < lim[0]; j0 += gwarps * 32) {
+        int j = j0 + lane;
+        bool valid = j < lim[0];
+        push_thread(valid, valid ? ldcg(a.R[0] + j) : 0, next, nbase);
+      }
+      for (int j = base[1] + gwarp; j < lim[1]; j += gwarps) push_coop<32>(ldcg(a.R[1] + j), next, nbase, s_red);
       for (int b = 2; b < NBIN; ++b)
         for (int j = base[b] + blockIdx.x; j < lim[b]; j += gridDim.x)
-          push_block(ldcg(a.R[b] + j), next, nbase);
+          push_coop<kBlock>(ldcg(a.R[b] + j), next, nbase, s_red);
+      stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
       flush_counters(a.ctrl, lc, scr);
       grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_PUSH);
       ++waves;
@@ -698,9 +832,9 @@ struct Kern {
     grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_REPAIR);
   }
 
-  // -------------------------------------------------------------------------
+  // =========================================================================
   // flow (dynamic.py:141-143) and cut certificate (solver.py:178-184)
-  // -------------------------------------------------------------------------
+  // =========================================================================
   __device__ void finalize(long long *scr) {
     const int n = a.n;
     long long f = 0;
@@ -733,14 +867,17 @@ struct Kern {
   }
 };
 
-template <typename CapT>
 #ifndef MFX_MIN_BLOCKS
 #define MFX_MIN_BLOCKS 2
 #endif
-__global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS) solve_kernel(const __grid_constant__ SolveArgs<CapT> a) {
+
+template <typename CapT>
+__global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
+    solve_kernel(const __grid_constant__ SolveArgs<CapT> a) {
   __shared__ int s_snap[C_NCTR];
   __shared__ int s_abort;
   __shared__ unsigned long long scr[kWarps];
+  __shared__ WarpQ wq[kWarps];
   if (a.gate && (a.gate[0] != LLONG_MAX || a.gate[1] != LLONG_MAX || a.gate[3] != LLONG_MAX ||
                  a.gate[4] != LLONG_MAX))
     return;  // the batch was rejected: state untouched, nothing to solve
@@ -756,10 +893,11 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS) solve_kernel(const __g
     sy.t_last = globaltimer();
     for (int i = 0; i < PH_N; ++i) sy.ph[i] = 0;
   }
+  if ((threadIdx.x & 31) == 0) wq[threadIdx.x >> 5].cnt[0] = wq[threadIdx.x >> 5].cnt[1] = 0;
   sy.s_snap = s_snap;
   sy.s_abort = &s_abort;
   __syncthreads();
-  Kern<CapT> k(a, sy, lc);
+  Kern<CapT> k(a, sy, lc, wq);
   unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
   if (a.what == WHAT_BARRIER) {  // barrier latency microbenchmark (kc iterations)
     for (int i = 0; i < a.kc && !s_abort; ++i) grid_sync(a.ctrl, sy, 0, 0, 0, PH_FINAL);
