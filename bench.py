@@ -278,9 +278,11 @@ def bench_ours(args, rank, world, local, pg):
     barrier(pg, local)
     e2e_ms = max_over_ranks(pg, e2e_ms, local)
     out["e2e_ms_per_step"] = e2e_ms / K
-    out["e2e_h2d"] = 3 * 8 * args.batch
-    # D2H per call: the device control block (296 B) + the batch error block (64 B)
-    out["e2e_d2h"] = 296 + 64
+    import ctypes
+    h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
+    _lib.load().mfx_transfer_bytes(args.batch, ctypes.byref(h2d), ctypes.byref(d2h))
+    out["e2e_h2d"] = int(h2d.value)  # batch (us, vs, new caps) int64
+    out["e2e_d2h"] = int(d2h.value)  # result control block + batch error block
     out["e2e_flows"] = e2e_flows
 
     # ---- GPU static re-solve on the updated capacities (the comparison point)

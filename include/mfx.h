@@ -179,6 +179,13 @@ int mfx_verify(const mfx_state *st, const mfx_graph *g, mfx_verify_report *rep);
 int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_per_sm,
                       double *ns_per_barrier);
 
+/* Diagnostics: per-barrier trace of the last solve launch when the process
+ * ran with $MFX_TRACE_CAP > 0.  Entry = phase << 60 | items << 32 | ns. */
+int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int64_t cap,
+                    int64_t *count);
+/* Host<->device bytes one mfx_solve_dynamic call of k updates moves. */
+int mfx_transfer_bytes(int64_t k, int64_t *h2d, int64_t *d2h);
+
 /* ---- host memory helpers (pinned staging for end-to-end timing) -------- */
 int mfx_host_alloc(size_t bytes, void **ptr);
 int mfx_host_free(void *ptr);

@@ -67,6 +67,7 @@ Workspace::~Workspace() {
   dfree(mark);
   dfree(stamp);
   dfree(vbin);
+  dfree(trace);
   dfree(slot_first);
   dfree(d_batch);
   dfree(d_slot);
@@ -124,6 +125,11 @@ cudaError_t ensure_workspace(Topology &t) {
     return e;
   if ((e = cudaMalloc(&w.d_err, sizeof(long long) * 8))) return e;
   if ((e = cudaMalloc(&w.d_red, sizeof(unsigned long long) * 64))) return e;
+  if (const char *tc = getenv("MFX_TRACE_CAP")) {
+    w.trace_cap = atoi(tc);
+    if (w.trace_cap > 0 && (e = cudaMalloc(&w.trace, sizeof(unsigned long long) * w.trace_cap)))
+      return e;
+  }
   if ((e = cudaMalloc(&w.vbin, n))) return e;
   if ((e = launch_vbin(t, w.vbin))) return e;
   if ((e = cudaMalloc(&w.mark, sizeof(unsigned) * n))) return e;
@@ -937,6 +943,27 @@ int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_p
   CK(cudaEventRecord(T.ev[1], T.stream));
   CK(cudaEventSynchronize(T.ev[1]));
   *ns_per_barrier = 1e6 * ev_ms(T.ev[0], T.ev[1]) / (iters > 0 ? iters : 1);
+  return MFX_OK;
+}
+
+int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int64_t cap,
+                    int64_t *count) {
+  Topology &T = *g->g.topo;
+  CK(cudaSetDevice(T.device));
+  *count = 0;
+  if (!T.ws.trace) return MFX_OK;
+  long long tn = 0;
+  CK(cudaMemcpy(&tn, &st->s.ctrl->trace_n, sizeof(tn), cudaMemcpyDeviceToHost));
+  if (tn > cap) tn = cap;
+  if (tn > T.ws.trace_cap) tn = T.ws.trace_cap;
+  if (tn > 0) CK(cudaMemcpy(out, T.ws.trace, sizeof(uint64_t) * tn, cudaMemcpyDeviceToHost));
+  *count = tn;
+  return MFX_OK;
+}
+
+int mfx_transfer_bytes(int64_t k, int64_t *h2d, int64_t *d2h) {
+  *h2d = 3 * (int64_t)sizeof(int64_t) * k;                       // batch us, vs, new caps
+  *d2h = (int64_t)sizeof(Ctrl) + 8 * (int64_t)sizeof(long long);  // result block + error block
   return MFX_OK;
 }
 

@@ -24,6 +24,8 @@ struct Workspace {
   unsigned *mark = nullptr;  // wave stamps, n
   unsigned *stamp = nullptr; // current wave stamp (1 word)
   uint8_t *vbin = nullptr;   // degree class per vertex, n
+  unsigned long long *trace = nullptr;  // diagnostics ($MFX_TRACE_CAP entries)
+  int trace_cap = 0;
   int *slot_first = nullptr; // batch duplicate detection, S (kept at kFirstNone)
   // batch staging
   int64_t kcap = 0;

@@ -70,6 +70,7 @@ struct Ctrl {
   long long reached;  // vertices reached by the last global relabel
   int overflow;
   int last_levels;  // BFS levels of the last global relabel
+  long long trace_n;  // entries written to the diagnostics trace by the last launch
 };
 
 // ---- small device helpers -------------------------------------------------

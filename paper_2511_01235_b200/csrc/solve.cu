@@ -63,6 +63,8 @@ struct SolveArgs {
   unsigned *stamp;  // persistent wave stamp shared by all states of the topology
   Ctrl *ctrl;
   const long long *gate;  // batch error block (dynamic solves), may be null
+  unsigned long long *trace;  // optional phase trace (diagnostics), may be null
+  int trace_cap;
 };
 
 // algorithmic bytes per event, CapT-dependent
@@ -97,6 +99,8 @@ struct Sync {
   unsigned long long deadline, ceiling;  // read once at kernel start
   unsigned long long t_last;             // block 0: phase timing
   unsigned long long ph[PH_N];
+  unsigned long long *trace;  // block 0: (phase << 60 | items << 32 | dt_ns) per barrier
+  int trace_cap, trace_n;
 };
 
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned *p, unsigned v) {
@@ -170,8 +174,16 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
     *sy.s_abort = ab;
     if (blockIdx.x == 0) {
       unsigned long long now = globaltimer();
-      sy.ph[phase] += now - sy.t_last;
+      unsigned long long dt = now - sy.t_last;
+      sy.ph[phase] += dt;
       sy.t_last = now;
+      if (sy.trace && sy.trace_n < sy.trace_cap) {
+        unsigned items = 0;  // work published for the next phase
+        for (int i = 0; i < 8; ++i) items += (unsigned)snapv[i];
+        sy.trace[sy.trace_n++] = ((unsigned long long)phase << 60) |
+                                 ((unsigned long long)(items & 0xFFFFFFFu) << 32) |
+                                 (dt & 0xFFFFFFFFull);
+      }
     }
   }
   __syncthreads();
@@ -892,6 +904,9 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     s_abort = vc->abort;
     sy.t_last = globaltimer();
     for (int i = 0; i < PH_N; ++i) sy.ph[i] = 0;
+    sy.trace = blockIdx.x == 0 ? a.trace : nullptr;
+    sy.trace_cap = a.trace_cap;
+    sy.trace_n = 0;
   }
   if ((threadIdx.x & 31) == 0) wq[threadIdx.x >> 5].cnt[0] = wq[threadIdx.x >> 5].cnt[1] = 0;
   sy.s_snap = s_snap;
@@ -930,6 +945,7 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     unsigned long long now = globaltimer();
     sy.ph[PH_FINAL] += now - sy.t_last;
     for (int i = 0; i < PH_N; ++i) a.ctrl->phase_ns[i] += sy.ph[i];
+    if (sy.trace) a.ctrl->trace_n = sy.trace_n;
   }
 }
 
@@ -993,6 +1009,8 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.stamp = W.stamp;
   a.ctrl = st.ctrl;
   a.gate = cfg.gate;
+  a.trace = W.trace;
+  a.trace_cap = W.trace_cap;
 
   ctrl_begin_kernel<<<1, 1, 0, T.stream>>>(st.ctrl, cfg.timeout_s, cfg.ceiling,
                                           cfg.reset_counters ? 1 : 0);

@@ -1,0 +1,71 @@
+"""Per-barrier trace of one static and one dynamic C2 solve (diagnostics).
+
+    MFX_TRACE_CAP=200000 python scripts/trace.py --side 2048
+Prints a histogram of phase durations by work-list size.
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("MFX_TRACE_CAP", "200000")
+
+import paper_2511_01235_b200 as mfx  # noqa: E402
+from paper_2511_01235_b200 import _lib, gen  # noqa: E402
+
+PH = {0: "bfs", 1: "push", 2: "repair", 3: "final"}
+
+
+def fetch(st, g):
+    cap = int(os.environ["MFX_TRACE_CAP"])
+    buf = (ctypes.c_uint64 * cap)()
+    cnt = ctypes.c_int64()
+    _lib.check(_lib.load().mfx_trace_fetch(st.handle, g.handle, buf, cap, ctypes.byref(cnt)))
+    a = np.frombuffer(buf, dtype=np.uint64, count=cnt.value).copy()
+    return (a >> np.uint64(60)).astype(int), ((a >> np.uint64(32)) & np.uint64(0xFFFFFFF)).astype(int), \
+        (a & np.uint64(0xFFFFFFFF)).astype(np.int64)
+
+
+def report(tag, st, g, res):
+    ph, items, dt = fetch(st, g)
+    print(f"== {tag}: {res.device['ms_solve']:.2f} ms, rounds {res.rounds}, "
+          f"levels {res.device['bfs_levels']}, waves {res.device['waves']}, barriers {len(ph)}")
+    # item count of entry i is the work of the phase that ends at entry i+1
+    work = np.concatenate([[0], items[:-1]])
+    for p in (0, 1):
+        m = ph == p
+        if not m.any():
+            continue
+        w, d = work[m], dt[m] / 1e3
+        print(f"  {PH[p]}: n={m.sum()} total {d.sum():.2f} ms, median {np.median(d):.1f} us")
+        for lo, hi in ((0, 1), (1, 100), (100, 1000), (1000, 10000), (10000, 100000), (100000, 1 << 40)):
+            k = (w >= lo) & (w < hi)
+            if k.any():
+                print(f"    items [{lo},{hi}): {k.sum():5d} phases, {d[k].sum():8.2f} ms, "
+                      f"mean {d[k].mean():7.1f} us, items/phase {w[k].mean():9.0f}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--side", type=int, default=2048)
+    ap.add_argument("--max-waves", type=int, default=0)
+    args = ap.parse_args()
+    us, vs, caps, s, t = gen.grid_graph(args.side, args.side, 0)
+    n = args.side * args.side + 2
+    g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps))
+    p = mfx.SolverParams(max_waves=args.max_waves)
+    mfx.solve_static(g, s, t, p)
+    r = mfx.solve_static(g, s, t, p)
+    report("static", r.state, g, r)
+    el = g.to_edge_list()
+    bu, bv, bc, _ = gen.fast_batch(n, el.us, el.vs, el.caps, s, t, 10000, "mixed", 0)
+    rr = mfx.solve_dynamic(r.state, g, mfx.UpdateBatch(bu, bv, bc), p)
+    report("dynamic", rr.state, g, rr)
+
+
+if __name__ == "__main__":
+    main()
