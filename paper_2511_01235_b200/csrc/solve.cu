@@ -233,9 +233,30 @@ struct Kern {
   WarpQ *q;  // this warp's staging queues
   int gtid, gthreads, gwarp, gwarps, lane, wib;
   int act_cnt;  // active discoveries counted by this lane in the current level
+  long long *s_sink;  // per-CTA sum of excess pushed into the sink this phase
 
-  __device__ Kern(const SolveArgs<CapT> &a_, Sync &sy_, Local &lc_, WarpQ *wq)
-      : a(a_), sy(sy_), lc(lc_) {
+  // Excess arriving at v.  The sink receives pushes from up to every pixel of
+  // the grid config in the same wave; a global atomic on ex[t] per push
+  // serialises at one L2 slice, so the sink's share is summed in shared
+  // memory and published once per CTA per phase (sink_flush).  Returns the
+  // previous excess of v (for the sink: a positive dummy, it never activates).
+  __device__ __forceinline__ long long add_excess(int v, long long d) {
+    if (v == a.t) {
+      atomicAdd((unsigned long long *)s_sink, (unsigned long long)d);
+      return 1;
+    }
+    return atomic_add(a.ex + v, d);
+  }
+  __device__ __forceinline__ void sink_flush() {  // whole CTA, before a grid barrier
+    __syncthreads();
+    if (threadIdx.x == 0 && *s_sink) {
+      atomic_add(a.ex + a.t, *s_sink);
+      *s_sink = 0;
+    }
+  }
+
+  __device__ Kern(const SolveArgs<CapT> &a_, Sync &sy_, Local &lc_, WarpQ *wq, long long *sink)
+      : a(a_), sy(sy_), lc(lc_), s_sink(sink) {
     gtid = blockIdx.x * blockDim.x + threadIdx.x;
     gthreads = gridDim.x * blockDim.x;
     lane = threadIdx.x & 31;
@@ -560,7 +581,7 @@ struct Kern {
               atomic_add(a.cf + rv[k], (CapT)dd);
               own_old = atomic_add(a.ex + u, -dd);
               own_d = dd;
-              oldv[k] = atomic_add(a.ex + vv[k], dd);
+              oldv[k] = add_excess(vv[k], dd);
               pushed |= 1u << k;
             }
           own_atomic = true;
@@ -694,7 +715,7 @@ struct Kern {
         if (amt > 0) {
           atomic_add(a.cf + i, (CapT)(-amt));
           atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
-          long long old = atomic_add(a.ex + v, amt);
+          long long old = add_excess(v, amt);
           act = old <= 0 && v != a.s && v != a.t;
           lc.pushes++;
           lc.bytes += Bytes<CapT>::kPush;
@@ -732,7 +753,7 @@ struct Kern {
         if (amt > 0) {
           atomic_add(a.cf + __ldg(a.rev + i), amt);
           atomic_add(a.ex + u, -(long long)amt);
-          atomic_add(a.ex + v, (long long)amt);
+          add_excess(v, (long long)amt);
           lc.repairs++;
           lc.bytes += Bytes<CapT>::kPush;
         }
@@ -762,7 +783,7 @@ struct Kern {
           if (amt > 0) {
             atomic_add(a.cf + __ldg(a.rev + lo + k), amt);
             atomic_add(a.ex + u, -(long long)amt);
-            atomic_add(a.ex + vv[k], (long long)amt);
+            add_excess(vv[k], (long long)amt);
             lc.repairs++;
             lc.bytes += Bytes<CapT>::kPush;
           }
@@ -818,6 +839,7 @@ struct Kern {
         for (int j = base[b] + blockIdx.x; j < lim[b]; j += gridDim.x)
           push_coop<kBlock>(ldcg(a.R[b] + j), next, nbase, s_red);
       stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
+      sink_flush();
       flush_counters(a.ctrl, lc, scr);
       grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_PUSH);
       ++waves;
@@ -835,6 +857,7 @@ struct Kern {
       if (end[b] > a.rcap) end[b] = a.rcap;
     }
     repair(end);
+    sink_flush();
     flush_counters(a.ctrl, lc, scr);
     if (gtid == 0) {
       a.ctrl->waves += waves;
@@ -890,6 +913,7 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
   __shared__ int s_abort;
   __shared__ unsigned long long scr[kWarps];
   __shared__ WarpQ wq[kWarps];
+  __shared__ long long s_sink;
   if (a.gate && (a.gate[0] != LLONG_MAX || a.gate[1] != LLONG_MAX || a.gate[3] != LLONG_MAX ||
                  a.gate[4] != LLONG_MAX))
     return;  // the batch was rejected: state untouched, nothing to solve
@@ -907,12 +931,13 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     sy.trace = blockIdx.x == 0 ? a.trace : nullptr;
     sy.trace_cap = a.trace_cap;
     sy.trace_n = 0;
+    s_sink = 0;
   }
   if ((threadIdx.x & 31) == 0) wq[threadIdx.x >> 5].cnt[0] = wq[threadIdx.x >> 5].cnt[1] = 0;
   sy.s_snap = s_snap;
   sy.s_abort = &s_abort;
   __syncthreads();
-  Kern<CapT> k(a, sy, lc, wq);
+  Kern<CapT> k(a, sy, lc, wq, &s_sink);
   unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
   if (a.what == WHAT_BARRIER) {  // barrier latency microbenchmark (kc iterations)
     for (int i = 0; i < a.kc && !s_abort; ++i) grid_sync(a.ctrl, sy, 0, 0, 0, PH_FINAL);
