@@ -61,6 +61,8 @@ typedef struct {
     int32_t flags;         /* reserved, 0                                          */
     int32_t wave_mult;     /* auto wave budget = wave_mult * BFS levels + wave_add */
     int32_t wave_add;      /*   (0, 0 -> 2, 16); used when max_waves == 0          */
+    int32_t schedule;      /* push phase: 0 asynchronous work queue, 1 waves       */
+    int32_t async_budget;  /* async: items per active vertex per round (0 -> 16)   */
 } mfx_params;
 
 /* FlowResult (solver.py:108-118) plus device counters. */
@@ -76,6 +78,7 @@ typedef struct {
     double ms_total;        /* whole call incl. host<->device copies, CUDA events       */
     int32_t status;
     int32_t launches;       /* kernels launched by this call                            */
+    int64_t async_items;    /* vertices processed by asynchronous push phases           */
 } mfx_result;
 
 /* mfx_verify report: the checks of oracle.py construct_flow / verify_preflow /

@@ -37,7 +37,8 @@ class GraphInfo(ctypes.Structure):
 class Params(ctypes.Structure):
     _fields_ = [("kernel_cycles", i64), ("mode", i32), ("max_waves", i32),
                 ("timeout_s", ctypes.c_double), ("blocks_per_sm", i32), ("flags", i32),
-                ("wave_mult", i32), ("wave_add", i32)]
+                ("wave_mult", i32), ("wave_add", i32), ("schedule", i32),
+                ("async_budget", i32)]
 
 
 class Result(ctypes.Structure):
@@ -46,7 +47,8 @@ class Result(ctypes.Structure):
                 ("bytes_alg", i64), ("updates", i64), ("ns_bfs", ctypes.c_double),
                 ("ns_push", ctypes.c_double), ("ns_repair", ctypes.c_double),
                 ("ms_update", ctypes.c_double), ("ms_solve", ctypes.c_double),
-                ("ms_total", ctypes.c_double), ("status", i32), ("launches", i32)]
+                ("ms_total", ctypes.c_double), ("status", i32), ("launches", i32),
+                ("async_items", i64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -67,6 +67,7 @@ Workspace::~Workspace() {
   dfree(mark);
   dfree(stamp);
   dfree(vbin);
+  dfree(rdirty);
   dfree(trace);
   dfree(slot_first);
   dfree(d_batch);
@@ -113,8 +114,13 @@ cudaError_t ensure_workspace(Topology &t) {
   for (int q = 0; q < 2; ++q)
     for (int b = 0; b < NBIN; ++b)
       if ((e = cudaMalloc(&w.F[q][b], sizeof(int) * n))) return e;
-  for (int b = 0; b < NBIN; ++b)
+  for (int b = 0; b < NBIN; ++b) {
     if ((e = cudaMalloc(&w.R[b], sizeof(int) * (size_t)w.rcap))) return e;
+    // async push consumers wait for slots != -1: lists start (and are reset to) empty
+    if ((e = cudaMemsetAsync(w.R[b], 0xFF, sizeof(int) * (size_t)w.rcap, t.stream))) return e;
+  }
+  if ((e = cudaMalloc(&w.rdirty, sizeof(int) * NBIN))) return e;
+  if ((e = cudaMemsetAsync(w.rdirty, 0, sizeof(int) * NBIN, t.stream))) return e;
   if ((e = cudaMalloc(&w.bases, sizeof(int) * n))) return e;
   if ((e = cudaMalloc(&w.heavy, sizeof(int) * n))) return e;
   if ((e = cudaMalloc(&w.stamp, sizeof(unsigned) * 4))) return e;
@@ -588,6 +594,9 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.kc = (int)kc;
   cfg.topology = p->mode;
   cfg.max_waves = p->max_waves;
+  cfg.async = p->schedule == 0;
+  if (const char *sch = getenv("MFX_SCHEDULE")) cfg.async = sch[0] != 'w';
+  if (p->async_budget > 0) cfg.async_budget = p->async_budget;
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;
@@ -615,6 +624,7 @@ static void fill_result(const mfx_state *st, mfx_result *r) {
   r->ns_push = (double)c.phase_ns[PH_PUSH];
   r->ns_repair = (double)c.phase_ns[PH_REPAIR];
   r->status = c.status;
+  r->async_items = (int64_t)c.async_items;
 }
 
 static int solve_status(const mfx_state *st, mfx_result *r) {

@@ -24,6 +24,7 @@ struct Workspace {
   unsigned *mark = nullptr;  // wave stamps, n
   unsigned *stamp = nullptr; // current wave stamp (1 word)
   uint8_t *vbin = nullptr;   // degree class per vertex, n
+  int *rdirty = nullptr;     // NBIN: used extent of each R list (reset to -1 before reuse)
   unsigned long long *trace = nullptr;  // diagnostics ($MFX_TRACE_CAP entries)
   int trace_cap = 0;
   int *slot_first = nullptr; // batch duplicate detection, S (kept at kFirstNone)
@@ -83,6 +84,8 @@ struct SolveConfig {
   int max_waves = 0;
   int wave_mult = 2;  // auto wave budget per round: wave_mult * BFS levels + wave_add
   int wave_add = 16;
+  int async = 1;          // asynchronous push phase (work queue) instead of waves
+  int async_budget = 16;  // items per initially active vertex before a global relabel
   int topology = 0;
   double timeout_s = 600.0;
   int blocks_per_sm = 0;

@@ -71,6 +71,12 @@ struct Ctrl {
   int overflow;
   int last_levels;  // BFS levels of the last global relabel
   long long trace_n;  // entries written to the diagnostics trace by the last launch
+  // asynchronous push phase: per-bin queue heads / completed items, stop flag
+  unsigned aq_head[NBIN];
+  unsigned aq_done[NBIN];
+  int aq_stop;
+  int aq_pad;
+  unsigned long long async_items;  // items processed by asynchronous push phases
 };
 
 // ---- small device helpers -------------------------------------------------

@@ -42,6 +42,9 @@ struct SolveArgs {
   int max_waves;  // > 0: fixed waves per round; 0: wave_mult * BFS levels + wave_add
   int wave_mult;
   int wave_add;
+  int async;         // asynchronous push phase (data mode only)
+  int async_budget;  // items per initially active vertex before the next global relabel
+  int *rdirty;       // NBIN used extents of the R lists (device, shared by states)
   int topology;
   int what;
   int rcap;
@@ -338,9 +341,12 @@ struct Kern {
   // =========================================================================
   // global relabel (kernels.py:168-215) as a level-synchronous frontier BFS
   // =========================================================================
+  unsigned ep_next;  // ownership stamp of the coming asynchronous push phase
+
   __device__ __forceinline__ void discover_post(bool disc, int v, int b, bool act, int *const *Fn,
                                                 const int *rbase, const int *zero) {
     act_cnt += act;
+    if (act && a.async) a.mark[v] = ep_next;  // queued for the push phase = owned
     append_binned(0, disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, a.n);
     append_binned(1, act && !a.topology, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap);
   }
@@ -413,13 +419,30 @@ struct Kern {
     act_cnt = 0;
   }
 
-  // returns the number of BFS levels; the active set is left in R (wave 0)
-  __device__ int bfs() {
+  // returns the number of BFS levels; the active set is left in R (wave 0).
+  // ep: ownership stamp the following asynchronous push phase will use.
+  __device__ int bfs(unsigned ep) {
     const int n = a.n;
     __shared__ int zero[NBIN];
     __shared__ int rb[NBIN];
+    ep_next = ep;
     if (threadIdx.x < NBIN) zero[threadIdx.x] = 0;
     __syncthreads();
+    // empty the R lists (async consumers wait on -1 slots) and the async counters
+    if (!a.topology) {  // (topology mode seeds R below and never runs asynchronously)
+      for (int b = 0; b < NBIN; ++b) {
+        int used = ldcg(a.rdirty + b);
+        if (used > a.rcap) used = a.rcap;
+        for (int j = gtid; j < used; j += gthreads) a.R[b][j] = -1;
+      }
+    }
+    if (gtid == 0) {
+      for (int b = 0; b < NBIN; ++b) {
+        a.ctrl->aq_head[b] = 0;
+        a.ctrl->aq_done[b] = 0;
+      }
+      a.ctrl->aq_stop = 0;
+    }
     // reset + seed bases (kernels.py:184-193); topology mode seeds wave 0
     for (int v0 = gwarp * 32; v0 < n; v0 += gwarps * 32) {
       int v = v0 + lane;
@@ -499,6 +522,7 @@ struct Kern {
       a.ctrl->levels += L;
       a.ctrl->last_levels = L;
       a.ctrl->reached = reached;
+      for (int b = 0; b < NBIN; ++b) a.rdirty[b] = sy.s_snap[C_RNEXT + b];
     }
     return L;
   }
@@ -522,6 +546,7 @@ struct Kern {
   // grows under concurrent pushes and only this thread lowers it, so
   // snapshot - own pushes is a safe lower bound; stale neighbour heights are
   // the lock-free algorithm's tolerated race.
+  template <bool Async>
   __device__ void push_thread(bool valid, int u, unsigned stamp, const int *nbase) {
     const int n = a.n;
     int lo = 0, d = 0, hu = n;
@@ -595,12 +620,24 @@ struct Kern {
       }
     }
     if (own_atomic) e_after = own_old - own_d;
+    // pushes must be visible before a head is handed to another owner
+    if (Async) __threadfence();
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) {
       bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
       activate(p, vv[k], stamp, nbase);
     }
-    activate(live && hu < n && e_after > 0, u, stamp, nbase);
+    if (Async) {
+      // Release ownership, then re-check: a pusher that found u owned did not
+      // enqueue it, so whichever of us sees the other's write re-enqueues
+      // (store/fence/load against add/fence/atomicMax).
+      if (valid) a.mark[u] = 0;
+      __threadfence();
+      bool again = valid && hu < n && ldcg(a.ex + u) > 0;
+      activate(again, u, stamp, nbase);
+    } else {
+      activate(live && hu < n && e_after > 0, u, stamp, nbase);
+    }
   }
 
   // Cooperative push for rows of more than kBin0Max slots, by a group of G
@@ -609,7 +646,7 @@ struct Kern {
   // the excess is then pushed across every admissible slot at height bh in
   // slot order (ordered prefix sum of the residuals), which is what
   // successive KC steps would do while bh stays the minimum, in one pass.
-  template <int G>
+  template <int G, bool Async>
   __device__ void push_coop(int u, unsigned stamp, const int *nbase, long long *s_red) {
     const int n = a.n;
     const int tid = G == 32 ? lane : threadIdx.x;
@@ -719,6 +756,7 @@ struct Kern {
           act = old <= 0 && v != a.s && v != a.t;
           lc.pushes++;
           lc.bytes += Bytes<CapT>::kPush;
+          if (Async && act) __threadfence();  // push visible before the hand-off
         }
         activate(act, v, stamp, nbase);
         carry += tot;
@@ -732,11 +770,16 @@ struct Kern {
       eu -= moved;
       if (G > 32) __syncthreads();
     }
-    // self re-activation from the fresh value returned by the last atomic
     bool self = false;
     if (tid == 0) {
-      long long e_after = any_push ? last_old - last_total : eu;
-      self = hu < n && e_after > 0;
+      if (Async) {  // release ownership, then re-check (see push_thread)
+        a.mark[u] = 0;
+        __threadfence();
+        self = hu < n && ldcg(a.ex + u) > 0;
+      } else {  // self re-activation from the fresh value returned by the last atomic
+        long long e_after = any_push ? last_old - last_total : eu;
+        self = hu < n && e_after > 0;
+      }
     }
     if (G == 32 || wib == 0) activate(self, u, stamp, nbase);
     if (G > 32) __syncthreads();
@@ -764,6 +807,7 @@ struct Kern {
   __device__ void repair(const int *end) {
     for (int j = gtid; j < end[0]; j += gthreads) {  // thread per row, loads batched
       int u = ldcg(a.R[0] + j);
+      if (u < 0) continue;  // reserved slot never filled (queue overflow)
       int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
       int hu = ldcg(a.h + u);
       lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kSlot;
@@ -792,6 +836,7 @@ struct Kern {
     }
     for (int j = gwarp; j < end[1]; j += gwarps) {
       int u = ldcg(a.R[1] + j);
+      if (u < 0) continue;
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int hu = ldcg(a.h + u);
       if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
@@ -800,6 +845,7 @@ struct Kern {
     for (int b = 2; b < NBIN; ++b) {
       for (int j = blockIdx.x; j < end[b]; j += gridDim.x) {
         int u = ldcg(a.R[b] + j);
+        if (u < 0) continue;  // (uniform across the CTA: same slot)
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         int hu = ldcg(a.h + u);
         if (threadIdx.x == 0)
@@ -832,12 +878,13 @@ struct Kern {
       for (int j0 = base[0] + gwarp * 32; j0 < lim[0]; j0 += gwarps * 32) {
         int j = j0 + lane;
         bool valid = j < lim[0];
-        push_thread(valid, valid ? ldcg(a.R[0] + j) : 0, next, nbase);
+        push_thread<false>(valid, valid ? ldcg(a.R[0] + j) : 0, next, nbase);
       }
-      for (int j = base[1] + gwarp; j < lim[1]; j += gwarps) push_coop<32>(ldcg(a.R[1] + j), next, nbase, s_red);
+      for (int j = base[1] + gwarp; j < lim[1]; j += gwarps)
+        push_coop<32, false>(ldcg(a.R[1] + j), next, nbase, s_red);
       for (int b = 2; b < NBIN; ++b)
         for (int j = base[b] + blockIdx.x; j < lim[b]; j += gridDim.x)
-          push_coop<kBlock>(ldcg(a.R[b] + j), next, nbase, s_red);
+          push_coop<kBlock, false>(ldcg(a.R[b] + j), next, nbase, s_red);
       stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
       sink_flush();
       flush_counters(a.ctrl, lc, scr);
@@ -862,8 +909,175 @@ struct Kern {
     if (gtid == 0) {
       a.ctrl->waves += waves;
       a.ctrl->rounds += 1;
+      for (int b = 0; b < NBIN; ++b) a.rdirty[b] = end[b];
     }
     // the barrier also clears the wave counters left by the last wave
+    grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_REPAIR);
+  }
+
+  // -------------------------------------------------------------------------
+  // asynchronous push phase: the R lists are work queues (tail = BFS count +
+  // appended, head = claimed, -1 = reserved but not yet written).  Light
+  // vertices are claimed 32 at a time by a warp, bin-1 rows one per warp,
+  // heavy rows one per CTA.  A vertex is owned while its mark equals the
+  // phase stamp: activation is atomicMax(mark, ep) < ep, and the owner
+  // releases (mark = 0) and re-checks its excess after processing, so every
+  // vertex with positive excess is queued at most once at any time.  The
+  // phase ends when every queued item is done (quiescence: done read before
+  // tail), or after a work budget (then the next global relabel re-derives
+  // the active set), with no barrier per hop.
+  // -------------------------------------------------------------------------
+  __device__ __forceinline__ int claim_one(int b, const int *nbase) {
+    unsigned *hp = a.ctrl->aq_head + b;
+    for (int tries = 0; tries < 64; ++tries) {
+      unsigned h = ld_acquire_u32(hp);
+      unsigned t = (unsigned)nbase[b] + (unsigned)ldcg(a.ctrl->live + C_RNEXT + b);
+      if (h >= t || (int)h >= a.rcap) return -1;
+      if (atomicCAS(hp, h, h + 1) == h) return (int)h;
+    }
+    return -1;
+  }
+
+  __device__ __forceinline__ int wait_slot(const int *list, int slot) {
+    int x;
+    while ((x = ldcg(list + slot)) < 0) __nanosleep(32);
+    return x;
+  }
+
+  // 0 = continue, 1 = quiescent, 2 = stopped (budget / overflow / watchdog)
+  __device__ int async_state(const int *nbase, long long budget) {
+    unsigned d = 0, t = 0;
+#pragma unroll
+    for (int b = 0; b < NBIN; ++b) d += ld_acquire_u32(a.ctrl->aq_done + b);
+#pragma unroll
+    for (int b = 0; b < NBIN; ++b) t += (unsigned)nbase[b] + (unsigned)ldcg(a.ctrl->live + C_RNEXT + b);
+    if (d == t) return 1;
+    volatile Ctrl *vc = a.ctrl;
+    if (vc->aq_stop || vc->abort || vc->overflow) return 2;
+    if ((long long)d >= budget) {
+      vc->aq_stop = 1;
+      return 2;
+    }
+    if (globaltimer() > sy.deadline) {
+      vc->abort = 1;
+      vc->status = 6;
+      return 2;
+    }
+    return 0;
+  }
+
+  __device__ void push_round_async(unsigned &stamp, unsigned long long *scr) {
+    __shared__ int nbase[NBIN];
+    __shared__ long long s_red[kWarps + 2];
+    __shared__ int s_item, s_bin, s_state;
+    const unsigned ep = ++stamp;  // the BFS marked the queued vertices with this stamp
+    long long active0 = 0;
+    for (int b = 0; b < NBIN; ++b) active0 += sy.s_snap[C_RNEXT + b];
+    const long long budget = (long long)a.async_budget * active0 + 4096;
+    if (threadIdx.x < NBIN) nbase[threadIdx.x] = sy.s_snap[C_RNEXT + threadIdx.x];
+    __syncthreads();
+    int my_slot = 0;
+    bool pend = false;
+    for (;;) {
+      // ---- heavy rows: one per CTA
+      if (threadIdx.x == 0) {
+        s_item = -1;
+        for (int b = NBIN - 1; b >= 2 && s_item < 0; --b) {
+          int x = claim_one(b, nbase);
+          if (x >= 0) {
+            s_item = x;
+            s_bin = b;
+          }
+        }
+      }
+      __syncthreads();
+      bool progress = false;
+      if (s_item >= 0) {
+        const int hb = s_bin;
+        __shared__ int s_u;
+        if (threadIdx.x == 0) s_u = wait_slot(a.R[hb], s_item);
+        __syncthreads();
+        push_coop<kBlock, true>(s_u, ep, nbase, s_red);
+        stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(a.ctrl->aq_done + hb, 1u);
+        }
+        progress = true;
+      } else {
+        // ---- bin-1 rows: one per warp
+        int x1 = -1;
+        if (lane == 0) x1 = claim_one(1, nbase);
+        x1 = __shfl_sync(FULL, x1, 0);
+        if (x1 >= 0) {
+          int u = 0;
+          if (lane == 0) u = wait_slot(a.R[1], x1);
+          u = __shfl_sync(FULL, u, 0);
+          push_coop<32, true>(u, ep, nbase, s_red);
+          stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
+          if (lane == 0) {
+            __threadfence();
+            atomicAdd(a.ctrl->aq_done + 1, 1u);
+          }
+          progress = true;
+        }
+        // ---- light vertices: a batch of 32 queue slots per warp
+        if (!__any_sync(FULL, pend)) {
+          unsigned c = 0;
+          if (lane == 0) c = atomicAdd(a.ctrl->aq_head + 0, 32u);
+          c = __shfl_sync(FULL, c, 0);
+          my_slot = (int)(c + lane);
+          pend = my_slot < a.rcap;
+        }
+        int item = pend ? ldcg(a.R[0] + my_slot) : -1;
+        bool ready = item >= 0;
+        unsigned rb = __ballot_sync(FULL, ready);
+        if (rb) {
+          push_thread<true>(ready, ready ? item : 0, ep, nbase);
+          stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
+          if (lane == 0) {
+            __threadfence();
+            atomicAdd(a.ctrl->aq_done + 0, (unsigned)__popc(rb));
+          }
+          pend = pend && !ready;
+          progress = true;
+        }
+      }
+      if (!__syncthreads_or(progress)) __nanosleep(200);
+      if (threadIdx.x == 0) s_state = async_state(nbase, budget);
+      __syncthreads();
+      if (s_state != 0) break;
+    }
+    sink_flush();
+    flush_counters(a.ctrl, lc, scr);
+    grid_sync(a.ctrl, sy, 0, 0, 0, PH_PUSH);
+    // repair (kernels.py:70-93) over every vertex taken from the queues
+    __shared__ int s_end[NBIN];
+    if (threadIdx.x < NBIN) {
+      int b = threadIdx.x;
+      int hd = (int)ldcg((const int *)(a.ctrl->aq_head + b));
+      int tl = nbase[b] + ldcg(a.ctrl->live + C_RNEXT + b);
+      int e = hd < tl ? hd : tl;
+      s_end[b] = e < a.rcap ? e : a.rcap;
+    }
+    __syncthreads();
+    int end[NBIN];
+    for (int b = 0; b < NBIN; ++b) end[b] = s_end[b];
+    repair(end);
+    sink_flush();
+    flush_counters(a.ctrl, lc, scr);
+    if (gtid == 0) {
+      unsigned d = 0;
+      for (int b = 0; b < NBIN; ++b) {
+        d += ldcg((const int *)(a.ctrl->aq_done + b));
+        int tl = nbase[b] + ldcg(a.ctrl->live + C_RNEXT + b);
+        a.rdirty[b] = tl < a.rcap ? tl : a.rcap;
+      }
+      a.ctrl->async_items += d;
+      a.ctrl->waves += 1;
+      a.ctrl->rounds += 1;
+    }
     grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_REPAIR);
   }
 
@@ -942,22 +1156,24 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
   if (a.what == WHAT_BARRIER) {  // barrier latency microbenchmark (kc iterations)
     for (int i = 0; i < a.kc && !s_abort; ++i) grid_sync(a.ctrl, sy, 0, 0, 0, PH_FINAL);
   } else if (a.what == WHAT_BFS) {
-    k.bfs();
+    k.bfs(stamp + 1);
     if (k.gtid == 0) a.ctrl->active = (long long)s_snap[C_ACTIVE];
     flush_counters(a.ctrl, lc, scr);
   } else if (a.what == WHAT_ROUND) {
     int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
-    k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
+    if (a.async) k.push_round_async(stamp, scr);
+    else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
     if (k.gtid == 0) *a.stamp = stamp;
   } else {
     bool final = true;
     if (a.what == WHAT_SOLVE) {
       for (;;) {
-        int L = k.bfs();
+        int L = k.bfs(stamp + 1);
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
         if (act == 0 || s_abort) break;
-        k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
+        if (a.async) k.push_round_async(stamp, scr);
+        else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
         if (s_abort) break;
       }
       if (k.gtid == 0) *a.stamp = stamp;
@@ -990,6 +1206,7 @@ __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long 
   if (reset_counters) {
     for (int i = 0; i < PH_N; ++i) c->phase_ns[i] = 0;
     c->pushes = c->relabels = c->repairs = c->rounds = c->levels = c->waves = c->bytes = 0;
+    c->async_items = 0;
   }
 }
 
@@ -1011,6 +1228,9 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.max_waves = cfg.max_waves;
   a.wave_mult = cfg.wave_mult;
   a.wave_add = cfg.wave_add;
+  a.async = cfg.async && !cfg.topology;
+  a.async_budget = cfg.async_budget;
+  a.rdirty = W.rdirty;
   a.topology = cfg.topology;
   a.what = cfg.what;
   a.rcap = W.rcap;

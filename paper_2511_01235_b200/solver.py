@@ -26,6 +26,7 @@ class SolverError(RuntimeError):
 L.register_error(L.MFX_SOLVER_ERROR, SolverError)
 
 MODES = ("data", "topology")
+SCHEDULES = ("async", "waves")  # device push-phase schedule (not a reference knob)
 
 
 def operation_ceiling(n: int, m_original: int) -> int:
@@ -56,6 +57,8 @@ class SolverParams:
     blocks_per_sm: int = 0
     wave_mult: int = 0
     wave_add: int = 0
+    schedule: str = "async"
+    async_budget: int = 0
 
     def resolve_threads(self) -> int:
         return 1
@@ -75,9 +78,12 @@ class SolverParams:
         self.validate()
         if self.kernel_cycles < 0:
             raise ValueError("kernel_cycles must be >= 1 (or 0 for the default)")
+        if self.schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {SCHEDULES}, got {self.schedule!r}")
         return L.Params(int(self.kernel_cycles), MODES.index(self.mode), int(self.max_waves),
                         float(self.timeout_s), int(self.blocks_per_sm), 0,
-                        int(self.wave_mult), int(self.wave_add))
+                        int(self.wave_mult), int(self.wave_add),
+                        SCHEDULES.index(self.schedule), int(self.async_budget))
 
 
 @dataclass

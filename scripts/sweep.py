@@ -40,7 +40,7 @@ def parse_knobs(spec):
     out = {}
     for kv in filter(None, spec.split(",")):
         k, v = kv.split("=")
-        out[k] = int(v)
+        out[k] = int(v) if v.lstrip("-").isdigit() else v
     return out
 
 
