@@ -944,16 +944,20 @@ struct Kern {
     return x;
   }
 
-  // 0 = continue, 1 = quiescent, 2 = stopped (budget / overflow / watchdog)
-  __device__ int async_state(const int *nbase, long long budget) {
+  // 0 = continue, 1 = quiescent, 2 = stopped (budget), 3 = stopped elsewhere,
+  // 4 = overflow, 5 = watchdog
+  __device__ int async_state(const int *nbase, long long budget, unsigned *dd, unsigned *tt) {
     unsigned d = 0, t = 0;
 #pragma unroll
     for (int b = 0; b < NBIN; ++b) d += ld_acquire_u32(a.ctrl->aq_done + b);
 #pragma unroll
     for (int b = 0; b < NBIN; ++b) t += (unsigned)nbase[b] + (unsigned)ldcg(a.ctrl->live + C_RNEXT + b);
+    *dd = d;
+    *tt = t;
     if (d == t) return 1;
     volatile Ctrl *vc = a.ctrl;
-    if (vc->aq_stop || vc->abort || vc->overflow) return 2;
+    if (vc->overflow) return 4;
+    if (vc->aq_stop || vc->abort) return 3;
     if ((long long)d >= budget) {
       vc->aq_stop = 1;
       return 2;
@@ -961,7 +965,7 @@ struct Kern {
     if (globaltimer() > sy.deadline) {
       vc->abort = 1;
       vc->status = 6;
-      return 2;
+      return 5;
     }
     return 0;
   }
@@ -970,6 +974,7 @@ struct Kern {
     __shared__ int nbase[NBIN];
     __shared__ long long s_red[kWarps + 2];
     __shared__ int s_item, s_bin, s_state;
+    __shared__ unsigned s_d, s_t;
     const unsigned ep = ++stamp;  // the BFS marked the queued vertices with this stamp
     long long active0 = 0;
     for (int b = 0; b < NBIN; ++b) active0 += sy.s_snap[C_RNEXT + b];
@@ -1045,10 +1050,13 @@ struct Kern {
         }
       }
       if (!__syncthreads_or(progress)) __nanosleep(200);
-      if (threadIdx.x == 0) s_state = async_state(nbase, budget);
+      if (threadIdx.x == 0) s_state = async_state(nbase, budget, &s_d, &s_t);
       __syncthreads();
       if (s_state != 0) break;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && sy.trace && sy.trace_n < sy.trace_cap)
+      sy.trace[sy.trace_n++] = (7ull << 60) | ((unsigned long long)(s_state & 0xF) << 56) |
+                               ((unsigned long long)(s_d & 0xFFFFFFFu) << 28) | (s_t & 0xFFFFFFFu);
     sink_flush();
     flush_counters(a.ctrl, lc, scr);
     grid_sync(a.ctrl, sy, 0, 0, 0, PH_PUSH);

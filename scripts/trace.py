@@ -32,6 +32,21 @@ def fetch(st, g):
 
 def report(tag, st, g, res):
     ph, items, dt = fetch(st, g)
+    raw = ph == 7
+    if raw.any():
+        cap = int(os.environ["MFX_TRACE_CAP"])
+        buf = (ctypes.c_uint64 * cap)()
+        cnt = ctypes.c_int64()
+        _lib.check(_lib.load().mfx_trace_fetch(st.handle, g.handle, buf, cap, ctypes.byref(cnt)))
+        a = np.frombuffer(buf, dtype=np.uint64, count=cnt.value)[raw]
+        states = (a >> np.uint64(56)) & np.uint64(0xF)
+        d = (a >> np.uint64(28)) & np.uint64(0xFFFFFFF)
+        t = a & np.uint64(0xFFFFFFF)
+        print(f"  async phases: {raw.sum()}  end states {np.bincount(states.astype(int)).tolist()}")
+        for i in range(min(12, len(a))):
+            print(f"    state {int(states[i])} done {int(d[i])} tail {int(t[i])}")
+        keep = ~raw
+        ph, items, dt = ph[keep], items[keep], dt[keep]
     print(f"== {tag}: {res.device['ms_solve']:.2f} ms, rounds {res.rounds}, "
           f"levels {res.device['bfs_levels']}, waves {res.device['waves']}, barriers {len(ph)}")
     # item count of entry i is the work of the phase that ends at entry i+1
