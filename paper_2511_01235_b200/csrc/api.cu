@@ -109,7 +109,10 @@ cudaError_t ensure_workspace(Topology &t) {
   if (w.mark) return cudaSuccess;
   size_t n = (size_t)(t.n > 0 ? t.n : 1);
   w.n = t.n;
-  w.rcap = (int)(2 * n + 1024);
+  {  // work lists: the asynchronous push phase logs every (re-)queued vertex
+    size_t rc = 4 * n + 4096;
+    w.rcap = rc > (size_t)INT_MAX ? INT_MAX : (int)rc;
+  }
   cudaError_t e;
   for (int q = 0; q < 2; ++q)
     for (int b = 0; b < NBIN; ++b)

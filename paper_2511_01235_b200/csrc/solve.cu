@@ -442,6 +442,7 @@ struct Kern {
         a.ctrl->aq_done[b] = 0;
       }
       a.ctrl->aq_stop = 0;
+      a.ctrl->overflow = 0;  // dropped items are re-found by this global relabel
     }
     // reset + seed bases (kernels.py:184-193); topology mode seeds wave 0
     for (int v0 = gwarp * 32; v0 < n; v0 += gwarps * 32) {
@@ -957,6 +958,12 @@ struct Kern {
     if (d == t) return 1;
     volatile Ctrl *vc = a.ctrl;
     if (vc->overflow) return 4;
+    // leave headroom in the queues: end the phase (global relabel) well before
+    // a list could overflow (an in-flight warp publishes at most 32 + 8*32 items)
+    if ((unsigned)nbase[0] + (unsigned)ldcg(a.ctrl->live + C_RNEXT) > (unsigned)(a.rcap - a.rcap / 8)) {
+      vc->aq_stop = 1;
+      return 2;
+    }
     if (vc->aq_stop || vc->abort) return 3;
     if ((long long)d >= budget) {
       vc->aq_stop = 1;
