@@ -59,9 +59,9 @@ typedef struct {
     double timeout_s;      /* device watchdog for one solve; 0 -> 600 s            */
     int32_t blocks_per_sm; /* persistent-grid occupancy; 0 -> auto                 */
     int32_t flags;         /* reserved, 0                                          */
-    int32_t wave_mult;     /* auto wave budget = wave_mult * BFS levels + wave_add */
-    int32_t wave_add;      /*   (0, 0 -> 2, 16); used when max_waves == 0          */
-    int32_t schedule;      /* push phase: 0 asynchronous work queue, 1 waves       */
+    int32_t wave_mult;     /* auto wave budget = wave_mult * BFS levels / 4        */
+    int32_t wave_add;      /*   + wave_add ((0, 0) -> (2, 4)); if max_waves == 0   */
+    int32_t schedule;      /* push phase: 0 waves, 1 asynchronous work queue       */
     int32_t async_budget;  /* async: items per active vertex per round (0 -> 16)   */
 } mfx_params;
 

@@ -597,8 +597,8 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.kc = (int)kc;
   cfg.topology = p->mode;
   cfg.max_waves = p->max_waves;
-  cfg.async = p->schedule == 0;
-  if (const char *sch = getenv("MFX_SCHEDULE")) cfg.async = sch[0] != 'w';
+  cfg.async = p->schedule == 1;
+  if (const char *sch = getenv("MFX_SCHEDULE")) cfg.async = sch[0] == 'a';
   if (p->async_budget > 0) cfg.async_budget = p->async_budget;
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;

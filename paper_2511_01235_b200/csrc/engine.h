@@ -82,9 +82,9 @@ struct SolveConfig {
   int forbidden = -1;  // vertex never discovered (s in dynamic mode)
   int kc = 1;
   int max_waves = 0;
-  int wave_mult = 2;  // auto wave budget per round: wave_mult * BFS levels + wave_add
-  int wave_add = 16;
-  int async = 1;          // asynchronous push phase (work queue) instead of waves
+  int wave_mult = 2;  // auto wave budget per round: wave_mult * BFS levels / 4 + wave_add
+  int wave_add = 4;
+  int async = 0;          // asynchronous push phase (work queue) instead of waves
   int async_budget = 16;  // items per initially active vertex before a global relabel
   int topology = 0;
   double timeout_s = 600.0;

@@ -46,6 +46,7 @@ enum CtrIdx {
   C_BASES = 8,   // bases list
   C_HEAVY = 9,   // heavy rows (finalize)
   C_ACTIVE = 10, // active vertices discovered by the global relabel
+  C_HUGE = 11,   // huge rows (finalize)
   C_NCTR = 16
 };
 

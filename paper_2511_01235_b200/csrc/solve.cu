@@ -1106,24 +1106,33 @@ struct Kern {
     for (int j = gtid; j < nb; j += gthreads) f += ldcg(a.ex + ldcg(a.bases + j));
     f = block_sum(f, scr);
     if (threadIdx.x == 0 && f) atomicAdd((unsigned long long *)&a.ctrl->flow, (unsigned long long)f);
+    // A-side rows: light ones inline; heavy rows (CTA each) listed from the
+    // front of `heavy`, huge rows (> kBin2Max slots, e.g. the source of the
+    // grid config with ~2.1 M slots; whole grid each) from the back.
     long long c = 0;
     for (int u = gtid; u < n; u += gthreads) {
       if (ldcg(a.h + u) != n) continue;
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       if (hi - lo > 64) {
-        int p = atomicAdd(a.ctrl->live + C_HEAVY, 1);
-        a.heavy[p] = u;
+        if (hi - lo > kBin2Max) a.heavy[n - 1 - atomicAdd(a.ctrl->live + C_HUGE, 1)] = u;
+        else a.heavy[atomicAdd(a.ctrl->live + C_HEAVY, 1)] = u;
         continue;
       }
       for (int i = lo; i < hi; ++i)
         if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
     }
-    grid_sync(a.ctrl, sy, 1u << C_HEAVY, 0, 0, PH_FINAL);
-    int nh = sy.s_snap[C_HEAVY];
+    grid_sync(a.ctrl, sy, (1u << C_HEAVY) | (1u << C_HUGE), 0, 0, PH_FINAL);
+    int nh = sy.s_snap[C_HEAVY], ng = sy.s_snap[C_HUGE];
     for (int j = blockIdx.x; j < nh; j += gridDim.x) {
       int u = ldcg(a.heavy + j);
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
+        if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
+    }
+    for (int j = 0; j < ng; ++j) {
+      int u = ldcg(a.heavy + n - 1 - j);
+      int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+      for (int i = lo + gtid; i < hi; i += gthreads)
         if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
     }
     c = block_sum(c, scr);
@@ -1177,7 +1186,7 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
   } else if (a.what == WHAT_ROUND) {
     int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
     if (a.async) k.push_round_async(stamp, scr);
-    else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
+    else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
     if (k.gtid == 0) *a.stamp = stamp;
   } else {
     bool final = true;
@@ -1188,7 +1197,7 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
         if (k.gtid == 0) a.ctrl->active = act;
         if (act == 0 || s_abort) break;
         if (a.async) k.push_round_async(stamp, scr);
-        else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L + a.wave_add);
+        else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
         if (s_abort) break;
       }
       if (k.gtid == 0) *a.stamp = stamp;

@@ -26,7 +26,7 @@ class SolverError(RuntimeError):
 L.register_error(L.MFX_SOLVER_ERROR, SolverError)
 
 MODES = ("data", "topology")
-SCHEDULES = ("async", "waves")  # device push-phase schedule (not a reference knob)
+SCHEDULES = ("waves", "async")  # device push-phase schedule (not a reference knob)
 
 
 def operation_ceiling(n: int, m_original: int) -> int:
@@ -57,7 +57,7 @@ class SolverParams:
     blocks_per_sm: int = 0
     wave_mult: int = 0
     wave_add: int = 0
-    schedule: str = "async"
+    schedule: str = "waves"
     async_budget: int = 0
 
     def resolve_threads(self) -> int:

@@ -257,8 +257,9 @@ def test_random_vs_oracle(mf, seed):
     m = int(rng.integers(1, 4000))
     us, vs, caps, s, t = gen.random_graph(n, m, seed)
     knobs = [dict(), dict(kernel_cycles=1), dict(kernel_cycles=64), dict(mode="topology"),
-             dict(schedule="waves", max_waves=1), dict(schedule="waves", max_waves=3, kernel_cycles=2),
-             dict(schedule="waves"), dict(async_budget=1), dict(async_budget=2, kernel_cycles=3),
+             dict(max_waves=1), dict(max_waves=3, kernel_cycles=2),
+             dict(schedule="async"), dict(schedule="async", async_budget=1),
+             dict(schedule="async", async_budget=2, kernel_cycles=3),
              dict(blocks_per_sm=1)][seed % 10]
     params = mf.SolverParams(**knobs)
     g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
