@@ -63,6 +63,8 @@ typedef struct {
     int32_t wave_add;      /*   + wave_add ((0, 0) -> (2, 4)); if max_waves == 0   */
     int32_t schedule;      /* push phase: 0 waves, 1 asynchronous work queue       */
     int32_t async_budget;  /* async: items per active vertex per round (0 -> 16)   */
+    int32_t bfs_local;     /* CTA-local BFS sub-levels per grid barrier: 0 -> 32,   */
+    int32_t pad_;          /*   < 0 -> strict level-synchronous BFS                */
 } mfx_params;
 
 /* FlowResult (solver.py:108-118) plus device counters. */
@@ -79,6 +81,7 @@ typedef struct {
     int32_t status;
     int32_t launches;       /* kernels launched by this call                            */
     int64_t async_items;    /* vertices processed by asynchronous push phases           */
+    int64_t bfs_epochs;     /* grid barriers spent in global relabels                   */
 } mfx_result;
 
 /* mfx_verify report: the checks of oracle.py construct_flow / verify_preflow /

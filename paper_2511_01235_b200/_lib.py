@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmfx.so")
+# $MFX_LIB_PATH: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("MFX_LIB_PATH") or os.path.join(_HERE, "_lib", "libmfx.so")
 
 MFX_OK = 0
 MFX_GRAPH_ERROR = 1
@@ -38,7 +39,7 @@ class Params(ctypes.Structure):
     _fields_ = [("kernel_cycles", i64), ("mode", i32), ("max_waves", i32),
                 ("timeout_s", ctypes.c_double), ("blocks_per_sm", i32), ("flags", i32),
                 ("wave_mult", i32), ("wave_add", i32), ("schedule", i32),
-                ("async_budget", i32)]
+                ("async_budget", i32), ("bfs_local", i32), ("pad_", i32)]
 
 
 class Result(ctypes.Structure):
@@ -48,7 +49,7 @@ class Result(ctypes.Structure):
                 ("ns_push", ctypes.c_double), ("ns_repair", ctypes.c_double),
                 ("ms_update", ctypes.c_double), ("ms_solve", ctypes.c_double),
                 ("ms_total", ctypes.c_double), ("status", i32), ("launches", i32),
-                ("async_items", i64)]
+                ("async_items", i64), ("bfs_epochs", i64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -65,6 +65,7 @@ Workspace::~Workspace() {
   dfree(bases);
   dfree(heavy);
   dfree(mark);
+  dfree(bmark);
   dfree(stamp);
   dfree(vbin);
   dfree(rdirty);
@@ -141,6 +142,8 @@ cudaError_t ensure_workspace(Topology &t) {
   }
   if ((e = cudaMalloc(&w.vbin, n))) return e;
   if ((e = launch_vbin(t, w.vbin))) return e;
+  if ((e = cudaMalloc(&w.bmark, sizeof(int) * n))) return e;
+  if ((e = cudaMemsetAsync(w.bmark, 0, sizeof(int) * n, t.stream))) return e;
   if ((e = cudaMalloc(&w.mark, sizeof(unsigned) * n))) return e;
   return cudaMemsetAsync(w.mark, 0, sizeof(unsigned) * n, t.stream);
 }
@@ -600,6 +603,8 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.async = p->schedule == 1;
   if (const char *sch = getenv("MFX_SCHEDULE")) cfg.async = sch[0] == 'a';
   if (p->async_budget > 0) cfg.async_budget = p->async_budget;
+  if (p->bfs_local != 0) cfg.bfs_local = p->bfs_local < 0 ? 0 : p->bfs_local;
+  if (const char *bl = getenv("MFX_BFS_LOCAL")) cfg.bfs_local = atoi(bl) < 0 ? 0 : atoi(bl);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;
@@ -628,6 +633,7 @@ static void fill_result(const mfx_state *st, mfx_result *r) {
   r->ns_repair = (double)c.phase_ns[PH_REPAIR];
   r->status = c.status;
   r->async_items = (int64_t)c.async_items;
+  r->bfs_epochs = (int64_t)c.epochs;
 }
 
 static int solve_status(const mfx_state *st, mfx_result *r) {

@@ -22,6 +22,7 @@ struct Workspace {
   int *bases = nullptr;  // last global relabel's base set, capacity n
   int *heavy = nullptr;  // heavy rows scratch, capacity n
   unsigned *mark = nullptr;  // wave stamps, n
+  int *bmark = nullptr;      // BFS epoch stamps (next-frontier dedupe), n
   unsigned *stamp = nullptr; // current wave stamp (1 word)
   uint8_t *vbin = nullptr;   // degree class per vertex, n
   int *rdirty = nullptr;     // NBIN: used extent of each R list (reset to -1 before reuse)
@@ -86,6 +87,7 @@ struct SolveConfig {
   int wave_add = 4;
   int async = 0;          // asynchronous push phase (work queue) instead of waves
   int async_budget = 16;  // items per initially active vertex before a global relabel
+  int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;
   int blocks_per_sm = 0;

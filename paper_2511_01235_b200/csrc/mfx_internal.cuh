@@ -31,6 +31,7 @@ constexpr int NBIN = 4;  // 0: thread/vertex, 1: warp/vertex, 2: CTA/vertex, 3: 
 constexpr int kBin0Max = 8;
 constexpr int kBin1Max = 1024;
 constexpr int kBin2Max = 65536;
+constexpr int kLQ = 2048;  // CTA-local BFS queue (per buffer)
 
 __host__ __device__ inline int bin_of(int deg) {
   return deg <= kBin0Max ? 0 : deg <= kBin1Max ? 1 : deg <= kBin2Max ? 2 : 3;
@@ -47,6 +48,8 @@ enum CtrIdx {
   C_HEAVY = 9,   // heavy rows (finalize)
   C_ACTIVE = 10, // active vertices discovered by the global relabel
   C_HUGE = 11,   // huge rows (finalize)
+  C_REACHED = 12, // vertices reached by the global relabel (bases + first discoveries)
+  C_DEPTH = 13,  // largest BFS label set (max-combined, not summed)
   C_NCTR = 16
 };
 
@@ -78,6 +81,7 @@ struct Ctrl {
   int aq_stop;
   int aq_pad;
   unsigned long long async_items;  // items processed by asynchronous push phases
+  unsigned long long epochs;       // grid barriers spent in global relabels
 };
 
 // ---- small device helpers -------------------------------------------------

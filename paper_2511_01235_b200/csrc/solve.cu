@@ -45,6 +45,8 @@ struct SolveArgs {
   int async;         // asynchronous push phase (data mode only)
   int async_budget;  // items per initially active vertex before the next global relabel
   int *rdirty;       // NBIN used extents of the R lists (device, shared by states)
+  int bfs_local;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
+  int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
   int what;
   int rcap;
@@ -135,7 +137,7 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
 #pragma unroll
       for (int i = 0; i < C_NCTR; ++i) {
         if (rd >> i & 1) {
-          vc->snap[i] = lv[i] + sv[i];
+          vc->snap[i] = i == C_DEPTH ? (lv[i] > sv[i] ? lv[i] : sv[i]) : lv[i] + sv[i];
           vc->live[i] = 0;
         } else if (clear_mask >> i & 1) {
           vc->snap[i] = 0;
@@ -339,51 +341,100 @@ struct Kern {
   }
 
   // =========================================================================
-  // global relabel (kernels.py:168-215) as a level-synchronous frontier BFS
+  // global relabel (kernels.py:168-215)
   // =========================================================================
+  // Frontier BFS over reverse residual slots with label-correcting relaxation
+  // (atomicMin on h): between two grid barriers ("epoch") a CTA may expand
+  // its own light discoveries for up to `local_levels` further BFS
+  // sub-levels, staged in a shared-memory queue and separated by
+  // __syncthreads only.  Heavy rows, queue overflow and the last sub-level's
+  // discoveries go to the global next frontier (deduplicated per epoch by an
+  // epoch stamp).  Every lowering of h[v] schedules an expansion of v that
+  // re-reads h[v], so the fixpoint is the exact BFS distance (bit-exact with
+  // the reference's FIFO BFS, tested); local_levels = 0 is the strict
+  // level-synchronous BFS with one grid barrier per level.
   unsigned ep_next;  // ownership stamp of the coming asynchronous push phase
+  unsigned bst;      // this epoch's stamp for next-frontier dedupe
+  int disc_cnt;      // first discoveries (+ bases) by this lane
+  int max_lab;       // largest label this lane set
+  bool loc_ok;       // discoveries may go to the CTA-local queue
+  bool loc_any;      // label-correcting mode (local_levels > 0)
+  int lq_nx;         // CTA-local queue receiving discoveries
+  int *lqb;          // CTA-local queues (shared memory, 2 x kLQ)
+  int *lq_cnt;       // their fill counters (shared memory)
 
-  __device__ __forceinline__ void discover_post(bool disc, int v, int b, bool act, int *const *Fn,
-                                                const int *rbase, const int *zero) {
-    act_cnt += act;
-    if (act && a.async) a.mark[v] = ep_next;  // queued for the push phase = owned
-    append_binned(0, disc, v, b, a.ctrl->live + C_FNEXT, Fn, zero, a.n);
-    append_binned(1, act && !a.topology, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap);
-  }
-
-  // Discovery through slot i (valid lanes only) of a frontier vertex: the
-  // reverse residual cf[rev i] is read as pc[i] - cf[i] from the same row.
-  __device__ __forceinline__ void discover_slot(bool valid, int i, int L, int *const *Fn,
-                                                const int *rbase, const int *zero) {
-    const int n = a.n;
-    int v = valid ? __ldg(a.adj + i) : 0;
-    bool disc = false;
-    if (valid && v != a.forbidden) {
-      CapT r = __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i));
-      if (r > 0 && ldcg(a.h + v) == n) disc = atomicCAS(a.h + v, n, L + 1) == n;
-    }
+  // Label of v lowered (low) to nl; first = v was unreached.  Warp-synchronous.
+  __device__ __forceinline__ void discovered(bool low, bool first, int v, int nl, int *const *Fn,
+                                             const int *rbase, const int *zero) {
     int b = 0;
     bool act = false;
-    if (disc) {
+    if (low) {
       b = vbin(v);
-      act = v != a.s && v != a.t && ldcg(a.ex + v) > 0;
-      lc.bytes += Bytes<CapT>::kDisc;
+      max_lab = nl > max_lab ? nl : max_lab;
+      if (first) {
+        ++disc_cnt;
+        act = v != a.s && v != a.t && ldcg(a.ex + v) > 0;
+        lc.bytes += Bytes<CapT>::kDisc;
+      }
     }
-    discover_post(disc, v, b, act, Fn, rbase, zero);
+    act_cnt += act;
+    if (act && a.async) a.mark[v] = ep_next;  // queued for the push phase = owned
+    append_binned(1, act && !a.topology, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap);
+    bool glob = low;
+    if (loc_ok) {  // light vertex: expand it in this CTA's next sub-level
+      bool l = low && b == 0;
+      unsigned m = __ballot_sync(FULL, l);
+      if (m) {
+        int leader = __ffs(m) - 1, pos0 = 0;
+        if (lane == leader) pos0 = atomicAdd(lq_cnt + lq_nx, __popc(m));
+        pos0 = __shfl_sync(FULL, pos0, leader);
+        int p = pos0 + __popc(m & lanemask_lt());
+        if (l && p < kLQ) {
+          lqb[lq_nx * kLQ + p] = v;
+          glob = false;
+        }
+      }
+    }
+    // once per epoch in the global list: a first discovery cannot be listed
+    // yet; a re-lowered vertex may be (label-correcting mode only)
+    if (glob && !first && loc_any) glob = atomicMax(a.bmark + v, bst) < bst;
+    else if (glob && loc_any) a.bmark[v] = bst;
+    append_binned(0, glob, v, b, a.ctrl->live + C_FNEXT, Fn, zero, a.n);
+  }
+
+  __device__ __forceinline__ bool relax(int v, int nl, bool &first) {
+    int old = atomicMin(a.h + v, nl);
+    first = old == a.n;
+    return nl < old;
+  }
+
+  // Discovery through slot i (valid lanes) of a frontier vertex at label
+  // nl - 1: the reverse residual cf[rev i] is read as pc[i] - cf[i] from the
+  // same row.
+  __device__ __forceinline__ void discover_slot(bool valid, int i, int nl, int *const *Fn,
+                                                const int *rbase, const int *zero) {
+    int v = valid ? __ldg(a.adj + i) : 0;
+    bool low = false, first = false;
+    if (valid && v != a.forbidden) {
+      CapT r = __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i));
+      if (r > 0 && ldcg(a.h + v) > nl) low = relax(v, nl, first);
+    }
+    discovered(low, first, v, nl, Fn, rbase, zero);
   }
 
   // Thread-per-vertex expansion for rows of <= kBin0Max slots: every load of
   // the row is issued before any result is consumed (ILP instead of a
   // dependent chain per slot).
-  __device__ __forceinline__ void expand_thread(bool valid, int u, int L, int *const *Fn,
-                                                const int *rbase, const int *zero) {
-    const int n = a.n;
-    int lo = 0, d = 0;
+  __device__ __forceinline__ void expand_thread(bool valid, int u, int *const *Fn, const int *rbase,
+                                                const int *zero) {
+    int lo = 0, d = 0, hu = a.n;
     if (valid) {
       lo = __ldg(a.off + u);
       d = __ldg(a.off + u + 1) - lo;
+      hu = ldcg(a.h + u);
       lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kBfsSlot;
     }
+    const int nl = hu + 1;
     int vv[kBin0Max], hv[kBin0Max];
     CapT rr[kBin0Max];
 #pragma unroll
@@ -394,21 +445,14 @@ struct Kern {
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k)  // head heights across residual slots only
       hv[k] = (rr[k] > 0 && vv[k] != a.forbidden) ? ldcg(a.h + vv[k]) : -1;
-    bool disc[kBin0Max];
-#pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) disc[k] = hv[k] == n && atomicCAS(a.h + vv[k], n, L + 1) == n;
-    int bb[kBin0Max];
-    bool act[kBin0Max];
+    bool low[kBin0Max], first[kBin0Max];
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) {
-      bb[k] = disc[k] ? vbin(vv[k]) : 0;
-      act[k] = disc[k] && vv[k] != a.s && vv[k] != a.t && ldcg(a.ex + vv[k]) > 0;
+      first[k] = false;
+      low[k] = hv[k] > nl && relax(vv[k], nl, first[k]);
     }
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) {
-      if (disc[k]) lc.bytes += Bytes<CapT>::kDisc;
-      discover_post(disc[k], vv[k], bb[k], act[k], Fn, rbase, zero);
-    }
+    for (int k = 0; k < kBin0Max; ++k) discovered(low[k], first[k], vv[k], nl, Fn, rbase, zero);
   }
 
   __device__ void level_flush(int *const *Fn, const int *rbase) {
@@ -417,16 +461,37 @@ struct Kern {
     int c = warp_sum(act_cnt);
     if (lane == 0 && c) atomicAdd(a.ctrl->live + C_ACTIVE, c);
     act_cnt = 0;
+    c = warp_sum(disc_cnt);
+    if (lane == 0 && c) atomicAdd(a.ctrl->live + C_REACHED, c);
+    disc_cnt = 0;
+    int m = max_lab;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      int w = __shfl_xor_sync(FULL, m, o);
+      m = w > m ? w : m;
+    }
+    if (lane == 0 && m) atomicMax(a.ctrl->live + C_DEPTH, m);
   }
 
-  // returns the number of BFS levels; the active set is left in R (wave 0).
-  // ep: ownership stamp the following asynchronous push phase will use.
-  __device__ int bfs(unsigned ep) {
+  // Returns the BFS depth (levels incl. level 0 = max label + 1); the active
+  // set is left in R (wave 0).  ep: ownership stamp the following
+  // asynchronous push phase will use; bstamp: persistent epoch stamp.
+  __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels) {
     const int n = a.n;
     __shared__ int zero[NBIN];
     __shared__ int rb[NBIN];
+    __shared__ int s_lq[2][kLQ];
+    __shared__ int s_lqc[2];
     ep_next = ep;
+    disc_cnt = 0;
+    max_lab = 0;
+    loc_ok = false;
+    loc_any = local_levels > 0;
+    lqb = &s_lq[0][0];
+    lq_cnt = s_lqc;
+    lq_nx = 0;
     if (threadIdx.x < NBIN) zero[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_lqc[threadIdx.x] = 0;
     __syncthreads();
     // empty the R lists (async consumers wait on -1 slots) and the async counters
     if (!a.topology) {  // (topology mode seeds R below and never runs asynchronously)
@@ -451,6 +516,7 @@ struct Kern {
       bool base = valid && (v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0));
       if (v == a.forbidden) base = false;
       if (valid) a.h[v] = base ? 0 : n;
+      disc_cnt += base;
       int b = base ? vbin(v) : 0;
       append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
       direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
@@ -461,10 +527,9 @@ struct Kern {
     level_flush(a.F0, zero);
     lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
     const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
-    const unsigned amask = 1u << C_ACTIVE;
+    const unsigned amask = (1u << C_ACTIVE) | (1u << C_REACHED) | (1u << C_DEPTH);
     grid_sync(a.ctrl, sy, fmask | (1u << C_BASES), rmask | amask, rmask | amask, PH_BFS);
-    long long reached = 0;
-    int L = 0;
+    int E = 0;
     for (;;) {
       int cnt[NBIN];
       int tot = 0;
@@ -474,58 +539,84 @@ struct Kern {
         tot += cnt[b];
       }
       if (tot == 0 || *sy.s_abort) break;
-      reached += tot;
       if (threadIdx.x < NBIN) rb[threadIdx.x] = sy.s_snap[C_RNEXT + threadIdx.x];
       __syncthreads();
-      int *const *Fc = (L & 1) ? a.F1 : a.F0;
-      int *const *Fn = (L & 1) ? a.F0 : a.F1;
+      bst = ++bstamp;
+      loc_ok = local_levels > 0;
+      int *const *Fc = (E & 1) ? a.F1 : a.F0;
+      int *const *Fn = (E & 1) ? a.F0 : a.F1;
       // bin 0: thread per vertex (warp-uniform trip count)
       for (int j0 = gwarp * 32; j0 < cnt[0]; j0 += gwarps * 32) {
         int j = j0 + lane;
         bool valid = j < cnt[0];
-        expand_thread(valid, valid ? ldcg(Fc[0] + j) : 0, L, Fn, rb, zero);
+        expand_thread(valid, valid ? ldcg(Fc[0] + j) : 0, Fn, rb, zero);
       }
       // bin 1: warp per vertex
       for (int j = gwarp; j < cnt[1]; j += gwarps) {
         int u = ldcg(Fc[1] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        int nl = ldcg(a.h + u) + 1;
         if (lane == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, L, Fn, rb, zero);
+        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl, Fn, rb, zero);
       }
       // bin 2: CTA per vertex
       for (int j = blockIdx.x; j < cnt[2]; j += gridDim.x) {
         int u = ldcg(Fc[2] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        int nl = ldcg(a.h + u) + 1;
         if (threadIdx.x == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i0 = lo; i0 < hi; i0 += blockDim.x) {
           int i = i0 + threadIdx.x;
-          discover_slot(i < hi, i, L, Fn, rb, zero);
+          discover_slot(i < hi, i, nl, Fn, rb, zero);
         }
       }
       // bin 3: whole grid per vertex
       for (int j = 0; j < cnt[3]; ++j) {
         int u = ldcg(Fc[3] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+        int nl = ldcg(a.h + u) + 1;
         if (gtid == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i0 = lo + gwarp * 32; i0 < hi; i0 += gthreads) {
           int i = i0 + lane;
-          discover_slot(i < hi, i, L, Fn, rb, zero);
+          discover_slot(i < hi, i, nl, Fn, rb, zero);
         }
       }
+      // CTA-local sub-levels over this CTA's own light discoveries
+      for (int sub = 1; sub <= local_levels; ++sub) {
+        __syncthreads();
+        const int cur = lq_nx;
+        int c = s_lqc[cur];
+        __syncthreads();
+        if (c == 0) break;
+        if (c > kLQ) c = kLQ;
+        if (threadIdx.x == 0) s_lqc[cur] = 0;  // cur becomes the receiver after next
+        lq_nx = cur ^ 1;
+        loc_ok = sub < local_levels;
+        for (int j0 = wib * 32; j0 < c; j0 += kWarps * 32) {
+          int j = j0 + lane;
+          bool valid = j < c;
+          expand_thread(valid, valid ? lqb[cur * kLQ + j] : 0, Fn, rb, zero);
+        }
+      }
+      loc_ok = false;
       level_flush(Fn, rb);
       grid_sync(a.ctrl, sy, fmask, rmask | amask, 0, PH_BFS);
-      ++L;
+      ++E;
     }
+    __syncthreads();
+    if (threadIdx.x < 2) s_lqc[threadIdx.x] = 0;
+    const int depth = sy.s_snap[C_DEPTH] + 1;
     if (gtid == 0) {
-      a.ctrl->levels += L;
-      a.ctrl->last_levels = L;
-      a.ctrl->reached = reached;
+      a.ctrl->levels += depth;
+      a.ctrl->epochs += E;
+      a.ctrl->last_levels = depth;
+      a.ctrl->reached = sy.s_snap[C_REACHED];
       for (int b = 0; b < NBIN; ++b) a.rdirty[b] = sy.s_snap[C_RNEXT + b];
     }
-    return L;
+    return depth;
   }
 
   // =========================================================================
@@ -1177,22 +1268,22 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
   __syncthreads();
   Kern<CapT> k(a, sy, lc, wq, &s_sink);
   unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
+  unsigned bstamp = ((volatile unsigned *)a.stamp)[1];  // persistent BFS epoch stamp
   if (a.what == WHAT_BARRIER) {  // barrier latency microbenchmark (kc iterations)
     for (int i = 0; i < a.kc && !s_abort; ++i) grid_sync(a.ctrl, sy, 0, 0, 0, PH_FINAL);
   } else if (a.what == WHAT_BFS) {
-    k.bfs(stamp + 1);
+    k.bfs(stamp + 1, bstamp, a.bfs_local);
     if (k.gtid == 0) a.ctrl->active = (long long)s_snap[C_ACTIVE];
     flush_counters(a.ctrl, lc, scr);
   } else if (a.what == WHAT_ROUND) {
     int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
     if (a.async) k.push_round_async(stamp, scr);
     else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
-    if (k.gtid == 0) *a.stamp = stamp;
   } else {
     bool final = true;
     if (a.what == WHAT_SOLVE) {
       for (;;) {
-        int L = k.bfs(stamp + 1);
+        int L = k.bfs(stamp + 1, bstamp, a.bfs_local);
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
         if (act == 0 || s_abort) break;
@@ -1200,11 +1291,14 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
         else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
         if (s_abort) break;
       }
-      if (k.gtid == 0) *a.stamp = stamp;
       flush_counters(a.ctrl, lc, scr);
       final = !s_abort;
     }
     if (final) k.finalize((long long *)scr);
+  }
+  if (k.gtid == 0) {  // persistent stamps (every thread advanced identical copies)
+    a.stamp[0] = stamp;
+    a.stamp[1] = bstamp;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // device phase times (block 0's view)
     unsigned long long now = globaltimer();
@@ -1231,6 +1325,7 @@ __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long 
     for (int i = 0; i < PH_N; ++i) c->phase_ns[i] = 0;
     c->pushes = c->relabels = c->repairs = c->rounds = c->levels = c->waves = c->bytes = 0;
     c->async_items = 0;
+    c->epochs = 0;
   }
 }
 
@@ -1255,6 +1350,8 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.async = cfg.async && !cfg.topology;
   a.async_budget = cfg.async_budget;
   a.rdirty = W.rdirty;
+  a.bfs_local = cfg.bfs_local;
+  a.bmark = W.bmark;
   a.topology = cfg.topology;
   a.what = cfg.what;
   a.rcap = W.rcap;

@@ -44,7 +44,9 @@ class SolverParams:
     ignored: the device schedule is always massively parallel and the flow
     value does not depend on it.  Device knobs: ``max_waves`` (push waves per
     round before the next global relabel, 0 = until the active list drains),
-    ``timeout_s`` (device watchdog; 0 = $MFX_TIMEOUT_S or 600 s), ``blocks_per_sm`` (persistent grid).
+    ``timeout_s`` (device watchdog; 0 = $MFX_TIMEOUT_S or 600 s), ``blocks_per_sm`` (persistent grid),
+    ``bfs_local`` (CTA-local BFS sub-levels per grid barrier in the global
+    relabel; 0 = default 32, < 0 = strict level-synchronous BFS).
     """
 
     kernel_cycles: int = 0
@@ -59,6 +61,7 @@ class SolverParams:
     wave_add: int = 0
     schedule: str = "waves"
     async_budget: int = 0
+    bfs_local: int = 0
 
     def resolve_threads(self) -> int:
         return 1
@@ -83,7 +86,8 @@ class SolverParams:
         return L.Params(int(self.kernel_cycles), MODES.index(self.mode), int(self.max_waves),
                         float(self.timeout_s), int(self.blocks_per_sm), 0,
                         int(self.wave_mult), int(self.wave_add),
-                        SCHEDULES.index(self.schedule), int(self.async_budget))
+                        SCHEDULES.index(self.schedule), int(self.async_budget),
+                        int(self.bfs_local), 0)
 
 
 @dataclass

@@ -85,7 +85,7 @@ def main():
         r = mfx.solve_static(gg, s, t, p)
         d = r.device
         row = {"knobs": spec or "default", "static_ms": round(d["ms_total"], 2),
-               "st_rounds": r.rounds, "st_levels": d["bfs_levels"], "st_waves": d["waves"],
+               "st_rounds": r.rounds, "st_levels": d["bfs_levels"], "st_epochs": d["bfs_epochs"], "st_waves": d["waves"],
                "st_bfs_ms": round(d["ns_bfs"] / 1e6, 2), "st_push_ms": round(d["ns_push"] / 1e6, 2),
                "st_repair_ms": round(d["ns_repair"] / 1e6, 2), "st_pushes": r.pushes,
                "st_relabels": r.relabels, "st_GBs": round(d["bytes_alg"] / d["ms_solve"] / 1e6, 1)}
@@ -97,13 +97,14 @@ def main():
             flows.append(rr.flow_value)
             dd = rr.device
             dyn.append((dd["ms_total"], rr.rounds, dd["bfs_levels"], dd["waves"], dd["ns_bfs"] / 1e6,
-                        dd["ns_push"] / 1e6, dd["ns_repair"] / 1e6, dd["ms_update"]))
+                        dd["ns_push"] / 1e6, dd["ns_repair"] / 1e6, dd["ms_update"], dd["bfs_epochs"]))
             st = rr.state
         a = np.array(dyn)
         row.update({"dyn_ms": round(a[:, 0].mean(), 2), "dyn_rounds": round(a[:, 1].mean(), 1),
                     "dyn_levels": round(a[:, 2].mean(), 1), "dyn_waves": round(a[:, 3].mean(), 1),
                     "dyn_bfs_ms": round(a[:, 4].mean(), 2), "dyn_push_ms": round(a[:, 5].mean(), 2),
-                    "dyn_repair_ms": round(a[:, 6].mean(), 2), "dyn_update_ms": round(a[:, 7].mean(), 3)})
+                    "dyn_repair_ms": round(a[:, 6].mean(), 2), "dyn_update_ms": round(a[:, 7].mean(), 3),
+                    "dyn_epochs": round(a[:, 8].mean(), 1)})
         rep = mfx.verify_gpu(st, gg, flows[-1])
         row["verified"] = rep.ok
         if ref_flows is None:
