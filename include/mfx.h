@@ -192,6 +192,66 @@ int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int6
 /* Host<->device bytes one mfx_solve_dynamic call of k updates moves. */
 int mfx_transfer_bytes(int64_t k, int64_t *h2d, int64_t *d2h);
 
+/* ---- vertex-range partition (config C5, > 2^31 slots) ------ */
+/* Part `rank` of `nparts` owns vertices [bounds[rank], bounds[rank+1]) and
+ * their rows of the global Bi-CSR (graph.py:126-174, same slot order), with
+ * local slot indices.  Peers reach each other's arrays through device
+ * pointers: mfx_part_attach_local (parts of one process, same GPU or NVLink
+ * P2P between GPUs) or mfx_part_export / mfx_part_attach (CUDA IPC, one
+ * process per GPU; the blobs travel over torch.distributed).  The host drives
+ * the reference round loop (solver.py:204-241) one phase at a time with a
+ * barrier + all-reduce between phases (paper_2511_01235_b200/partition.py). */
+typedef struct mfx_part mfx_part;
+enum {
+    MFX_PH_LINK = 0,          /* rev[] by binary search in the owner's row      */
+    MFX_PH_LINK_PC = 1,       /* pair sums cap0[i] + cap0[rev i]                */
+    MFX_PH_INIT = 2,          /* init_residuals (state.py:30-39)               */
+    MFX_PH_SATURATE = 3,      /* saturate_source (state.py:42-59); a0 = gated  */
+    MFX_PH_BFS_INIT = 4,      /* a0 = dynamic bases (dynamic.py:119-133)       */
+    MFX_PH_BFS_EXPAND = 5,    /* a: L, cur, cnt0, cnt1, dyn (kernels.py:168-215) */
+    MFX_PH_SWAP = 6,          /* -> counters: fn0 fn1 rt0 rt1 active reached ovf bases */
+    MFX_PH_PUSH = 7,          /* a: b0 e0 b1 e1 kc stamp (kernels.py:19-67)    */
+    MFX_PH_REPAIR = 8,        /* a: e0 e1 (kernels.py:70-93)                   */
+    MFX_PH_FINAL = 9,         /* a0 = #bases -> flow, cut partials             */
+    MFX_PH_ACTIVE = 10,       /* -> active vertices (state.py:62-67)           */
+    MFX_PH_BATCH_RESOLVE = 11,/* -> error block (dynamic.py:63-88)             */
+    MFX_PH_BATCH_APPLY = 12,  /* a0 = apply (dynamic.py:103-104)               */
+    MFX_PH_BATCH_FIX = 13     /* pair sums + negative repair (dynamic.py:105-109) */
+};
+/* Edge arrays in device memory of `device` (any edges; those touching the
+ * owned range are selected on the device). */
+int mfx_part_create(int64_t n, int nparts, int rank, const int64_t *bounds, int64_t m,
+                    const int64_t *d_us, const int64_t *d_vs, const int64_t *d_caps,
+                    int64_t source, int64_t sink, int device, mfx_part **out);
+int mfx_part_create_host(int64_t n, int nparts, int rank, const int64_t *bounds, int64_t m,
+                         const int64_t *us, const int64_t *vs, const int64_t *caps,
+                         int64_t source, int64_t sink, int device, mfx_part **out);
+void mfx_part_free(mfx_part *p);
+/* info[8] = lo, hi, local slots, local original slots, round-list capacity,
+ * device, nparts, rank */
+int mfx_part_info(const mfx_part *p, int64_t *info);
+int mfx_part_export(const mfx_part *p, void *blob, int64_t cap, int64_t *len);
+int mfx_part_attach(mfx_part *p, int peer, const void *blob, int64_t len);
+int mfx_part_attach_local(mfx_part *p, const mfx_part *q);
+/* One phase (args, out: 8 x int64); synchronous at return. */
+int mfx_part_phase(mfx_part *p, int phase, const int64_t *args, int64_t *out);
+/* This part's share of an update batch; gidx = index in the whole batch,
+ * slot_base = global index of the part's first slot (error reports). */
+int mfx_part_stage_batch(mfx_part *p, int64_t k, const int64_t *us, const int64_t *vs,
+                         const int64_t *caps, const int64_t *gidx, int64_t slot_base);
+int mfx_part_download(const mfx_part *p, int64_t *off, int64_t *adj, int64_t *rev, int64_t *cap0,
+                      int64_t *cf, uint8_t *orig, int64_t *excess, int64_t *height);
+
+/* Device R-MAT edge list (gen.py rmat_graph recursion, counter-based hash
+ * stream): m = 2^scale * edge_factor edges into caller-allocated device
+ * arrays; *source / *sink = argmax out-degree / in-degree (!= source). */
+int mfx_rmat_device(int scale, int64_t edge_factor, uint64_t seed, double a, double b, double c,
+                    int device, int64_t *d_us, int64_t *d_vs, int64_t *d_caps, int64_t *source,
+                    int64_t *sink);
+/* Slot-balanced vertex-range cut of a device edge list: bounds[nparts + 1]. */
+int mfx_part_bounds_device(int64_t n, int64_t m, const int64_t *d_us, const int64_t *d_vs,
+                           int nparts, int device, int64_t *bounds);
+
 /* ---- host memory helpers (pinned staging for end-to-end timing) -------- */
 int mfx_host_alloc(size_t bytes, void **ptr);
 int mfx_host_free(void *ptr);

@@ -112,6 +112,26 @@ SIGNATURES = {
     "mfx_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(vp)]),
     "mfx_host_free": (ctypes.c_int, [vp]),
     "mfx_graph_stream": (vp, [vp]),
+    # vertex-range partition
+    "mfx_part_create": (ctypes.c_int, [i64, ctypes.c_int, ctypes.c_int, p_i64, i64, vp, vp, vp,
+                                       i64, i64, ctypes.c_int, ctypes.POINTER(vp)]),
+    "mfx_part_create_host": (ctypes.c_int, [i64, ctypes.c_int, ctypes.c_int, p_i64, i64, p_i64,
+                                            p_i64, p_i64, i64, i64, ctypes.c_int,
+                                            ctypes.POINTER(vp)]),
+    "mfx_part_free": (None, [vp]),
+    "mfx_part_info": (ctypes.c_int, [vp, p_i64]),
+    "mfx_part_export": (ctypes.c_int, [vp, vp, i64, p_i64]),
+    "mfx_part_attach": (ctypes.c_int, [vp, ctypes.c_int, vp, i64]),
+    "mfx_part_attach_local": (ctypes.c_int, [vp, vp]),
+    "mfx_part_phase": (ctypes.c_int, [vp, ctypes.c_int, p_i64, p_i64]),
+    "mfx_part_stage_batch": (ctypes.c_int, [vp, i64, p_i64, p_i64, p_i64, p_i64, i64]),
+    "mfx_part_download": (ctypes.c_int, [vp, p_i64, p_i64, p_i64, p_i64, p_i64, p_u8, p_i64,
+                                         p_i64]),
+    "mfx_rmat_device": (ctypes.c_int, [ctypes.c_int, i64, ctypes.c_uint64, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp,
+                                       vp, p_i64, p_i64]),
+    "mfx_part_bounds_device": (ctypes.c_int, [i64, i64, vp, vp, ctypes.c_int, ctypes.c_int,
+                                              p_i64]),
 }
 
 _lib = None

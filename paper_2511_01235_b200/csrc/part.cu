@@ -1,0 +1,1235 @@
+// part.cu -- vertex-range partitioned solver (config C5, R-MAT 26,
+// ~2.1 B Bi-CSR slots: more than the int32 slot layout of one device holds).
+//
+// Part r owns the vertices [lo_r, hi_r) and their Bi-CSR rows (the slot range
+// [off[lo_r], off[hi_r]) of the global layout, in the reference's slot order,
+// graph.py:143-171), with local int32 slot indices and global head ids.  For
+// every slot i, rev[i] is the index of the reverse slot inside the part that
+// owns the head, found by a binary search of that part's row over peer
+// memory.  Every array a peer touches (off, adj, cap0, pc, cf, ex, h, mark,
+// frontiers, round lists, counters) is reached through a PeerTab of device
+// pointers: same-device pointers when several parts share one GPU (tests),
+// NVLink P2P pointers when the parts of one process sit on several GPUs, or
+// CUDA IPC mappings when each GPU has its own process (torch.distributed).
+//
+// The round loop is bulk-synchronous and driven by the host, one phase per
+// call (mfx_part_phase), with a cross-part barrier + tiny all-reduce between
+// phases ("one exchange step per phase"):
+//   global relabel  level-synchronous BFS; a discovery of a remote vertex is
+//                   an atomicCAS on the owner's h plus an append to the
+//                   owner's next frontier (and its round list when active)
+//   push wave       bounded push/relabel (kernels.py:19-67) over the round
+//                   list; on a cut slot cf[i] -= d stays local, the reverse
+//                   residual and the head's excess are remote atomics
+//   repair          steep residual slots (kernels.py:70-93)
+//   finalize        local flow / cut partials, summed by the host
+// All remote-visible updates are system-scope atomics, so concurrent parts
+// (other GPUs over NVLink, other processes) combine exactly; phases are
+// separated by stream synchronisation + the host barrier.
+#include <limits.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/mfx.h"
+#include "engine.h"
+
+namespace mfx {
+
+constexpr int kMaxParts = 8;
+constexpr int kPartHeavy = 2048;  // rows above this are expanded / pushed by a whole CTA
+constexpr int kPartBlock = 256;
+
+// per-part device counters (int32, written by every part)
+enum PartCtr {
+  PC_FN0 = 0,      // next frontier fill, bin 0 / 1
+  PC_FN1 = 1,
+  PC_RT0 = 2,      // round-list tails, bin 0 / 1
+  PC_RT1 = 3,
+  PC_ACTIVE = 4,   // active vertices discovered by the global relabel
+  PC_REACHED = 5,  // vertices reached (bases + discoveries)
+  PC_OVF = 6,      // round-list overflow
+  PC_BASES = 7,
+  PC_BAD = 8,      // link: slots without a reverse
+  PC_N = 16
+};
+// per-part 64-bit statistics (local writes only)
+enum PartStat { PS_PUSH = 0, PS_RELABEL, PS_REPAIR, PS_BYTES, PS_FLOW, PS_CUT, PS_ACTIVE, PS_N = 8 };
+// batch error block (int64), LLONG_MAX = none
+enum PartErr { PE_NEG = 0, PE_UNKNOWN, PE_DUPSLOT, PE_DUPK, PE_OVER, PE_N = 8 };
+
+struct PeerTab {
+  int P;
+  int n;  // global vertex count
+  int lo[kMaxParts + 1];
+  const int *off[kMaxParts];
+  const int *adj[kMaxParts];
+  const int *cap0[kMaxParts];
+  int *pc[kMaxParts];
+  int *cf[kMaxParts];
+  long long *ex[kMaxParts];
+  int *h[kMaxParts];
+  unsigned *mark[kMaxParts];
+  int *F[kMaxParts][2][2];  // [part][buffer][bin]
+  int *R[kMaxParts][2];     // [part][bin]
+  int *ctr[kMaxParts];
+};
+
+// device buffers of one part; the order here is the IPC export order
+enum PartBuf {
+  B_OFF = 0, B_ADJ, B_CAP0, B_PC, B_CF, B_EX, B_H, B_MARK, B_F00, B_F01, B_F10, B_F11, B_R0, B_R1,
+  B_CTR, B_NBUF
+};
+
+struct PartObj {
+  int device = 0;
+  int P = 1, rank = 0;
+  long long n = 0;
+  int lo = 0, hi = 0, nl = 0;  // owned vertex range, local row count
+  int S = 0;                   // local slots
+  long long slot_base = 0;     // global index of local slot 0
+  int m_original = 0;          // local original slots
+  int s = -1, t = -1;
+  int rcap = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  void *buf[B_NBUF] = {};
+  size_t bytes[B_NBUF] = {};
+  // local-only
+  int *rev = nullptr;
+  uint8_t *orig = nullptr;
+  int *bases = nullptr;
+  unsigned long long *stat = nullptr;
+  long long *err = nullptr;
+  int *slot_first = nullptr;
+  int *bslot = nullptr;        // batch scratch
+  long long *bbuf = nullptr;   // batch staging: u, v, cap, global index
+  long long bcap = 0;
+  int bk = 0;
+  PeerTab tab;
+  bool opened[kMaxParts][B_NBUF] = {};  // IPC mappings to close
+  ~PartObj();
+};
+
+PartObj::~PartObj() {
+  cudaSetDevice(device);
+  for (int p = 0; p < kMaxParts; ++p)
+    for (int b = 0; b < B_NBUF; ++b)
+      if (opened[p][b]) {
+        void *ptr = nullptr;
+        switch (b) {
+          case B_OFF: ptr = (void *)tab.off[p]; break;
+          case B_ADJ: ptr = (void *)tab.adj[p]; break;
+          case B_CAP0: ptr = (void *)tab.cap0[p]; break;
+          case B_PC: ptr = tab.pc[p]; break;
+          case B_CF: ptr = tab.cf[p]; break;
+          case B_EX: ptr = tab.ex[p]; break;
+          case B_H: ptr = tab.h[p]; break;
+          case B_MARK: ptr = tab.mark[p]; break;
+          case B_F00: ptr = tab.F[p][0][0]; break;
+          case B_F01: ptr = tab.F[p][0][1]; break;
+          case B_F10: ptr = tab.F[p][1][0]; break;
+          case B_F11: ptr = tab.F[p][1][1]; break;
+          case B_R0: ptr = tab.R[p][0]; break;
+          case B_R1: ptr = tab.R[p][1]; break;
+          case B_CTR: ptr = tab.ctr[p]; break;
+        }
+        if (ptr) cudaIpcCloseMemHandle(ptr);
+      }
+  for (int b = 0; b < B_NBUF; ++b)
+    if (buf[b]) cudaFree(buf[b]);
+  for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)stat, (void *)err,
+                  (void *)slot_first, (void *)bslot, (void *)bbuf})
+    if (p) cudaFree(p);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+static void tab_set_self(PartObj &o, int p) {
+  PeerTab &T = o.tab;
+  T.off[p] = (const int *)o.buf[B_OFF];
+  T.adj[p] = (const int *)o.buf[B_ADJ];
+  T.cap0[p] = (const int *)o.buf[B_CAP0];
+  T.pc[p] = (int *)o.buf[B_PC];
+  T.cf[p] = (int *)o.buf[B_CF];
+  T.ex[p] = (long long *)o.buf[B_EX];
+  T.h[p] = (int *)o.buf[B_H];
+  T.mark[p] = (unsigned *)o.buf[B_MARK];
+  T.F[p][0][0] = (int *)o.buf[B_F00];
+  T.F[p][0][1] = (int *)o.buf[B_F01];
+  T.F[p][1][0] = (int *)o.buf[B_F10];
+  T.F[p][1][1] = (int *)o.buf[B_F11];
+  T.R[p][0] = (int *)o.buf[B_R0];
+  T.R[p][1] = (int *)o.buf[B_R1];
+  T.ctr[p] = (int *)o.buf[B_CTR];
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+#define PGS_LOOP(i, cnt)                                                          \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (cnt); \
+       i += (long long)gridDim.x * blockDim.x)
+
+__device__ __forceinline__ int owner_of(const PeerTab &T, int v) {
+  int p = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxParts; ++q)
+    if (q < T.P && v >= T.lo[q]) p = q;
+  return p;
+}
+__device__ __forceinline__ int vol_ld(const int *p) { return *(const volatile int *)p; }
+__device__ __forceinline__ long long vol_ld(const long long *p) {
+  return *(const volatile long long *)p;
+}
+__device__ __forceinline__ int sys_add(int *p, int v) { return atomicAdd_system(p, v); }
+__device__ __forceinline__ long long sys_add(long long *p, long long v) {
+  return (long long)atomicAdd_system((unsigned long long *)p, (unsigned long long)v);
+}
+__device__ __forceinline__ int heavy_of(const PeerTab &T, int p, int vl) {
+  return (T.off[p][vl + 1] - T.off[p][vl]) > kPartHeavy ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// build helpers
+// ---------------------------------------------------------------------------
+__global__ void part_flag_kernel(long long m, const long long *us, const long long *vs, long long lo,
+                                 long long hi, char *flag) {
+  PGS_LOOP(i, m) {
+    long long u = us[i], v = vs[i];
+    flag[i] = (u >= lo && u < hi) || (v >= lo && v < hi);
+  }
+}
+
+__global__ void part_slice_kernel(int nl, int lo, const int *goff, int *off) {
+  PGS_LOOP(i, (long long)nl + 1) off[i] = goff[lo + i] - goff[lo];
+}
+
+__global__ void part_copy_slots_kernel(long long S, long long base, const int *gadj,
+                                       const long long *gcap, const uint8_t *gorig, int *adj,
+                                       int *cap0, uint8_t *orig, unsigned long long *bad) {
+  PGS_LOOP(i, S) {
+    adj[i] = gadj[base + i];
+    long long c = gcap[base + i];
+    if (c >= (1ll << 30)) atomicAdd(bad, 1ull);
+    cap0[i] = (int)c;
+    orig[i] = gorig[base + i];
+  }
+}
+
+// rev[i]: slot of (adj[i], u) inside the part owning adj[i] (graph.py:171)
+__global__ void part_rev_kernel(PeerTab T, int me, int nl, long long S, const int *off,
+                                const int *adj, int *rev, int *ctr) {
+  PGS_LOOP(i, S) {
+    int a = 0, b = nl;  // row u: last row with off[u] <= i
+    while (b - a > 1) {
+      int mid = (a + b) >> 1;
+      if (off[mid] <= (int)i) a = mid;
+      else b = mid;
+    }
+    int ug = T.lo[me] + a;
+    int x = adj[i];
+    int p = owner_of(T, x);
+    int xl = x - T.lo[p];
+    const int *po = T.off[p], *pa = T.adj[p];
+    int lo = po[xl], hi = po[xl + 1];
+    while (lo < hi) {
+      int mid = lo + ((hi - lo) >> 1);
+      if (pa[mid] < ug) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < po[xl + 1] && pa[lo] == ug) rev[i] = lo;
+    else {
+      rev[i] = -1;
+      atomicAdd(ctr + PC_BAD, 1);
+    }
+  }
+}
+
+__global__ void part_pc_kernel(PeerTab T, int me, long long S, const int *rev, int *ctr) {
+  const int *adj = T.adj[me], *cap0 = T.cap0[me];
+  int *pc = T.pc[me];
+  PGS_LOOP(i, S) {
+    int p = owner_of(T, adj[i]);
+    long long s2 = (long long)cap0[i] + (long long)T.cap0[p][rev[i]];
+    if (s2 >= (1ll << 31)) atomicAdd(ctr + PC_BAD, 1);
+    pc[i] = (int)s2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// state
+// ---------------------------------------------------------------------------
+__global__ void part_init_kernel(PeerTab T, int me, int nl, long long S) {
+  PGS_LOOP(i, S) T.cf[me][i] = T.cap0[me][i];
+  PGS_LOOP(v, nl) {
+    T.ex[me][v] = 0;
+    T.h[me][v] = 0;
+    T.mark[me][v] = 0;
+  }
+}
+
+// saturate_source (state.py:42-59) on the part owning s: one CTA per chunk
+__global__ void part_saturate_kernel(PeerTab T, int me, int sl, const int *rev,
+                                     const long long *gate) {
+  if (gate && (gate[PE_NEG] != LLONG_MAX || gate[PE_UNKNOWN] != LLONG_MAX ||
+               gate[PE_DUPK] != LLONG_MAX || gate[PE_OVER] != LLONG_MAX))
+    return;
+  __shared__ long long part[kPartBlock / 32];
+  const int lo = T.off[me][sl], hi = T.off[me][sl + 1];
+  long long sum = 0;
+  for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < hi;
+       i += (long long)gridDim.x * blockDim.x) {
+    int d = T.cf[me][i];
+    if (d > 0) {
+      T.cf[me][i] = 0;
+      int v = T.adj[me][i];
+      int p = owner_of(T, v);
+      sys_add(T.cf[p] + rev[i], d);
+      sys_add(T.ex[p] + (v - T.lo[p]), (long long)d);
+      sum += d;
+    }
+  }
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int w = 0; w < kPartBlock / 32; ++w) tot += part[w];
+    if (tot) sys_add(T.ex[me] + sl, -tot);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// global relabel: level-synchronous BFS (kernels.py:168-215)
+// ---------------------------------------------------------------------------
+__global__ void part_bfs_init_kernel(PeerTab T, int me, int nl, int s, int t, int dyn,
+                                     int forbidden, int *bases) {
+  const int n = T.n, lo = T.lo[me];
+  int *ctr = T.ctr[me];
+  PGS_LOOP(v, nl) {
+    int g = lo + (int)v;
+    bool base = g == t || (dyn && g != s && vol_ld(T.ex[me] + v) < 0);
+    if (g == forbidden) base = false;
+    T.h[me][v] = base ? 0 : n;
+    if (base) {
+      int b = heavy_of(T, me, (int)v);
+      T.F[me][0][b][atomicAdd(ctr + PC_FN0 + b, 1)] = (int)v;
+      bases[atomicAdd(ctr + PC_BASES, 1)] = (int)v;
+      atomicAdd(ctr + PC_REACHED, 1);
+    }
+  }
+}
+
+__device__ __forceinline__ void part_discover(const PeerTab &T, int me, int i, int L, int cur, int s,
+                                              int t, int forbidden, int rcap) {
+  int v = T.adj[me][i];
+  if (v == forbidden) return;
+  int r = T.pc[me][i] - vol_ld(T.cf[me] + i);  // reverse residual cf[rev i] (pair sum)
+  if (r <= 0) return;
+  int p = owner_of(T, v);
+  int vl = v - T.lo[p];
+  int *hp = T.h[p] + vl;
+  if (vol_ld(hp) != T.n) return;
+  if (atomicCAS_system(hp, T.n, L + 1) != T.n) return;
+  int b = heavy_of(T, p, vl);
+  int pos = atomicAdd_system(T.ctr[p] + PC_FN0 + b, 1);
+  T.F[p][cur ^ 1][b][pos] = vl;
+  atomicAdd_system(T.ctr[p] + PC_REACHED, 1);
+  if (v != s && v != t && vol_ld(T.ex[p] + vl) > 0) {
+    atomicAdd_system(T.ctr[p] + PC_ACTIVE, 1);
+    int q = atomicAdd_system(T.ctr[p] + PC_RT0 + b, 1);
+    if (q < rcap) T.R[p][b][q] = vl;
+    else atomicExch_system(T.ctr[p] + PC_OVF, 1);
+  }
+}
+
+__global__ void part_bfs_expand_kernel(PeerTab T, int me, int L, int cur, int cnt0, int cnt1,
+                                       int s, int t, int forbidden, int rcap) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int gwarps = (gridDim.x * blockDim.x) >> 5;
+  const int *F0 = T.F[me][cur][0], *F1 = T.F[me][cur][1];
+  for (int j = gwarp; j < cnt0; j += gwarps) {  // warp per light row
+    int u = F0[j];
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    for (int i = lo + lane; i < hi; i += 32) part_discover(T, me, i, L, cur, s, t, forbidden, rcap);
+  }
+  for (int j = blockIdx.x; j < cnt1; j += gridDim.x) {  // CTA per heavy row
+    int u = F1[j];
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
+      part_discover(T, me, i, L, cur, s, t, forbidden, rcap);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// push wave (kernels.py:19-67): cooperative per row (warp or CTA), pushing
+// along every admissible slot at the minimum residual height in slot order
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void part_activate(const PeerTab &T, int v, unsigned stamp, int s, int t,
+                                              int rcap) {
+  if (v == s || v == t) return;
+  int p = owner_of(T, v);
+  int vl = v - T.lo[p];
+  if (atomicMax_system(T.mark[p] + vl, stamp) >= stamp) return;  // already in the next wave
+  int b = heavy_of(T, p, vl);
+  int q = atomicAdd_system(T.ctr[p] + PC_RT0 + b, 1);
+  if (q < rcap) T.R[p][b][q] = vl;
+  else atomicExch_system(T.ctr[p] + PC_OVF, 1);
+}
+
+template <int G>
+__device__ void part_push_row(const PeerTab &T, int me, int u, int kc, unsigned stamp, int s, int t,
+                              int rcap, const int *rev, unsigned long long *loc,
+                              long long *s_red) {
+  const int n = T.n;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int tid = G == 32 ? lane : threadIdx.x;
+  const int ug = T.lo[me] + u;
+  const int lo = T.off[me][u], hi = T.off[me][u + 1];
+  int *cf = T.cf[me];
+  const int *adj = T.adj[me];
+  // one read, broadcast: every thread of the group must take the same loop
+  // decisions (the CTA variant synchronises inside the loop)
+  int hu;
+  long long eu;
+  if (G == 32) {
+    hu = __shfl_sync(0xffffffffu, lane == 0 ? vol_ld(T.h[me] + u) : 0, 0);
+    eu = __shfl_sync(0xffffffffu, lane == 0 ? vol_ld(T.ex[me] + u) : 0ll, 0);
+  } else {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_red[0] = vol_ld(T.h[me] + u);
+      s_red[1] = vol_ld(T.ex[me] + u);
+    }
+    __syncthreads();
+    hu = (int)s_red[0];
+    eu = s_red[1];
+    __syncthreads();
+  }
+  for (int cnt = 0; cnt < kc; ++cnt) {
+    if (eu <= 0 || hu >= n) break;
+    unsigned long long best = ~0ull;  // (height, slot) of the first minimum (kernels.py:40-48)
+    for (int i = lo + tid; i < hi; i += G) {
+      if (vol_ld(cf + i) > 0) {
+        int v = adj[i];
+        int p = owner_of(T, v);
+        unsigned hv = (unsigned)vol_ld(T.h[p] + (v - T.lo[p]));
+        unsigned long long key = ((unsigned long long)hv << 32) | (unsigned)(i - lo);
+        best = key < best ? key : best;
+      }
+    }
+    best = warp_min_u64(best);
+    if (G > 32) {
+      __syncthreads();
+      if (lane == 0) s_red[wib] = (long long)best;
+      __syncthreads();
+      best = ~0ull;
+      for (int w = 0; w < G / 32; ++w)
+        best = (unsigned long long)s_red[w] < best ? (unsigned long long)s_red[w] : best;
+      __syncthreads();
+    }
+    if (tid == 0) loc[PS_BYTES] += 20 + 12ull * (hi - lo);
+    if (best == ~0ull) {  // no residual out-slot
+      hu = n;
+      if (tid == 0) {
+        T.h[me][u] = n;
+        loc[PS_RELABEL]++;
+      }
+      break;
+    }
+    int bh = (int)(best >> 32);
+    if (hu <= bh) {  // relabel from the scan snapshot
+      hu = bh + 1 > n ? n : bh + 1;
+      if (tid == 0) {
+        T.h[me][u] = hu;
+        loc[PS_RELABEL]++;
+      }
+      continue;
+    }
+    int first = lo + (int)(best & 0xFFFFFFFFu);
+    long long carry = 0;
+    for (int i0 = first - ((first - lo) % G); i0 < hi && carry < eu; i0 += G) {
+      int i = i0 + tid;
+      long long c = 0;
+      int v = 0, p = 0;
+      if (i < hi && i >= first) {
+        c = vol_ld(cf + i);
+        if (c > 0) {
+          v = adj[i];
+          p = owner_of(T, v);
+          if (vol_ld(T.h[p] + (v - T.lo[p])) != bh) c = 0;
+        }
+      }
+      long long incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        long long w = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += w;
+      }
+      long long tot;
+      if (G > 32) {
+        __syncthreads();
+        if (lane == 31) s_red[wib] = incl;
+        __syncthreads();
+        long long before = 0;
+        tot = 0;
+        for (int w = 0; w < G / 32; ++w) {
+          long long x = s_red[w];
+          if (w < wib) before += x;
+          tot += x;
+        }
+        incl += before;
+        __syncthreads();
+      } else {
+        tot = __shfl_sync(0xffffffffu, incl, 31);
+      }
+      long long room = eu - carry - (incl - c);
+      long long amt = room <= 0 ? 0 : (room < c ? room : c);
+      if (amt > 0) {
+        atomicAdd(cf + i, (int)-amt);
+        sys_add(T.cf[p] + rev[i], (int)amt);
+        long long old = sys_add(T.ex[p] + (v - T.lo[p]), amt);
+        loc[PS_PUSH]++;
+        loc[PS_BYTES] += 28;
+        if (old <= 0) part_activate(T, v, stamp, s, t, rcap);
+      }
+      carry += tot;
+    }
+    long long moved = carry < eu ? carry : eu;
+    if (tid == 0 && moved > 0) sys_add(T.ex[me] + u, -moved);
+    eu -= moved;
+  }
+  if (G > 32) __syncthreads();
+  if (tid == 0 && hu < n && vol_ld(T.ex[me] + u) > 0) part_activate(T, ug, stamp, s, t, rcap);
+}
+
+__global__ void part_push_kernel(PeerTab T, int me, int b0, int e0, int b1, int e1, int kc,
+                                 unsigned stamp, int s, int t, int rcap, const int *rev,
+                                 unsigned long long *stat) {
+  __shared__ long long s_red[kPartBlock / 32 + 2];
+  unsigned long long loc[PS_N] = {};
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int gwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int j = b0 + gwarp; j < e0; j += gwarps)
+    part_push_row<32>(T, me, T.R[me][0][j], kc, stamp, s, t, rcap, rev, loc, s_red);
+  for (int j = b1 + blockIdx.x; j < e1; j += gridDim.x)
+    part_push_row<kPartBlock>(T, me, T.R[me][1][j], kc, stamp, s, t, rcap, rev, loc, s_red);
+  for (int k = 0; k < 4; ++k) {
+    unsigned long long x = warp_sum(loc[k]);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(stat + k, x);
+  }
+}
+
+// repair (kernels.py:70-93) over every vertex that ran in the round
+__global__ void part_repair_kernel(PeerTab T, int me, int e0, int e1, const int *rev,
+                                   unsigned long long *stat) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int gwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long reps = 0;
+  for (int bin = 0; bin < 2; ++bin) {
+    int e = bin ? e1 : e0;
+    for (int j = gwarp; j < e; j += gwarps) {
+      int u = T.R[me][bin][j];
+      int lo = T.off[me][u], hi = T.off[me][u + 1];
+      int hu = vol_ld(T.h[me] + u);
+      for (int i = lo + lane; i < hi; i += 32) {
+        if (vol_ld(T.cf[me] + i) <= 0) continue;
+        int v = T.adj[me][i];
+        int p = owner_of(T, v);
+        int vl = v - T.lo[p];
+        if (hu > vol_ld(T.h[p] + vl) + 1) {
+          int amt = atomicExch(T.cf[me] + i, 0);
+          if (amt > 0) {
+            sys_add(T.cf[p] + rev[i], amt);
+            sys_add(T.ex[me] + u, -(long long)amt);
+            sys_add(T.ex[p] + vl, (long long)amt);
+            ++reps;
+          }
+        }
+      }
+    }
+  }
+  reps = warp_sum(reps);
+  if (lane == 0 && reps) atomicAdd(stat + PS_REPAIR, reps);
+}
+
+// flow over the local bases (dynamic.py:141-143) and the local part of the cut
+// (solver.py:178-184): original slots from A = {h == n} into B
+__global__ void part_final_kernel(PeerTab T, int me, int nl, int nb, const int *bases,
+                                  const uint8_t *orig, unsigned long long *stat) {
+  const int n = T.n, lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int gwarps = (gridDim.x * blockDim.x) >> 5;
+  long long f = 0, c = 0;
+  PGS_LOOP(j, nb) f += vol_ld(T.ex[me] + bases[j]);
+  for (int u = gwarp; u < nl; u += gwarps) {
+    if (vol_ld(T.h[me] + u) != n) continue;
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    for (int i = lo + lane; i < hi; i += 32) {
+      if (!orig[i]) continue;
+      int v = T.adj[me][i];
+      int p = owner_of(T, v);
+      if (vol_ld(T.h[p] + (v - T.lo[p])) != n) c += T.cap0[me][i];
+    }
+  }
+  f = warp_sum(f);
+  c = warp_sum(c);
+  if (lane == 0) {
+    if (f) atomicAdd(stat + PS_FLOW, (unsigned long long)f);
+    if (c) atomicAdd(stat + PS_CUT, (unsigned long long)c);
+  }
+}
+
+__global__ void part_active_kernel(PeerTab T, int me, int nl, int s, int t,
+                                   unsigned long long *stat) {
+  unsigned long long a = 0;
+  PGS_LOOP(v, nl) {
+    int g = T.lo[me] + (int)v;
+    if (g != s && g != t && T.ex[me][v] > 0 && T.h[me][v] < T.n) ++a;
+  }
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0 && a) atomicAdd(stat + PS_ACTIVE, a);
+}
+
+// ---------------------------------------------------------------------------
+// dynamic batch (dynamic.py:63-116): the host routes update j to the part
+// owning us[j]; validation first (no mutation), apply only if every part's
+// share of the batch is valid
+// ---------------------------------------------------------------------------
+__global__ void part_batch_resolve_kernel(PeerTab T, int me, long long k, const long long *bu,
+                                          const long long *bv, const long long *bc,
+                                          const long long *bj, const uint8_t *orig,
+                                          const int *rev, int *slot, int *first, long long *err) {
+  PGS_LOOP(j, k) {
+    long long c = bc[j], gj = bj[j];
+    if (c < 0) atomicMin(err + PE_NEG, gj);
+    int ul = (int)(bu[j] - T.lo[me]);
+    long long v = bv[j];
+    int i = -1;
+    if (v >= 0 && v < T.n) {
+      int lo = T.off[me][ul], hi = T.off[me][ul + 1];
+      while (lo < hi) {
+        int mid = lo + ((hi - lo) >> 1);
+        if (T.adj[me][mid] < (int)v) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < T.off[me][ul + 1] && T.adj[me][lo] == (int)v) i = lo;
+    }
+    slot[j] = i;
+    if (i < 0 || !orig[i]) {
+      atomicMin(err + PE_UNKNOWN, gj);
+    } else {
+      atomicMin(first + i, (int)gj);
+      if (c >= 0) {
+        int p = owner_of(T, (int)v);
+        if (c >= (1ll << 30) || c + (long long)T.cap0[p][rev[i]] >= (1ll << 31))
+          atomicMin(err + PE_OVER, gj);
+      }
+    }
+  }
+}
+
+__global__ void part_batch_dup_kernel(long long k, long long slot_base, const int *slot,
+                                      const int *first, const long long *bj, long long *err) {
+  PGS_LOOP(j, k) {
+    int i = slot[j];
+    if (i >= 0 && first[i] != (int)bj[j]) atomicMin(err + PE_DUPSLOT, slot_base + i);
+  }
+}
+
+__global__ void part_batch_dupidx_kernel(long long k, long long slot_base, const int *slot,
+                                         const int *first, const long long *bj, long long *err) {
+  long long ds = err[PE_DUPSLOT];
+  if (ds == LLONG_MAX) return;
+  PGS_LOOP(j, k) {
+    int i = slot[j];
+    if (i >= 0 && slot_base + i == ds && first[i] != (int)bj[j]) atomicMin(err + PE_DUPK, bj[j]);
+  }
+}
+
+__global__ void part_batch_apply_kernel(PeerTab T, int me, long long k, const long long *bc,
+                                        const int *slot, int *first, int apply) {
+  PGS_LOOP(j, k) {
+    int i = slot[j];
+    if (i < 0) continue;
+    first[i] = kFirstNone;
+    if (apply) {
+      int nc = (int)bc[j];
+      T.cf[me][i] += nc - T.cap0[me][i];
+      ((int *)T.cap0[me])[i] = nc;
+    }
+  }
+}
+
+// after every part applied: pair sums of touched pairs and the negative
+// residual repair (flow reversal, dynamic.py:105-109) with its excess move
+__global__ void part_batch_fix_kernel(PeerTab T, int me, long long k, const long long *bu,
+                                      const int *slot, const int *rev) {
+  PGS_LOOP(j, k) {
+    int i = slot[j];
+    int v = T.adj[me][i];
+    int p = owner_of(T, v);
+    int r = rev[i];
+    int pcv = T.cap0[me][i] + T.cap0[p][r];
+    T.pc[me][i] = pcv;
+    T.pc[p][r] = pcv;
+    int c = T.cf[me][i];
+    if (c < 0) {
+      T.cf[me][i] = 0;
+      sys_add(T.cf[p] + r, c);
+      sys_add(T.ex[me] + (int)(bu[j] - T.lo[me]), -(long long)c);
+      sys_add(T.ex[p] + (v - T.lo[p]), (long long)c);
+    }
+  }
+}
+
+static inline int pgrid(long long work, int sms) {
+  long long g = (work + kPartBlock - 1) / kPartBlock;
+  long long cap = (long long)sms * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace mfx
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace mfx;
+
+struct mfx_part {
+  PartObj o;
+};
+
+namespace mfx {
+static int part_fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+}  // namespace mfx
+
+#define PCK(x)                                                                         \
+  do {                                                                                 \
+    cudaError_t _e = (x);                                                              \
+    if (_e != cudaSuccess)                                                             \
+      return part_fail(MFX_CUDA_ERROR, "CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), \
+                       __FILE__, __LINE__, cudaGetErrorString(_e));                    \
+  } while (0)
+
+static int part_build(PartObj &o, long long m, const int64_t *d_us, const int64_t *d_vs,
+                      const int64_t *d_caps) {
+  cudaStream_t st = o.stream;
+  // edges incident to the owned range
+  char *flag = nullptr;
+  int64_t *sel = nullptr;
+  int *nsel = nullptr;
+  size_t M = (size_t)(m > 0 ? m : 1);
+  PCK(cudaMalloc(&flag, M));
+  PCK(cudaMalloc(&sel, 3 * M * sizeof(int64_t)));
+  PCK(cudaMalloc(&nsel, sizeof(int) * 4));
+  long long msel = 0;
+  if (m > 0) {
+    part_flag_kernel<<<pgrid(m, o.num_sms), kPartBlock, 0, st>>>(m, (const long long *)d_us,
+                                                               (const long long *)d_vs, o.lo, o.hi,
+                                                               flag);
+    size_t tb = 0;
+    PCK(cub::DeviceSelect::Flagged(nullptr, tb, d_us, flag, sel, nsel, (int64_t)m, st));
+    void *tmp = nullptr;
+    PCK(cudaMalloc(&tmp, tb));
+    const int64_t *src[3] = {d_us, d_vs, d_caps};
+    int cnt[3];
+    for (int k = 0; k < 3; ++k) {
+      size_t t2 = tb;
+      PCK(cub::DeviceSelect::Flagged(tmp, t2, src[k], flag, sel + k * M, nsel + k, (int64_t)m, st));
+    }
+    PCK(cudaMemcpyAsync(cnt, nsel, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+    PCK(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+    msel = cnt[0];
+    count_launch(4);
+  }
+  cudaFree(flag);
+  cudaFree(nsel);
+  // Bi-CSR of the selected edges over all n vertices: the owned rows are
+  // exactly the owned rows of the global layout (every edge touching them)
+  Topology topo;
+  topo.device = o.device;
+  topo.stream = st;
+  topo.num_sms = o.num_sms;
+  int64_t err[2];
+  int64_t *gcap = nullptr;
+  cudaError_t e = build_bicsr_device(o.n, msel, sel, sel + M, sel + 2 * M, topo, &gcap, err, nullptr);
+  cudaFree(sel);
+  topo.stream = nullptr;  // owned by the part
+  PCK(e);
+  if (err[0]) {
+    if (gcap) cudaFree(gcap);
+    if (err[0] == 5)
+      return part_fail(MFX_VALUE_ERROR, "partition exceeds the int32 slot layout of one device");
+    return part_fail(MFX_GRAPH_ERROR, "invalid edge list (kind %lld at selected edge %lld)",
+                     (long long)err[0], (long long)err[1]);
+  }
+  int glo = 0, ghi = 0;
+  PCK(cudaMemcpy(&glo, topo.off + o.lo, sizeof(int), cudaMemcpyDeviceToHost));
+  PCK(cudaMemcpy(&ghi, topo.off + o.hi, sizeof(int), cudaMemcpyDeviceToHost));
+  o.S = ghi - glo;
+  size_t SS = (size_t)(o.S > 0 ? o.S : 1), NL = (size_t)(o.nl > 0 ? o.nl : 1);
+  o.rcap = (int)std::min<long long>(4ll * NL + 4096, INT_MAX);
+  size_t sizes[B_NBUF] = {sizeof(int) * (NL + 1), sizeof(int) * SS, sizeof(int) * SS,
+                          sizeof(int) * SS, sizeof(int) * SS, sizeof(long long) * NL,
+                          sizeof(int) * NL, sizeof(unsigned) * NL, sizeof(int) * NL,
+                          sizeof(int) * NL, sizeof(int) * NL, sizeof(int) * NL,
+                          sizeof(int) * (size_t)o.rcap, sizeof(int) * (size_t)o.rcap,
+                          sizeof(int) * PC_N};
+  for (int b = 0; b < B_NBUF; ++b) {
+    o.bytes[b] = sizes[b];
+    PCK(cudaMalloc(&o.buf[b], sizes[b]));
+  }
+  PCK(cudaMemsetAsync(o.buf[B_CTR], 0, sizeof(int) * PC_N, st));
+  PCK(cudaMalloc(&o.rev, sizeof(int) * SS));
+  PCK(cudaMalloc(&o.orig, SS));
+  PCK(cudaMalloc(&o.bases, sizeof(int) * NL));
+  PCK(cudaMalloc(&o.stat, sizeof(unsigned long long) * PS_N));
+  PCK(cudaMalloc(&o.err, sizeof(long long) * PE_N));
+  PCK(cudaMalloc(&o.slot_first, sizeof(int) * SS));
+  PCK(cudaMemsetAsync(o.slot_first, 0x7f, sizeof(int) * SS, st));
+  unsigned long long *bad = nullptr;
+  PCK(cudaMalloc(&bad, sizeof(unsigned long long)));
+  PCK(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st));
+  part_slice_kernel<<<pgrid(o.nl + 1, o.num_sms), kPartBlock, 0, st>>>(o.nl, o.lo, topo.off,
+                                                                      (int *)o.buf[B_OFF]);
+  if (o.S > 0)
+    part_copy_slots_kernel<<<pgrid(o.S, o.num_sms), kPartBlock, 0, st>>>(
+        o.S, glo, topo.adj, (const long long *)gcap, topo.orig, (int *)o.buf[B_ADJ],
+        (int *)o.buf[B_CAP0], o.orig, bad);
+  unsigned long long hb = 0;
+  PCK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  PCK(cudaStreamSynchronize(st));
+  count_launch(2);
+  cudaFree(bad);
+  cudaFree(gcap);
+  if (hb)
+    return part_fail(MFX_VALUE_ERROR,
+                     "the partitioned engine stores int32 residuals: capacities must stay below 2^30");
+  // local original slots
+  {
+    std::vector<uint8_t> h((size_t)o.S);
+    if (o.S > 0) PCK(cudaMemcpy(h.data(), o.orig, (size_t)o.S, cudaMemcpyDeviceToHost));
+    long long mo = 0;
+    for (uint8_t x : h) mo += x != 0;
+    o.m_original = (int)mo;
+  }
+  return MFX_OK;
+}
+
+extern "C" {
+
+int mfx_part_create(int64_t n, int nparts, int rank, const int64_t *bounds, int64_t m,
+                    const int64_t *d_us, const int64_t *d_vs, const int64_t *d_caps,
+                    int64_t source, int64_t sink, int device, mfx_part **out) {
+  *out = nullptr;
+  if (n <= 0) return part_fail(MFX_GRAPH_ERROR, "vertex count must be positive, got %lld", (long long)n);
+  if (n >= INT_MAX) return part_fail(MFX_VALUE_ERROR, "vertex ids must fit int32");
+  if (nparts < 1 || nparts > kMaxParts)
+    return part_fail(MFX_VALUE_ERROR, "nparts must be in [1, %d], got %d", kMaxParts, nparts);
+  if (rank < 0 || rank >= nparts) return part_fail(MFX_VALUE_ERROR, "rank %d out of range", rank);
+  if (bounds[0] != 0 || bounds[nparts] != n)
+    return part_fail(MFX_VALUE_ERROR, "partition bounds must start at 0 and end at n");
+  for (int p = 0; p < nparts; ++p)
+    if (bounds[p + 1] <= bounds[p])
+      return part_fail(MFX_VALUE_ERROR, "partition bounds must be strictly increasing");
+  if (source < 0 || source >= n || sink < 0 || sink >= n || source == sink)
+    return part_fail(MFX_VALUE_ERROR, "invalid source/sink (%lld, %lld)", (long long)source,
+                     (long long)sink);
+  int count = 0;
+  PCK(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count)
+    return part_fail(MFX_VALUE_ERROR, "device %d out of range [0, %d)", device, count);
+  PCK(cudaSetDevice(device));
+  mfx_part *P = new mfx_part();
+  PartObj &o = P->o;
+  o.device = device;
+  o.P = nparts;
+  o.rank = rank;
+  o.n = n;
+  o.lo = (int)bounds[rank];
+  o.hi = (int)bounds[rank + 1];
+  o.nl = o.hi - o.lo;
+  o.s = (int)source;
+  o.t = (int)sink;
+  memset(&o.tab, 0, sizeof(o.tab));
+  o.tab.P = nparts;
+  o.tab.n = (int)n;
+  for (int p = 0; p <= nparts; ++p) o.tab.lo[p] = (int)bounds[p];
+  for (int p = nparts + 1; p <= kMaxParts; ++p) o.tab.lo[p] = (int)n;
+  cudaError_t e = cudaStreamCreateWithFlags(&o.stream, cudaStreamNonBlocking);
+  if (!e) e = cudaDeviceGetAttribute(&o.num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e) {
+    delete P;
+    PCK(e);
+  }
+  int rc = part_build(o, m, d_us, d_vs, d_caps);
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  tab_set_self(o, rank);
+  *out = P;
+  return MFX_OK;
+}
+
+int mfx_part_create_host(int64_t n, int nparts, int rank, const int64_t *bounds, int64_t m,
+                         const int64_t *us, const int64_t *vs, const int64_t *caps,
+                         int64_t source, int64_t sink, int device, mfx_part **out) {
+  *out = nullptr;
+  PCK(cudaSetDevice(device));
+  size_t M = (size_t)(m > 0 ? m : 1);
+  int64_t *d = nullptr;
+  PCK(cudaMalloc(&d, 3 * M * sizeof(int64_t)));
+  if (m > 0) {
+    PCK(cudaMemcpy(d, us, m * sizeof(int64_t), cudaMemcpyHostToDevice));
+    PCK(cudaMemcpy(d + M, vs, m * sizeof(int64_t), cudaMemcpyHostToDevice));
+    PCK(cudaMemcpy(d + 2 * M, caps, m * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  int rc = mfx_part_create(n, nparts, rank, bounds, m, d, d + M, d + 2 * M, source, sink, device, out);
+  cudaFree(d);
+  return rc;
+}
+
+void mfx_part_free(mfx_part *p) { delete p; }
+
+int mfx_part_info(const mfx_part *p, int64_t *info) {
+  const PartObj &o = p->o;
+  info[0] = o.lo;
+  info[1] = o.hi;
+  info[2] = o.S;
+  info[3] = o.m_original;
+  info[4] = o.rcap;
+  info[5] = o.device;
+  info[6] = o.P;
+  info[7] = o.rank;
+  return MFX_OK;
+}
+
+int mfx_part_export(const mfx_part *p, void *blob, int64_t cap, int64_t *len) {
+  const PartObj &o = p->o;
+  int64_t need = (int64_t)(B_NBUF * sizeof(cudaIpcMemHandle_t));
+  *len = need;
+  if (cap < need) return part_fail(MFX_VALUE_ERROR, "export blob needs %lld bytes", (long long)need);
+  PCK(cudaSetDevice(o.device));
+  for (int b = 0; b < B_NBUF; ++b) {
+    cudaIpcMemHandle_t h;
+    PCK(cudaIpcGetMemHandle(&h, o.buf[b]));
+    memcpy((char *)blob + b * sizeof(h), &h, sizeof(h));
+  }
+  return MFX_OK;
+}
+
+int mfx_part_attach(mfx_part *p, int peer, const void *blob, int64_t len) {
+  PartObj &o = p->o;
+  if (peer < 0 || peer >= o.P || peer == o.rank)
+    return part_fail(MFX_VALUE_ERROR, "peer %d invalid for rank %d of %d", peer, o.rank, o.P);
+  if (len < (int64_t)(B_NBUF * sizeof(cudaIpcMemHandle_t)))
+    return part_fail(MFX_VALUE_ERROR, "short peer blob");
+  PCK(cudaSetDevice(o.device));
+  void *ptr[B_NBUF];
+  for (int b = 0; b < B_NBUF; ++b) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char *)blob + b * sizeof(h), sizeof(h));
+    PCK(cudaIpcOpenMemHandle(&ptr[b], h, cudaIpcMemLazyEnablePeerAccess));
+    o.opened[peer][b] = true;
+  }
+  PeerTab &T = o.tab;
+  T.off[peer] = (const int *)ptr[B_OFF];
+  T.adj[peer] = (const int *)ptr[B_ADJ];
+  T.cap0[peer] = (const int *)ptr[B_CAP0];
+  T.pc[peer] = (int *)ptr[B_PC];
+  T.cf[peer] = (int *)ptr[B_CF];
+  T.ex[peer] = (long long *)ptr[B_EX];
+  T.h[peer] = (int *)ptr[B_H];
+  T.mark[peer] = (unsigned *)ptr[B_MARK];
+  T.F[peer][0][0] = (int *)ptr[B_F00];
+  T.F[peer][0][1] = (int *)ptr[B_F01];
+  T.F[peer][1][0] = (int *)ptr[B_F10];
+  T.F[peer][1][1] = (int *)ptr[B_F11];
+  T.R[peer][0] = (int *)ptr[B_R0];
+  T.R[peer][1] = (int *)ptr[B_R1];
+  T.ctr[peer] = (int *)ptr[B_CTR];
+  return MFX_OK;
+}
+
+int mfx_part_attach_local(mfx_part *p, const mfx_part *q) {
+  PartObj &o = p->o;
+  const PartObj &r = q->o;
+  if (r.P != o.P || r.rank == o.rank || r.n != o.n)
+    return part_fail(MFX_VALUE_ERROR, "parts do not belong to the same partition set");
+  if (r.device != o.device) {  // NVLink P2P between the GPUs of one process
+    PCK(cudaSetDevice(o.device));
+    cudaError_t e = cudaDeviceEnablePeerAccess(r.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) PCK(e);
+    cudaGetLastError();
+  }
+  const PeerTab &R = r.tab;  // r's own entry was set when r was created
+  PeerTab &T = o.tab;
+  const int k = r.rank;
+  T.off[k] = R.off[k];
+  T.adj[k] = R.adj[k];
+  T.cap0[k] = R.cap0[k];
+  T.pc[k] = R.pc[k];
+  T.cf[k] = R.cf[k];
+  T.ex[k] = R.ex[k];
+  T.h[k] = R.h[k];
+  T.mark[k] = R.mark[k];
+  for (int a = 0; a < 2; ++a) {
+    for (int b = 0; b < 2; ++b) T.F[k][a][b] = R.F[k][a][b];
+    T.R[k][a] = R.R[k][a];
+  }
+  T.ctr[k] = R.ctr[k];
+  return MFX_OK;
+}
+
+// Phases.  args/out are 8 x int64; see include/mfx.h for the meaning.
+int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
+  PartObj &o = pp->o;
+  PCK(cudaSetDevice(o.device));
+  cudaStream_t st = o.stream;
+  const PeerTab &T = o.tab;
+  const int me = o.rank;
+  int *ctr = (int *)o.buf[B_CTR];
+  const int G = o.num_sms * 4;
+  for (int k = 0; k < 8; ++k) out[k] = 0;
+  for (int p = 0; p < o.P; ++p)
+    if (!T.off[p]) return part_fail(MFX_VALUE_ERROR, "part %d not attached to peer %d", me, p);
+  switch (phase) {
+    case MFX_PH_LINK: {
+      PCK(cudaMemsetAsync(ctr + PC_BAD, 0, sizeof(int), st));
+      if (o.S > 0)
+        part_rev_kernel<<<pgrid(o.S, o.num_sms), kPartBlock, 0, st>>>(
+            T, me, o.nl, o.S, (const int *)o.buf[B_OFF], (const int *)o.buf[B_ADJ], o.rev, ctr);
+      count_launch();
+      break;
+    }
+    case MFX_PH_LINK_PC: {
+      if (o.S > 0)
+        part_pc_kernel<<<pgrid(o.S, o.num_sms), kPartBlock, 0, st>>>(T, me, o.S, o.rev, ctr);
+      count_launch();
+      break;
+    }
+    case MFX_PH_INIT: {
+      part_init_kernel<<<pgrid((long long)o.S + o.nl, o.num_sms), kPartBlock, 0, st>>>(T, me, o.nl, o.S);
+      PCK(cudaMemsetAsync(o.stat, 0, sizeof(unsigned long long) * PS_N, st));
+      count_launch();
+      break;
+    }
+    case MFX_PH_SATURATE: {
+      if (o.s >= o.lo && o.s < o.hi) {
+        part_saturate_kernel<<<o.num_sms, kPartBlock, 0, st>>>(T, me, o.s - o.lo, o.rev,
+                                                                args[0] ? o.err : nullptr);
+        count_launch();
+      }
+      break;
+    }
+    case MFX_PH_BFS_INIT: {  // args: dyn
+      PCK(cudaMemsetAsync(ctr, 0, sizeof(int) * PC_N, st));
+      int forbidden = args[0] ? o.s : -1;
+      part_bfs_init_kernel<<<pgrid(o.nl, o.num_sms), kPartBlock, 0, st>>>(
+          T, me, o.nl, o.s, o.t, (int)args[0], forbidden, o.bases);
+      count_launch();
+      break;
+    }
+    case MFX_PH_BFS_EXPAND: {  // args: L, cur, cnt0, cnt1, dyn
+      int forbidden = args[4] ? o.s : -1;
+      if (args[2] + args[3] > 0) {
+        part_bfs_expand_kernel<<<G, kPartBlock, 0, st>>>(T, me, (int)args[0], (int)args[1],
+                                                         (int)args[2], (int)args[3], o.s, o.t,
+                                                         forbidden, o.rcap);
+        count_launch();
+      }
+      break;
+    }
+    case MFX_PH_SWAP: {  // -> out: next frontier per bin, round-list tails, active, reached, ovf, bases
+      int h[PC_N];
+      PCK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+      PCK(cudaStreamSynchronize(st));
+      PCK(cudaMemsetAsync(ctr + PC_FN0, 0, 2 * sizeof(int), st));
+      for (int k = 0; k < 8; ++k) out[k] = h[k];
+      break;
+    }
+    case MFX_PH_PUSH: {  // args: b0, e0, b1, e1, kc, stamp
+      int b0 = (int)args[0], e0 = (int)std::min<int64_t>(args[1], o.rcap);
+      int b1 = (int)args[2], e1 = (int)std::min<int64_t>(args[3], o.rcap);
+      if (e0 > b0 || e1 > b1) {
+        part_push_kernel<<<G, kPartBlock, 0, st>>>(T, me, b0, e0, b1, e1, (int)args[4],
+                                                   (unsigned)args[5], o.s, o.t, o.rcap, o.rev,
+                                                   o.stat);
+        count_launch();
+      }
+      break;
+    }
+    case MFX_PH_REPAIR: {  // args: e0, e1
+      int e0 = (int)std::min<int64_t>(args[0], o.rcap), e1 = (int)std::min<int64_t>(args[1], o.rcap);
+      if (e0 + e1 > 0) {
+        part_repair_kernel<<<G, kPartBlock, 0, st>>>(T, me, e0, e1, o.rev, o.stat);
+        count_launch();
+      }
+      break;
+    }
+    case MFX_PH_FINAL: {  // args: #bases -> out[0] flow partial, out[1] cut partial
+      PCK(cudaMemsetAsync(o.stat + PS_FLOW, 0, 2 * sizeof(unsigned long long), st));
+      part_final_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.nl, (int)args[0], o.bases, o.orig, o.stat);
+      count_launch();
+      break;
+    }
+    case MFX_PH_ACTIVE: {
+      PCK(cudaMemsetAsync(o.stat + PS_ACTIVE, 0, sizeof(unsigned long long), st));
+      part_active_kernel<<<pgrid(o.nl, o.num_sms), kPartBlock, 0, st>>>(T, me, o.nl, o.s, o.t, o.stat);
+      count_launch();
+      break;
+    }
+    case MFX_PH_BATCH_RESOLVE: {
+      long long init[PE_N];
+      for (int k = 0; k < PE_N; ++k) init[k] = LLONG_MAX;
+      PCK(cudaMemcpyAsync(o.err, init, sizeof(init), cudaMemcpyHostToDevice, st));
+      long long k = o.bk;
+      if (k > 0) {
+        const long long *B = (const long long *)o.bbuf;
+        int g = pgrid(k, o.num_sms);
+        part_batch_resolve_kernel<<<g, kPartBlock, 0, st>>>(T, me, k, B, B + o.bcap, B + 2 * o.bcap,
+                                                            B + 3 * o.bcap, o.orig, o.rev, o.bslot,
+                                                            o.slot_first, o.err);
+        part_batch_dup_kernel<<<g, kPartBlock, 0, st>>>(k, o.slot_base, o.bslot, o.slot_first,
+                                                        B + 3 * o.bcap, o.err);
+        part_batch_dupidx_kernel<<<g, kPartBlock, 0, st>>>(k, o.slot_base, o.bslot, o.slot_first,
+                                                           B + 3 * o.bcap, o.err);
+        count_launch(3);
+      }
+      long long h[PE_N];
+      PCK(cudaMemcpyAsync(h, o.err, sizeof(h), cudaMemcpyDeviceToHost, st));
+      PCK(cudaStreamSynchronize(st));
+      for (int q = 0; q < 8; ++q) out[q] = h[q];
+      break;
+    }
+    case MFX_PH_BATCH_APPLY: {  // args: apply (0 = only restore scratch)
+      long long k = o.bk;
+      if (k > 0) {
+        const long long *B = (const long long *)o.bbuf;
+        part_batch_apply_kernel<<<pgrid(k, o.num_sms), kPartBlock, 0, st>>>(
+            T, me, k, B + 2 * o.bcap, o.bslot, o.slot_first, (int)args[0]);
+        count_launch();
+      }
+      break;
+    }
+    case MFX_PH_BATCH_FIX: {
+      long long k = o.bk;
+      if (k > 0) {
+        const long long *B = (const long long *)o.bbuf;
+        part_batch_fix_kernel<<<pgrid(k, o.num_sms), kPartBlock, 0, st>>>(T, me, k, B, o.bslot, o.rev);
+        count_launch();
+      }
+      break;
+    }
+    default:
+      return part_fail(MFX_VALUE_ERROR, "unknown partition phase %d", phase);
+  }
+  PCK(cudaGetLastError());
+  PCK(cudaStreamSynchronize(st));
+  if (phase == MFX_PH_LINK || phase == MFX_PH_LINK_PC) {
+    int bad = 0;
+    PCK(cudaMemcpy(&bad, ctr + PC_BAD, sizeof(int), cudaMemcpyDeviceToHost));
+    if (bad)
+      return part_fail(MFX_VALUE_ERROR,
+                       phase == MFX_PH_LINK ? "%d slots without a reverse slot in the owning part"
+                                            : "%d pair capacities overflow int32 residual storage",
+                       bad);
+  }
+  if (phase == MFX_PH_FINAL || phase == MFX_PH_ACTIVE || phase == MFX_PH_PUSH ||
+      phase == MFX_PH_REPAIR || phase == MFX_PH_INIT) {
+    unsigned long long h[PS_N];
+    PCK(cudaMemcpy(h, o.stat, sizeof(h), cudaMemcpyDeviceToHost));
+    if (phase == MFX_PH_FINAL) {
+      out[0] = (int64_t)h[PS_FLOW];
+      out[1] = (int64_t)h[PS_CUT];
+    } else if (phase == MFX_PH_ACTIVE) {
+      out[0] = (int64_t)h[PS_ACTIVE];
+    } else {
+      out[0] = (int64_t)h[PS_PUSH];
+      out[1] = (int64_t)h[PS_RELABEL];
+      out[2] = (int64_t)h[PS_REPAIR];
+      out[3] = (int64_t)h[PS_BYTES];
+    }
+  }
+  return MFX_OK;
+}
+
+// Stage this part's share of an update batch (host arrays; gidx = the
+// update's index in the whole batch, for reference-identical error reports).
+int mfx_part_stage_batch(mfx_part *pp, int64_t k, const int64_t *us, const int64_t *vs,
+                         const int64_t *caps, const int64_t *gidx, int64_t slot_base) {
+  PartObj &o = pp->o;
+  PCK(cudaSetDevice(o.device));
+  for (int64_t j = 0; j < k; ++j)
+    if (us[j] < o.lo || us[j] >= o.hi)
+      return part_fail(MFX_VALUE_ERROR, "update %lld routed to the wrong part", (long long)gidx[j]);
+  if (k > o.bcap) {
+    if (o.bbuf) cudaFree(o.bbuf);
+    if (o.bslot) cudaFree(o.bslot);
+    o.bbuf = nullptr;
+    o.bslot = nullptr;
+    long long cap = k > 1024 ? k : 1024;
+    PCK(cudaMalloc(&o.bbuf, sizeof(long long) * 4 * (size_t)cap));
+    PCK(cudaMalloc(&o.bslot, sizeof(int) * (size_t)cap));
+    o.bcap = cap;
+  }
+  o.bk = (int)k;
+  o.slot_base = slot_base;
+  if (k > 0) {
+    long long *B = o.bbuf;
+    PCK(cudaMemcpyAsync(B, us, sizeof(int64_t) * k, cudaMemcpyHostToDevice, o.stream));
+    PCK(cudaMemcpyAsync(B + o.bcap, vs, sizeof(int64_t) * k, cudaMemcpyHostToDevice, o.stream));
+    PCK(cudaMemcpyAsync(B + 2 * o.bcap, caps, sizeof(int64_t) * k, cudaMemcpyHostToDevice, o.stream));
+    PCK(cudaMemcpyAsync(B + 3 * o.bcap, gidx, sizeof(int64_t) * k, cudaMemcpyHostToDevice, o.stream));
+    PCK(cudaStreamSynchronize(o.stream));
+  }
+  return MFX_OK;
+}
+
+// Download the local arrays (any may be NULL): off[nl+1], adj/rev/cap0/cf[S]
+// (int64, rev as local slot indices of the owner), orig[S], excess/height[nl].
+int mfx_part_download(const mfx_part *pp, int64_t *off, int64_t *adj, int64_t *rev, int64_t *cap0,
+                      int64_t *cf, uint8_t *orig, int64_t *excess, int64_t *height) {
+  const PartObj &o = pp->o;
+  PCK(cudaSetDevice(o.device));
+  auto widen = [&](const void *d, int64_t *h, size_t cnt) -> int {
+    if (!h || cnt == 0) return MFX_OK;
+    std::vector<int> tmp(cnt);
+    PCK(cudaMemcpy(tmp.data(), d, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < cnt; ++i) h[i] = tmp[i];
+    return MFX_OK;
+  };
+  int rc;
+  if ((rc = widen(o.buf[B_OFF], off, (size_t)o.nl + 1))) return rc;
+  if ((rc = widen(o.buf[B_ADJ], adj, (size_t)o.S))) return rc;
+  if ((rc = widen(o.rev, rev, (size_t)o.S))) return rc;
+  if ((rc = widen(o.buf[B_CAP0], cap0, (size_t)o.S))) return rc;
+  if ((rc = widen(o.buf[B_CF], cf, (size_t)o.S))) return rc;
+  if ((rc = widen(o.buf[B_H], height, (size_t)o.nl))) return rc;
+  if (orig && o.S > 0) PCK(cudaMemcpy(orig, o.orig, (size_t)o.S, cudaMemcpyDeviceToHost));
+  if (excess && o.nl > 0)
+    PCK(cudaMemcpy(excess, o.buf[B_EX], sizeof(int64_t) * (size_t)o.nl, cudaMemcpyDeviceToHost));
+  return MFX_OK;
+}
+
+}  // extern "C"
