@@ -239,6 +239,11 @@ int mfx_part_phase(mfx_part *p, int phase, const int64_t *args, int64_t *out);
  * slot_base = global index of the part's first slot (error reports). */
 int mfx_part_stage_batch(mfx_part *p, int64_t k, const int64_t *us, const int64_t *vs,
                          const int64_t *caps, const int64_t *gidx, int64_t slot_base);
+/* Device batch sampler (gen.py fast_batch semantics) over this part's
+ * original slots: k_dec decrements, then k_inc increments, into host arrays;
+ * *got = updates produced. */
+int mfx_part_sample_batch(mfx_part *p, int64_t k_dec, int64_t k_inc, uint64_t seed, double bias,
+                          int64_t *us, int64_t *vs, int64_t *caps, int64_t *got);
 int mfx_part_download(const mfx_part *p, int64_t *off, int64_t *adj, int64_t *rev, int64_t *cap0,
                       int64_t *cf, uint8_t *orig, int64_t *excess, int64_t *height);
 

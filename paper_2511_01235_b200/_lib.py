@@ -127,6 +127,8 @@ SIGNATURES = {
     "mfx_part_stage_batch": (ctypes.c_int, [vp, i64, p_i64, p_i64, p_i64, p_i64, i64]),
     "mfx_part_download": (ctypes.c_int, [vp, p_i64, p_i64, p_i64, p_i64, p_i64, p_u8, p_i64,
                                          p_i64]),
+    "mfx_part_sample_batch": (ctypes.c_int, [vp, i64, i64, ctypes.c_uint64, ctypes.c_double,
+                                             p_i64, p_i64, p_i64, p_i64]),
     "mfx_rmat_device": (ctypes.c_int, [ctypes.c_int, i64, ctypes.c_uint64, ctypes.c_double,
                                        ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp,
                                        vp, p_i64, p_i64]),

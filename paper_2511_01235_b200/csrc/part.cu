@@ -690,6 +690,88 @@ __global__ void part_batch_fix_kernel(PeerTab T, int me, long long k, const long
   }
 }
 
+// ---------------------------------------------------------------------------
+// device batch sampler for the largest graphs (gen.py fast_batch semantics:
+// exponential-race keys E/w over the original slots, w = bias on s-out / t-in
+// edges; decrements on positive capacities, new in [0, old); increments on
+// the rest, new in [old+1, 2 old + 10]).  Candidates below a threshold are
+// compacted and only they are sorted.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long smix(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ int row_of(const int *off, int nl, int i) {
+  int a = 0, b = nl;
+  while (b - a > 1) {
+    int mid = (a + b) >> 1;
+    if (off[mid] <= i) a = mid;
+    else b = mid;
+  }
+  return a;
+}
+
+__global__ void part_sample_kernel(PeerTab T, int me, int nl, long long S, const uint8_t *orig,
+                                   const uint8_t *taken, int s, int t, double bias,
+                                   unsigned long long seed, int dec, double tau, int cap,
+                                   unsigned long long *cand, int *cnt) {
+  const int *off = T.off[me], *adj = T.adj[me], *cap0 = T.cap0[me];
+  PGS_LOOP(i, S) {
+    if (!orig[i] || taken[i] || (dec && cap0[i] <= 0)) continue;
+    unsigned long long hsh = smix(seed ^ smix((unsigned long long)(T.lo[me]) * 0x100000001ull + i));
+    double uu = ((double)(hsh >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    double w = 1.0;
+    if (adj[i] == t) w = bias;
+    else if (s >= T.lo[me] && s < T.lo[me + 1] && off[s - T.lo[me]] <= i && i < off[s - T.lo[me] + 1])
+      w = bias;
+    double key = -log(uu) / w;
+    if (key < tau) {
+      int q = atomicAdd(cnt, 1);
+      if (q < cap) {
+        float kf = (float)key;
+        cand[q] = ((unsigned long long)__float_as_uint(kf) << 32) | (unsigned)i;
+      }
+    }
+  }
+}
+
+__global__ void part_sample_emit_kernel(PeerTab T, int me, int nl, const int *slots, int k,
+                                        int dec, unsigned long long seed, uint8_t *taken,
+                                        long long *ou, long long *ov, long long *oc) {
+  const int *off = T.off[me], *adj = T.adj[me], *cap0 = T.cap0[me];
+  PGS_LOOP(j, k) {
+    int i = slots[j];
+    taken[i] = 1;
+    long long old = cap0[i];
+    unsigned long long hsh = smix(seed ^ 0xD1B54A32D192ED03ull ^ smix((unsigned long long)i + 1));
+    ou[j] = T.lo[me] + row_of(off, nl, i);
+    ov[j] = adj[i];
+    oc[j] = dec ? (long long)(hsh % (unsigned long long)old)
+                : old + 1 + (long long)(hsh % (unsigned long long)(old + 10));
+  }
+}
+
+__global__ void part_untake_kernel(const int *slots, int k, uint8_t *taken) {
+  PGS_LOOP(j, k) taken[slots[j]] = 0;
+}
+
+__global__ void part_weight_kernel(PeerTab T, int me, long long S, const uint8_t *orig, int s, int t,
+                                   double bias, unsigned long long *acc) {
+  const int *off = T.off[me], *adj = T.adj[me];
+  unsigned long long a = 0;
+  PGS_LOOP(i, S) {
+    if (!orig[i]) continue;
+    bool hub = adj[i] == t || (s >= T.lo[me] && s < T.lo[me + 1] && off[s - T.lo[me]] <= i &&
+                               i < off[s - T.lo[me] + 1]);
+    a += hub ? (unsigned long long)bias : 1ull;
+  }
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0 && a) atomicAdd(acc, a);
+}
+
 static inline int pgrid(long long work, int sms) {
   long long g = (work + kPartBlock - 1) / kPartBlock;
   long long cap = (long long)sms * 8;
@@ -1208,6 +1290,98 @@ int mfx_part_stage_batch(mfx_part *pp, int64_t k, const int64_t *us, const int64
 
 // Download the local arrays (any may be NULL): off[nl+1], adj/rev/cap0/cf[S]
 // (int64, rev as local slot indices of the owner), orig[S], excess/height[nl].
+// Sample k_dec decrements then k_inc increments from this part's original
+// slots (host output arrays of k_dec + k_inc entries, (u, v)-sorted within
+// each kind); *got = updates produced.
+int mfx_part_sample_batch(mfx_part *pp, int64_t k_dec, int64_t k_inc, uint64_t seed, double bias,
+                          int64_t *us, int64_t *vs, int64_t *caps, int64_t *got) {
+  PartObj &o = pp->o;
+  PCK(cudaSetDevice(o.device));
+  cudaStream_t st = o.stream;
+  *got = 0;
+  const long long S = o.S;
+  if (S == 0 || k_dec + k_inc == 0) return MFX_OK;
+  uint8_t *taken = nullptr;
+  PCK(cudaMalloc(&taken, (size_t)S));
+  PCK(cudaMemsetAsync(taken, 0, (size_t)S, st));
+  unsigned long long *acc = nullptr;
+  PCK(cudaMalloc(&acc, sizeof(unsigned long long)));
+  PCK(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), st));
+  part_weight_kernel<<<pgrid(S, o.num_sms), kPartBlock, 0, st>>>(o.tab, o.rank, S, o.orig, o.s, o.t,
+                                                               bias, acc);
+  unsigned long long W = 0;
+  PCK(cudaMemcpyAsync(&W, acc, sizeof(W), cudaMemcpyDeviceToHost, st));
+  PCK(cudaStreamSynchronize(st));
+  long long done = 0;
+  std::vector<int> all_slots;
+  for (int kind = 0; kind < 2; ++kind) {
+    const long long want = kind == 0 ? k_dec : k_inc;
+    if (want <= 0) continue;
+    const int cap = (int)std::min<long long>(8 * want + 4096, S);
+    unsigned long long *cand = nullptr, *sorted = nullptr;
+    int *cnt = nullptr;
+    PCK(cudaMalloc(&cand, sizeof(unsigned long long) * cap));
+    PCK(cudaMalloc(&sorted, sizeof(unsigned long long) * cap));
+    PCK(cudaMalloc(&cnt, sizeof(int)));
+    double tau = 3.0 * (double)want / (double)(W > 0 ? W : 1) + 1e-12;
+    int c = 0;
+    for (int it = 0; it < 60; ++it) {
+      PCK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+      part_sample_kernel<<<pgrid(S, o.num_sms), kPartBlock, 0, st>>>(
+          o.tab, o.rank, o.nl, S, o.orig, taken, o.s, o.t, bias, seed * 2 + kind, kind == 0, tau,
+          cap, cand, cnt);
+      PCK(cudaMemcpyAsync(&c, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+      PCK(cudaStreamSynchronize(st));
+      count_launch();
+      if (c > cap) tau *= 0.5;                       // too many candidates
+      else if (c < want && tau < 1e30) tau *= 4.0;  // too few: widen (or nothing left)
+      else break;
+      if (c < want && tau >= 1e30) break;
+    }
+    if (c > cap) c = cap;
+    size_t tb = 0;
+    PCK(cub::DeviceRadixSort::SortKeys(nullptr, tb, cand, sorted, c, 0, 64, st));
+    void *tmp = nullptr;
+    PCK(cudaMalloc(&tmp, tb > 0 ? tb : 1));
+    PCK(cub::DeviceRadixSort::SortKeys(tmp, tb, cand, sorted, c, 0, 64, st));
+    std::vector<unsigned long long> h((size_t)c);
+    PCK(cudaMemcpyAsync(h.data(), sorted, sizeof(unsigned long long) * (size_t)c,
+                        cudaMemcpyDeviceToHost, st));
+    PCK(cudaStreamSynchronize(st));
+    long long take = std::min<long long>(want, c);
+    std::vector<int> slots((size_t)take);
+    for (long long j = 0; j < take; ++j) slots[j] = (int)(h[j] & 0xFFFFFFFFull);
+    std::sort(slots.begin(), slots.end());
+    int *d_slots = nullptr;
+    long long *d_out = nullptr;
+    PCK(cudaMalloc(&d_slots, sizeof(int) * (size_t)(take > 0 ? take : 1)));
+    PCK(cudaMalloc(&d_out, sizeof(long long) * 3 * (size_t)(take > 0 ? take : 1)));
+    if (take > 0) {
+      PCK(cudaMemcpyAsync(d_slots, slots.data(), sizeof(int) * take, cudaMemcpyHostToDevice, st));
+      part_sample_emit_kernel<<<pgrid(take, o.num_sms), kPartBlock, 0, st>>>(
+          o.tab, o.rank, o.nl, d_slots, (int)take, kind == 0, seed * 2 + kind, taken, d_out,
+          d_out + take, d_out + 2 * take);
+      PCK(cudaMemcpyAsync(us + done, d_out, sizeof(long long) * take, cudaMemcpyDeviceToHost, st));
+      PCK(cudaMemcpyAsync(vs + done, d_out + take, sizeof(long long) * take, cudaMemcpyDeviceToHost, st));
+      PCK(cudaMemcpyAsync(caps + done, d_out + 2 * take, sizeof(long long) * take,
+                          cudaMemcpyDeviceToHost, st));
+      PCK(cudaStreamSynchronize(st));
+      count_launch();
+    }
+    done += take;
+    cudaFree(tmp);
+    cudaFree(cand);
+    cudaFree(sorted);
+    cudaFree(cnt);
+    cudaFree(d_slots);
+    cudaFree(d_out);
+  }
+  cudaFree(taken);
+  cudaFree(acc);
+  *got = done;
+  return MFX_OK;
+}
+
 int mfx_part_download(const mfx_part *pp, int64_t *off, int64_t *adj, int64_t *rev, int64_t *cap0,
                       int64_t *cf, uint8_t *orig, int64_t *excess, int64_t *height) {
   const PartObj &o = pp->o;

@@ -430,6 +430,67 @@ class PartitionedGraph:
         flow, cut, st = self._rounds(params, 1, t0)
         return self._finish(flow, cut, st, t0)
 
+    def sample_batch(self, k: int, seed: int, bias: float = 10.0) -> UpdateBatch:
+        """A mixed batch of k updates drawn on the device from the current
+        capacities (gen.py fast_batch semantics: half decrements on positive
+        edges, half increments, bias on s-out / t-in edges), split over the
+        parts in proportion to their original edges; (u, v)-sorted."""
+        P = self.group.nparts
+        share = np.array([self.info[r][3] for r in range(P)], np.float64)
+        share = share / max(share.sum(), 1.0)
+
+        def split(x):
+            c = np.floor(share * x).astype(np.int64)
+            c[: x - int(c.sum())] += 1
+            return c
+        kd, ki = split(k // 2), split(k - k // 2)
+        got = {}
+        for r, h in self.handles.items():
+            want = int(kd[r] + ki[r])
+            a, b, c = (np.zeros(max(want, 1), np.int64) for _ in range(3))
+            n_out = ctypes.c_int64()
+            L.check(self.lib.mfx_part_sample_batch(h, int(kd[r]), int(ki[r]),
+                                                   int(seed) * 131 + r, float(bias), L.ptr64(a),
+                                                   L.ptr64(b), L.ptr64(c), ctypes.byref(n_out)))
+            got[r] = (a[:n_out.value], b[:n_out.value], c[:n_out.value])
+        every = {}
+        for d in self.group.allgather({r: tuple(x.tolist() for x in v) for r, v in got.items()}):
+            every.update(d)
+        us = np.concatenate([np.asarray(every[r][0], np.int64) for r in range(P)])
+        vs = np.concatenate([np.asarray(every[r][1], np.int64) for r in range(P)])
+        cs = np.concatenate([np.asarray(every[r][2], np.int64) for r in range(P)])
+        order = np.lexsort((vs, us))
+        return UpdateBatch(us[order], vs[order], cs[order])
+
+    @classmethod
+    def rmat(cls, scale: int, edge_factor: int = 16, seed: int = 0, group=None, device: int = 0,
+             a: float = 0.57, b: float = 0.19, c: float = 0.19):
+        """C5-shaped graph generated on the device (csrc/gen.cu: the gen.py
+        R-MAT recursion with a counter-based stream) and split by slot-
+        balanced vertex ranges; every rank draws the same edge list on its
+        own GPU and keeps the edges touching its range."""
+        import torch
+        group = group or LocalGroup(1)
+        lib = L.load()
+        n = 1 << scale
+        m = n * edge_factor
+        dev = f"cuda:{group.devices[0]}"
+        e = [torch.empty(m, dtype=torch.int64, device=dev) for _ in range(3)]
+        s, t = ctypes.c_int64(), ctypes.c_int64()
+        L.check(lib.mfx_rmat_device(scale, edge_factor, seed, a, b, c, group.devices[0],
+                                    e[0].data_ptr(), e[1].data_ptr(), e[2].data_ptr(),
+                                    ctypes.byref(s), ctypes.byref(t)))
+        bounds = np.zeros(group.nparts + 1, np.int64)
+        L.check(lib.mfx_part_bounds_device(n, m, e[0].data_ptr(), e[1].data_ptr(), group.nparts,
+                                           group.devices[0], L.ptr64(bounds)))
+        if len(set(group.devices)) > 1:
+            raise ValueError("device generation expects the local parts on one GPU")
+        pg = cls(n, None, None, None, s.value, t.value, group, bounds=bounds,
+                 device_edges=(e[0].data_ptr(), e[1].data_ptr(), e[2].data_ptr(), m))
+        del e
+        torch.cuda.empty_cache()
+        return pg
+
     def download(self, r: int) -> dict:
         """Local arrays of part r (int64): off, adj, rev, cap0, cf, orig,
         excess, height."""

@@ -175,3 +175,21 @@ def test_two_processes_ipc_gloo(tmp_path):
     assert got[0] == got[1]
     rec = G.rec["grid64"]
     assert [int(x) for x in got[0]] == [rec["static_flow"]] + [e["flow"] for e in rec["chain"]]
+
+
+def test_device_rmat_sampler_and_dynamic_equals_resolve(part):
+    """Device-generated R-MAT (C5 generator at scale 14) over 3 parts:
+    sampled batches are valid mixed updates, and after each the dynamic
+    flow equals a static re-solve on the updated capacities."""
+    pg = part.PartitionedGraph.rmat(14, 16, 3, part.LocalGroup(3))
+    f0 = pg.solve_static().flow_value
+    assert f0 > 0
+    for b in range(3):
+        batch = pg.sample_batch(2000, seed=b)
+        assert len(batch) == 2000
+        keys = batch.us * pg.n + batch.vs
+        assert np.unique(keys).size == len(batch) and np.all(batch.new_caps >= 0)
+        d = pg.solve_dynamic(batch)
+        s = pg.solve_static()
+        assert d.flow_value == s.flow_value == d.cut_capacity
+    pg.close()
