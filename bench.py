@@ -48,6 +48,11 @@ def parse():
     ap.add_argument("--max-waves", type=int, default=0)
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no e2e / cpu baseline / re-solve legs")
+    ap.add_argument("--config", default="C2", choices=["C2", "C5"],
+                    help="C2: single-GPU headline; C5: R-MAT 26 vertex-range partitioned "
+                         "(one part per rank under torchrun, --parts parts on one GPU otherwise)")
+    ap.add_argument("--scale", type=int, default=26, help="C5 R-MAT scale")
+    ap.add_argument("--parts", type=int, default=4, help="C5 parts when run as one process")
     return ap.parse_args()
 
 
@@ -396,6 +401,70 @@ def bench_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def bench_c5(args, rank, world, local, pg):
+    """C5: R-MAT (scale 26, ef 16) split by vertex range.  Under
+    torchrun every rank hosts one part on its GPU (NCCL all-reduces, CUDA IPC
+    peer mappings); as one process, --parts parts share cuda:0.  Each step
+    is one chained batch of --batch mixed updates sampled on the device
+    before the timed region and applied from host memory (H2D of the batch
+    and D2H of the per-phase counters inside the timed region, so `value`
+    is end to end)."""
+    import torch
+
+    from paper_2511_01235_b200 import partition
+    torch.cuda.set_device(local)
+    group = partition.TorchGroup(device=local) if world > 1 else \
+        partition.LocalGroup(args.parts, [local] * args.parts)
+    t0 = time.perf_counter()
+    g = partition.PartitionedGraph.rmat(args.scale, 16, 0, group, device=local)
+    build_s = time.perf_counter() - t0
+    st = g.solve_static()
+    W, K = args.warmup, args.steps
+    k = args.batch if args.batch != BATCH else 1_000_000  # C5 batches: 1M updates
+    for i in range(W):
+        g.solve_dynamic(g.sample_batch(k, seed=i))
+    timed, flows = [], []
+    calls0 = g.calls
+    with ClockSampler(local) as clk:
+        for i in range(W, W + K):
+            b = g.sample_batch(k, seed=i)  # device sampler, outside the timed solve
+            barrier(pg, local)
+            torch.cuda.synchronize()
+            r = g.solve_dynamic(b)  # host batch in, counters out (end to end)
+            torch.cuda.synchronize()
+            timed.append(r.seconds)  # max over ranks inside solve_dynamic
+            flows.append(r.flow_value)
+    calls = (g.calls - calls0) / K
+    rs = g.solve_static()
+    assert rs.flow_value == flows[-1], (rs.flow_value, flows[-1])
+    ms = 1e3 * sum(timed) / K
+    if rank != 0:
+        return
+    parts = group.nparts
+    line = {
+        "metric": METRIC, "value": round(ms, 3), "unit": "ms/batch", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms, 3), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"C5: R-MAT scale {args.scale} ef 16 (device generator, seed 0), "
+                               f"{g.m} Bi-CSR slots, chained batches of {k} mixed "
+                               f"updates (device sampler, bias 10)",
+                   "parallelism": f"vertex-range partition, {parts} parts on {world} GPU(s)",
+                   "l2": "inputs larger than L2 (~44 GB of Bi-CSR + state)"},
+        "static_maxflow_edges_per_s": round(g.m_original / st.seconds, 1),
+        "static_ms": round(1e3 * st.seconds, 3), "build_s": round(build_s, 2),
+        "gpu_static_resolve_ms": round(1e3 * rs.seconds, 3),
+        "dynamic_speedup_vs_gpu_static_resolve": round(rs.seconds * 1e3 / ms, 2),
+        "flow_static": st.flow_value, "flows": flows[:3], "resolve_agrees": True,
+        "e2e": {"value": round(ms, 3), "unit": "ms/batch",
+                "h2d_bytes_per_step": 32 * k,
+                "d2h_bytes_per_step": int(64 * calls)},
+        "roofline": None, "clocks": clk.summary(),
+        "note": "partitioned path is host-driven per phase; the roofline line is the C2 "
+                "single-GPU bench (python bench.py)",
+    }
+    print(json.dumps(line), flush=True)
+
+
 def config_block(args, world):
     return {"workload": f"C2: {args.grid}x{args.grid} 4-neighbour grid + terminal edge per pixel "
                         f"(caps U[1,100], seed 0), chained batches of {args.batch} mixed updates "
@@ -410,7 +479,15 @@ def main():
     rank, world, local, pg = dist_setup(args)
     if args.impl == "reference":
         if rank == 0:
-            bench_reference(args, rank, world)
+            if args.config == "C5":
+                print(json.dumps({"impl": "reference", "unavailable":
+                                  "the reference CPU build_bicsr cannot hold the 2.1 B-slot C5 "
+                                  "graph (SURVEY 6.2); C5 parity = dynamic vs GPU static re-solve"}))
+            else:
+                bench_reference(args, rank, world)
+        return
+    if args.config == "C5":
+        bench_c5(args, rank, world, local, pg)
         return
     out = bench_ours(args, rank, world, local, pg)
     if rank != 0:

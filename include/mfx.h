@@ -38,7 +38,8 @@ typedef enum {
     MFX_SOLVER_ERROR = 3,
     MFX_VALUE_ERROR = 4,
     MFX_CUDA_ERROR = 5,
-    MFX_TIMEOUT = 6
+    MFX_TIMEOUT = 6,
+    MFX_PARSE_ERROR = 7 /* ParseError (io.py:20-26); line in mfx_io_error_line() */
 } mfx_status;
 
 typedef struct mfx_graph mfx_graph; /* device Bi-CSR: shared topology + private cap0 */
@@ -58,13 +59,15 @@ typedef struct {
     int32_t max_waves;     /* push waves per round before a global relabel; 0 auto */
     double timeout_s;      /* device watchdog for one solve; 0 -> 600 s            */
     int32_t blocks_per_sm; /* persistent-grid occupancy; 0 -> auto                 */
-    int32_t flags;         /* reserved, 0                                          */
+    int32_t flags;         /* bit 0: BFS relaxes by atomic only (no h pre-load)    */
     int32_t wave_mult;     /* auto wave budget = wave_mult * BFS levels / 4        */
     int32_t wave_add;      /*   + wave_add ((0, 0) -> (2, 4)); if max_waves == 0   */
     int32_t schedule;      /* push phase: 0 waves, 1 asynchronous work queue       */
     int32_t async_budget;  /* async: items per active vertex per round (0 -> 16)   */
     int32_t bfs_local;     /* CTA-local BFS sub-levels per grid barrier: 0 -> 32,   */
-    int32_t pad_;          /*   < 0 -> strict level-synchronous BFS                */
+                           /*   < 0 -> strict level-synchronous BFS                */
+    int32_t bfs_local_max; /* ... used while the frontier <= this many items per   */
+                           /*   CTA; 0 -> 64                                        */
 } mfx_params;
 
 /* FlowResult (solver.py:108-118) plus device counters. */
@@ -256,6 +259,27 @@ int mfx_rmat_device(int scale, int64_t edge_factor, uint64_t seed, double a, dou
 /* Slot-balanced vertex-range cut of a device edge list: bounds[nparts + 1]. */
 int mfx_part_bounds_device(int64_t n, int64_t m, const int64_t *d_us, const int64_t *d_vs,
                            int nparts, int device, int64_t *bounds);
+
+/* ---- file formats (io.py:33-182): native readers feeding the builder --- */
+typedef struct mfx_edges mfx_edges; /* parsed host edge list */
+/* parse_graph (io.py:33-109): DIMACS max, 1-indexed ids -> 0-indexed. */
+int mfx_io_parse_graph(const char *path, mfx_edges **out);
+/* parse_updates (io.py:121-144) syntax and range checks; the edge lookup and
+ * duplicate checks (dynamic.py:63-88) are the caller's, against the graph. */
+int mfx_io_parse_updates(const char *path, int64_t n, mfx_edges **out);
+/* parse_edge_list (io.py:153-182). */
+int mfx_io_parse_edge_list(const char *path, int one_indexed, mfx_edges **out);
+/* info[4] = n, m, source, sink (-1 when the format has none). */
+int mfx_edges_info(const mfx_edges *e, int64_t *info);
+int mfx_edges_get(const mfx_edges *e, int64_t *us, int64_t *vs, int64_t *caps);
+void mfx_edges_free(mfx_edges *e);
+/* Line number of the last MFX_PARSE_ERROR (0 = end-of-file checks). */
+int64_t mfx_io_error_line(void);
+/* write_graph (io.py:112-118) / write_updates (io.py:147-150). */
+int mfx_io_write_graph(const char *path, int64_t n, int64_t m, int64_t source, int64_t sink,
+                       const int64_t *us, const int64_t *vs, const int64_t *caps);
+int mfx_io_write_updates(const char *path, int64_t k, const int64_t *us, const int64_t *vs,
+                         const int64_t *caps);
 
 /* ---- host memory helpers (pinned staging for end-to-end timing) -------- */
 int mfx_host_alloc(size_t bytes, void **ptr);

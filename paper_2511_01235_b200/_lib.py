@@ -21,6 +21,7 @@ MFX_SOLVER_ERROR = 3
 MFX_VALUE_ERROR = 4
 MFX_CUDA_ERROR = 5
 MFX_TIMEOUT = 6
+MFX_PARSE_ERROR = 7
 
 i64 = ctypes.c_int64
 i32 = ctypes.c_int32
@@ -39,7 +40,7 @@ class Params(ctypes.Structure):
     _fields_ = [("kernel_cycles", i64), ("mode", i32), ("max_waves", i32),
                 ("timeout_s", ctypes.c_double), ("blocks_per_sm", i32), ("flags", i32),
                 ("wave_mult", i32), ("wave_add", i32), ("schedule", i32),
-                ("async_budget", i32), ("bfs_local", i32), ("pad_", i32)]
+                ("async_budget", i32), ("bfs_local", i32), ("bfs_local_max", i32)]
 
 
 class Result(ctypes.Structure):
@@ -129,6 +130,16 @@ SIGNATURES = {
                                          p_i64]),
     "mfx_part_sample_batch": (ctypes.c_int, [vp, i64, i64, ctypes.c_uint64, ctypes.c_double,
                                              p_i64, p_i64, p_i64, p_i64]),
+    "mfx_io_parse_graph": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(vp)]),
+    "mfx_io_parse_updates": (ctypes.c_int, [ctypes.c_char_p, i64, ctypes.POINTER(vp)]),
+    "mfx_io_parse_edge_list": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(vp)]),
+    "mfx_edges_info": (ctypes.c_int, [vp, p_i64]),
+    "mfx_edges_get": (ctypes.c_int, [vp, p_i64, p_i64, p_i64]),
+    "mfx_edges_free": (None, [vp]),
+    "mfx_io_error_line": (i64, []),
+    "mfx_io_write_graph": (ctypes.c_int, [ctypes.c_char_p, i64, i64, i64, i64, p_i64, p_i64,
+                                          p_i64]),
+    "mfx_io_write_updates": (ctypes.c_int, [ctypes.c_char_p, i64, p_i64, p_i64, p_i64]),
     "mfx_rmat_device": (ctypes.c_int, [ctypes.c_int, i64, ctypes.c_uint64, ctypes.c_double,
                                        ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp,
                                        vp, p_i64, p_i64]),

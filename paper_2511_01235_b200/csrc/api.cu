@@ -603,8 +603,12 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.async = p->schedule == 1;
   if (const char *sch = getenv("MFX_SCHEDULE")) cfg.async = sch[0] == 'a';
   if (p->async_budget > 0) cfg.async_budget = p->async_budget;
+  cfg.flags = p->flags;
+  if (const char *fl = getenv("MFX_FLAGS")) cfg.flags = atoi(fl);
   if (p->bfs_local != 0) cfg.bfs_local = p->bfs_local < 0 ? 0 : p->bfs_local;
   if (const char *bl = getenv("MFX_BFS_LOCAL")) cfg.bfs_local = atoi(bl) < 0 ? 0 : atoi(bl);
+  if (p->bfs_local_max > 0) cfg.bfs_local_max = p->bfs_local_max;
+  if (const char *bm = getenv("MFX_BFS_LOCAL_MAX")) cfg.bfs_local_max = atoi(bm);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;

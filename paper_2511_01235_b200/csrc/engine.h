@@ -87,6 +87,8 @@ struct SolveConfig {
   int wave_add = 4;
   int async = 0;          // asynchronous push phase (work queue) instead of waves
   int async_budget = 16;  // items per initially active vertex before a global relabel
+  int flags = 0;          // mfx_params.flags (bit 0: BFS without h pre-load)
+  int bfs_local_max = 64; // ... while the frontier holds <= this many items per CTA
   int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;

@@ -25,7 +25,10 @@
 
 namespace mfx {
 
-constexpr int kBlock = 256;
+#ifndef MFX_BLOCK
+#define MFX_BLOCK 256
+#endif
+constexpr int kBlock = MFX_BLOCK;  // threads per CTA (the solve kernel runs 2 CTAs/SM at 256)
 constexpr int kWarps = kBlock / 32;
 constexpr int NBIN = 4;  // 0: thread/vertex, 1: warp/vertex, 2: CTA/vertex, 3: huge
 constexpr int kBin0Max = 8;

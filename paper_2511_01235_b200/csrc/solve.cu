@@ -46,6 +46,8 @@ struct SolveArgs {
   int async_budget;  // items per initially active vertex before the next global relabel
   int *rdirty;       // NBIN used extents of the R lists (device, shared by states)
   int bfs_local;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
+  int flags;         // bit 0: BFS relaxes with the atomic alone (no pre-load of h[v])
+  int bfs_local_max; // CTA-local sub-levels only when the frontier <= this many items per CTA
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
   int what;
@@ -345,62 +347,37 @@ struct Kern {
   // =========================================================================
   // Frontier BFS over reverse residual slots with label-correcting relaxation
   // (atomicMin on h): between two grid barriers ("epoch") a CTA may expand
-  // its own light discoveries for up to `local_levels` further BFS
-  // sub-levels, staged in a shared-memory queue and separated by
-  // __syncthreads only.  Heavy rows, queue overflow and the last sub-level's
-  // discoveries go to the global next frontier (deduplicated per epoch by an
-  // epoch stamp).  Every lowering of h[v] schedules an expansion of v that
-  // re-reads h[v], so the fixpoint is the exact BFS distance (bit-exact with
-  // the reference's FIFO BFS, tested); local_levels = 0 is the strict
-  // level-synchronous BFS with one grid barrier per level.
+  // its own discoveries for up to `local_levels` further BFS sub-levels,
+  // staged in a shared-memory queue and separated by __syncthreads only.
+  // Queue overflow and the last sub-level's discoveries go to the global next
+  // frontier (deduplicated per epoch by an epoch stamp).  Every lowering of
+  // h[v] schedules an expansion of v that re-reads h[v], so the fixpoint is
+  // the exact BFS distance (bit-exact with the reference's FIFO BFS, tested);
+  // local_levels = 0 is the strict level-synchronous BFS.
+  //
+  // A discovery costs one atomic: the item carries a "first visit" flag
+  // (bit 31) and the expansion of that item, which loads off/h anyway, also
+  // loads ex and appends an active vertex to the round list (state.py:62-67)
+  // binned by the degree it just read.  Rows longer than kBin0Max met by a
+  // thread-per-item pass are handed to the CTA's warps (shared list) or, past
+  // kBin1Max, to the next epoch's CTA / grid-wide lists.
+  static constexpr int kFirstBit = (int)0x80000000;
+  static constexpr int kIdMask = 0x7fffffff;
+  static constexpr int kHQ = 256;  // CTA heavy-row list
   unsigned ep_next;  // ownership stamp of the coming asynchronous push phase
   unsigned bst;      // this epoch's stamp for next-frontier dedupe
   int disc_cnt;      // first discoveries (+ bases) by this lane
   int max_lab;       // largest label this lane set
   bool loc_ok;       // discoveries may go to the CTA-local queue
-  bool loc_any;      // label-correcting mode (local_levels > 0)
+  bool nocheck;      // relax with the atomic alone (no h[v] pre-load)
   int lq_nx;         // CTA-local queue receiving discoveries
   int *lqb;          // CTA-local queues (shared memory, 2 x kLQ)
   int *lq_cnt;       // their fill counters (shared memory)
-
-  // Label of v lowered (low) to nl; first = v was unreached.  Warp-synchronous.
-  __device__ __forceinline__ void discovered(bool low, bool first, int v, int nl, int *const *Fn,
-                                             const int *rbase, const int *zero) {
-    int b = 0;
-    bool act = false;
-    if (low) {
-      b = vbin(v);
-      max_lab = nl > max_lab ? nl : max_lab;
-      if (first) {
-        ++disc_cnt;
-        act = v != a.s && v != a.t && ldcg(a.ex + v) > 0;
-        lc.bytes += Bytes<CapT>::kDisc;
-      }
-    }
-    act_cnt += act;
-    if (act && a.async) a.mark[v] = ep_next;  // queued for the push phase = owned
-    append_binned(1, act && !a.topology, v, b, a.ctrl->live + C_RNEXT, a.R, rbase, a.rcap);
-    bool glob = low;
-    if (loc_ok) {  // light vertex: expand it in this CTA's next sub-level
-      bool l = low && b == 0;
-      unsigned m = __ballot_sync(FULL, l);
-      if (m) {
-        int leader = __ffs(m) - 1, pos0 = 0;
-        if (lane == leader) pos0 = atomicAdd(lq_cnt + lq_nx, __popc(m));
-        pos0 = __shfl_sync(FULL, pos0, leader);
-        int p = pos0 + __popc(m & lanemask_lt());
-        if (l && p < kLQ) {
-          lqb[lq_nx * kLQ + p] = v;
-          glob = false;
-        }
-      }
-    }
-    // once per epoch in the global list: a first discovery cannot be listed
-    // yet; a re-lowered vertex may be (label-correcting mode only)
-    if (glob && !first && loc_any) glob = atomicMax(a.bmark + v, bst) < bst;
-    else if (glob && loc_any) a.bmark[v] = bst;
-    append_binned(0, glob, v, b, a.ctrl->live + C_FNEXT, Fn, zero, a.n);
-  }
+  int *hq;           // CTA heavy-row list (shared memory, kHQ)
+  int *hq_cnt;
+  bool hq_ok;        // long rows may go to the CTA's heavy-row list
+  const int *rb_;    // round-list bases of this epoch (shared)
+  int *const *Fn_;   // next-frontier lists of this epoch
 
   __device__ __forceinline__ bool relax(int v, int nl, bool &first) {
     int old = atomicMin(a.h + v, nl);
@@ -408,32 +385,93 @@ struct Kern {
     return nl < old;
   }
 
+  // Label of v lowered (low) to nl; first = v was unreached.  Warp-synchronous.
+  __device__ __forceinline__ void discovered(bool low, bool first, int v, int nl) {
+    if (low) {
+      max_lab = nl > max_lab ? nl : max_lab;
+      if (first) {
+        ++disc_cnt;
+        lc.bytes += Bytes<CapT>::kDisc;
+      }
+    }
+    const int item = v | (first ? kFirstBit : 0);
+    bool glob = low;
+    if (loc_ok) {  // expand it in this CTA's next sub-level
+      unsigned m = __ballot_sync(FULL, low);
+      if (m) {
+        int leader = __ffs(m) - 1, pos0 = 0;
+        if (lane == leader) pos0 = atomicAdd(lq_cnt + lq_nx, __popc(m));
+        pos0 = __shfl_sync(FULL, pos0, leader);
+        int p = pos0 + __popc(m & lanemask_lt());
+        if (low && p < kLQ) {
+          lqb[lq_nx * kLQ + p] = item;
+          glob = false;
+        }
+      }
+    }
+    // once per epoch in the global list: a first discovery cannot be listed
+    // yet; a re-lowered vertex may be (rows handed to the next epoch make
+    // even the level-synchronous mode label-correcting)
+    if (glob && !first) glob = atomicMax(a.bmark + v, bst) < bst;
+    else if (glob) a.bmark[v] = bst;
+    stage(0, glob, item, a.ctrl->live + C_FNEXT, Fn_[0], 0, a.n);
+  }
+
   // Discovery through slot i (valid lanes) of a frontier vertex at label
   // nl - 1: the reverse residual cf[rev i] is read as pc[i] - cf[i] from the
   // same row.
-  __device__ __forceinline__ void discover_slot(bool valid, int i, int nl, int *const *Fn,
-                                                const int *rbase, const int *zero) {
+  __device__ __forceinline__ void discover_slot(bool valid, int i, int nl) {
     int v = valid ? __ldg(a.adj + i) : 0;
     bool low = false, first = false;
     if (valid && v != a.forbidden) {
       CapT r = __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i));
-      if (r > 0 && ldcg(a.h + v) > nl) low = relax(v, nl, first);
+      if (r > 0 && (nocheck || ldcg(a.h + v) > nl)) low = relax(v, nl, first);
     }
-    discovered(low, first, v, nl, Fn, rbase, zero);
+    discovered(low, first, v, nl);
   }
 
-  // Thread-per-vertex expansion for rows of <= kBin0Max slots: every load of
-  // the row is issued before any result is consumed (ILP instead of a
-  // dependent chain per slot).
-  __device__ __forceinline__ void expand_thread(bool valid, int u, int *const *Fn, const int *rbase,
-                                                const int *zero) {
+  // Thread per item: the row (<= kBin0Max slots) is expanded with every load
+  // issued before any result is consumed; first visits join the round list
+  // when active; longer rows are handed on.  Warp-synchronous.
+  __device__ __forceinline__ void expand_item(bool valid, int item) {
+    const int u = item & kIdMask;
+    const bool first = valid && item < 0;
     int lo = 0, d = 0, hu = a.n;
+    long long eu = 0;
     if (valid) {
       lo = __ldg(a.off + u);
       d = __ldg(a.off + u + 1) - lo;
       hu = ldcg(a.h + u);
-      lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kBfsSlot;
+      if (first) eu = ldcg(a.ex + u);
+      lc.bytes += Bytes<CapT>::kVertex;
     }
+    const bool act = first && u != a.s && u != a.t && eu > 0;
+    act_cnt += act;
+    if (act && a.async) a.mark[u] = ep_next;  // queued for the push phase = owned
+    append_binned(1, act && !a.topology, u, bin_of(d), a.ctrl->live + C_RNEXT, a.R, rb_, a.rcap);
+    const bool heavy = valid && d > kBin0Max;
+    if (__any_sync(FULL, heavy)) {
+      // (only items of the grid-wide pass: those are spread evenly over the
+      // CTAs; a CTA's own sub-levels hand long rows to the whole grid)
+      bool mid = hq_ok && heavy && d <= kBin1Max, to_cta = false;
+      unsigned m = __ballot_sync(FULL, mid);
+      if (m) {  // warp-per-row rows: this CTA's warps, after this pass
+        int leader = __ffs(m) - 1, pos0 = 0;
+        if (lane == leader) pos0 = atomicAdd(hq_cnt, __popc(m));
+        pos0 = __shfl_sync(FULL, pos0, leader);
+        int p = pos0 + __popc(m & lanemask_lt());
+        if (mid && p < kHQ) {
+          hq[p] = u;
+          to_cta = true;
+        }
+      }
+      int hb = heavy && !to_cta ? bin_of(d) : 0;
+#pragma unroll
+      for (int b = 1; b < NBIN; ++b)  // next epoch's warp / CTA / grid lists
+        direct(heavy && !to_cta && hb == b, u, a.ctrl->live + C_FNEXT + b, Fn_[b], 0, a.n);
+    }
+    if (heavy) d = 0;
+    lc.bytes += (unsigned long long)d * Bytes<CapT>::kBfsSlot;
     const int nl = hu + 1;
     int vv[kBin0Max], hv[kBin0Max];
     CapT rr[kBin0Max];
@@ -442,17 +480,43 @@ struct Kern {
       vv[k] = k < d ? __ldg(a.adj + lo + k) : -1;
       rr[k] = k < d ? __ldg(a.pc + lo + k) - (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
     }
+    bool low[kBin0Max], fst[kBin0Max];
+    if (nocheck) {
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k)  // head heights across residual slots only
-      hv[k] = (rr[k] > 0 && vv[k] != a.forbidden) ? ldcg(a.h + vv[k]) : -1;
-    bool low[kBin0Max], first[kBin0Max];
+      for (int k = 0; k < kBin0Max; ++k) {
+        fst[k] = false;
+        low[k] = rr[k] > 0 && vv[k] != a.forbidden && relax(vv[k], nl, fst[k]);
+      }
+    } else {
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) {
-      first[k] = false;
-      low[k] = hv[k] > nl && relax(vv[k], nl, first[k]);
+      for (int k = 0; k < kBin0Max; ++k)  // head heights across residual slots only
+        hv[k] = (rr[k] > 0 && vv[k] != a.forbidden) ? ldcg(a.h + vv[k]) : -1;
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) {
+        fst[k] = false;
+        low[k] = hv[k] > nl && relax(vv[k], nl, fst[k]);
+      }
     }
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) discovered(low[k], first[k], vv[k], nl, Fn, rbase, zero);
+    for (int k = 0; k < kBin0Max; ++k) discovered(low[k], fst[k], vv[k], nl);
+  }
+
+  // Warp per row over the CTA's heavy-row list (whole CTA calls).
+  __device__ void drain_heavy() {
+    __syncthreads();
+    int c = *hq_cnt;
+    __syncthreads();
+    if (c == 0) return;
+    if (c > kHQ) c = kHQ;
+    for (int j = wib; j < c; j += kWarps) {
+      int u = hq[j];
+      int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+      int nl = ldcg(a.h + u) + 1;
+      if (lane == 0) lc.bytes += (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
+      for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *hq_cnt = 0;
   }
 
   __device__ void level_flush(int *const *Fn, const int *rbase) {
@@ -482,16 +546,24 @@ struct Kern {
     __shared__ int rb[NBIN];
     __shared__ int s_lq[2][kLQ];
     __shared__ int s_lqc[2];
+    __shared__ int s_hq[kHQ];
+    __shared__ int s_hqc;
     ep_next = ep;
     disc_cnt = 0;
     max_lab = 0;
     loc_ok = false;
-    loc_any = local_levels > 0;
+    nocheck = (a.flags & 1) != 0;
     lqb = &s_lq[0][0];
     lq_cnt = s_lqc;
     lq_nx = 0;
+    hq = s_hq;
+    hq_cnt = &s_hqc;
+    hq_ok = true;
+    rb_ = zero;
+    Fn_ = a.F0;
     if (threadIdx.x < NBIN) zero[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_lqc[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_hqc = 0;
     __syncthreads();
     // empty the R lists (async consumers wait on -1 slots) and the async counters
     if (!a.topology) {  // (topology mode seeds R below and never runs asynchronously)
@@ -541,26 +613,30 @@ struct Kern {
       if (tot == 0 || *sy.s_abort) break;
       if (threadIdx.x < NBIN) rb[threadIdx.x] = sy.s_snap[C_RNEXT + threadIdx.x];
       __syncthreads();
+      rb_ = rb;
       bst = ++bstamp;
-      loc_ok = local_levels > 0;
+      // CTA-local sub-levels only while the frontier is thin (latency-bound
+      // levels); wide levels stay grid-wide so no CTA serialises a share of
+      // them (R-MAT hubs)
+      loc_ok = local_levels > 0 && tot <= a.bfs_local_max * (int)gridDim.x;
       int *const *Fc = (E & 1) ? a.F1 : a.F0;
-      int *const *Fn = (E & 1) ? a.F0 : a.F1;
-      // bin 0: thread per vertex (warp-uniform trip count)
+      Fn_ = (E & 1) ? a.F0 : a.F1;
+      // bin 0: thread per item (warp-uniform trip count)
       for (int j0 = gwarp * 32; j0 < cnt[0]; j0 += gwarps * 32) {
         int j = j0 + lane;
         bool valid = j < cnt[0];
-        expand_thread(valid, valid ? ldcg(Fc[0] + j) : 0, Fn, rb, zero);
+        expand_item(valid, valid ? ldcg(Fc[0] + j) : 0);
       }
-      // bin 1: warp per vertex
+      // bin 1: warp per row
       for (int j = gwarp; j < cnt[1]; j += gwarps) {
         int u = ldcg(Fc[1] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         int nl = ldcg(a.h + u) + 1;
         if (lane == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl, Fn, rb, zero);
+        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl);
       }
-      // bin 2: CTA per vertex
+      // bin 2: CTA per row
       for (int j = blockIdx.x; j < cnt[2]; j += gridDim.x) {
         int u = ldcg(Fc[2] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
@@ -569,10 +645,10 @@ struct Kern {
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i0 = lo; i0 < hi; i0 += blockDim.x) {
           int i = i0 + threadIdx.x;
-          discover_slot(i < hi, i, nl, Fn, rb, zero);
+          discover_slot(i < hi, i, nl);
         }
       }
-      // bin 3: whole grid per vertex
+      // bin 3: whole grid per row
       for (int j = 0; j < cnt[3]; ++j) {
         int u = ldcg(Fc[3] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
@@ -581,11 +657,14 @@ struct Kern {
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i0 = lo + gwarp * 32; i0 < hi; i0 += gthreads) {
           int i = i0 + lane;
-          discover_slot(i < hi, i, nl, Fn, rb, zero);
+          discover_slot(i < hi, i, nl);
         }
       }
-      // CTA-local sub-levels over this CTA's own light discoveries
-      for (int sub = 1; sub <= local_levels; ++sub) {
+      drain_heavy();
+      hq_ok = false;
+      // CTA-local sub-levels over this CTA's own discoveries
+      const bool local_epoch = loc_ok;
+      for (int sub = 1; sub <= local_levels && local_epoch; ++sub) {
         __syncthreads();
         const int cur = lq_nx;
         int c = s_lqc[cur];
@@ -598,11 +677,12 @@ struct Kern {
         for (int j0 = wib * 32; j0 < c; j0 += kWarps * 32) {
           int j = j0 + lane;
           bool valid = j < c;
-          expand_thread(valid, valid ? lqb[cur * kLQ + j] : 0, Fn, rb, zero);
+          expand_item(valid, valid ? lqb[cur * kLQ + j] : 0);
         }
       }
+      hq_ok = true;
       loc_ok = false;
-      level_flush(Fn, rb);
+      level_flush(Fn_, rb);
       grid_sync(a.ctrl, sy, fmask, rmask | amask, 0, PH_BFS);
       ++E;
     }
@@ -622,13 +702,11 @@ struct Kern {
   // =========================================================================
   // push phase (kernels.py:19-67) with in-phase re-activation
   // =========================================================================
-  // Append v to the next wave once (stamp dedupe).  Warp-synchronous.
-  __device__ __forceinline__ void activate(bool pred, int v, unsigned stamp, const int *nbase) {
-    int b = 0;
-    if (pred) {
-      pred = atomicMax(a.mark + v, stamp) < stamp;
-      if (pred) b = vbin(v);
-    }
+  // Append v (degree class b, loaded ahead by the caller) to the next wave
+  // once (stamp dedupe).  Warp-synchronous.
+  __device__ __forceinline__ void activate(bool pred, int v, int b, unsigned stamp,
+                                           const int *nbase) {
+    if (pred) pred = atomicMax(a.mark + v, stamp) < stamp;
     append_binned(1, pred, v, b, a.ctrl->live + C_RNEXT, a.R, nbase, a.rcap);
   }
 
@@ -660,8 +738,12 @@ struct Kern {
       rv[k] = k < d ? __ldg(a.rev + lo + k) : 0;
       cc[k] = k < d ? (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
     }
+    int bb[kBin0Max];  // degree classes of the heads, in flight with their heights
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) hh[k] = cc[k] > 0 ? ldcg(a.h + vv[k]) : INT_MAX;
+    for (int k = 0; k < kBin0Max; ++k) {
+      hh[k] = cc[k] > 0 ? ldcg(a.h + vv[k]) : INT_MAX;
+      bb[k] = cc[k] > 0 ? vbin(vv[k]) : 0;
+    }
     lc.bytes += (unsigned long long)d * Bytes<CapT>::kSlot;
     // Each slot is pushed at most once per visit (a push either saturates it
     // or exhausts u), so the old head excess per slot fits in registers and
@@ -717,7 +799,7 @@ struct Kern {
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) {
       bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
-      activate(p, vv[k], stamp, nbase);
+      activate(p, vv[k], bb[k], stamp, nbase);
     }
     if (Async) {
       // Release ownership, then re-check: a pusher that found u owned did not
@@ -726,9 +808,9 @@ struct Kern {
       if (valid) a.mark[u] = 0;
       __threadfence();
       bool again = valid && hu < n && ldcg(a.ex + u) > 0;
-      activate(again, u, stamp, nbase);
+      activate(again, u, 0, stamp, nbase);  // (rows here have <= kBin0Max slots)
     } else {
-      activate(live && hu < n && e_after > 0, u, stamp, nbase);
+      activate(live && hu < n && e_after > 0, u, 0, stamp, nbase);
     }
   }
 
@@ -814,11 +896,12 @@ struct Kern {
       for (int i0 = first - ((first - lo) % G); i0 < hi && carry < eu; i0 += G) {
         int i = i0 + tid;
         long long c = 0;
-        int v = 0;
+        int v = 0, vb = 0;
         if (i < hi && i >= first) {
           c = (long long)ldcg((const CapT *)(a.cf + i));
           if (c > 0) {
             v = __ldg(a.adj + i);
+            vb = vbin(v);  // in flight with the height
             if (ldcg(a.h + v) != bh) c = 0;
           }
         }
@@ -850,7 +933,7 @@ struct Kern {
           lc.bytes += Bytes<CapT>::kPush;
           if (Async && act) __threadfence();  // push visible before the hand-off
         }
-        activate(act, v, stamp, nbase);
+        activate(act, v, vb, stamp, nbase);
         carry += tot;
       }
       long long moved = carry < eu ? carry : eu;
@@ -873,7 +956,7 @@ struct Kern {
         self = hu < n && e_after > 0;
       }
     }
-    if (G == 32 || wib == 0) activate(self, u, stamp, nbase);
+    if (G == 32 || wib == 0) activate(self, u, bin_of(hi - lo), stamp, nbase);
     if (G > 32) __syncthreads();
   }
 
@@ -1351,6 +1434,8 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.async_budget = cfg.async_budget;
   a.rdirty = W.rdirty;
   a.bfs_local = cfg.bfs_local;
+  a.flags = cfg.flags;
+  a.bfs_local_max = cfg.bfs_local_max;
   a.bmark = W.bmark;
   a.topology = cfg.topology;
   a.what = cfg.what;

@@ -189,6 +189,7 @@ class PartitionedGraph:
     def __init__(self, n, us, vs, caps, source, sink, group=None, bounds=None,
                  device_edges=None):
         self.lib = L.load()
+        self.calls = 0
         self.group = group or LocalGroup(1)
         self.n = int(n)
         self.source, self.sink = int(source), int(sink)
@@ -259,6 +260,7 @@ class PartitionedGraph:
         a = np.zeros(8, np.int64)
         a[:len(args)] = args
         out = np.zeros(8, np.int64)
+        self.calls += 1  # one phase = a few launches + up to 64 B of counters read back
         L.check(self.lib.mfx_part_phase(self.handles[r], phase, L.ptr64(a), L.ptr64(out)))
         return out
 

@@ -62,6 +62,8 @@ class SolverParams:
     schedule: str = "waves"
     async_budget: int = 0
     bfs_local: int = 0
+    bfs_local_max: int = 0
+    device_flags: int = 0
 
     def resolve_threads(self) -> int:
         return 1
@@ -84,10 +86,10 @@ class SolverParams:
         if self.schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {SCHEDULES}, got {self.schedule!r}")
         return L.Params(int(self.kernel_cycles), MODES.index(self.mode), int(self.max_waves),
-                        float(self.timeout_s), int(self.blocks_per_sm), 0,
+                        float(self.timeout_s), int(self.blocks_per_sm), int(self.device_flags),
                         int(self.wave_mult), int(self.wave_add),
                         SCHEDULES.index(self.schedule), int(self.async_budget),
-                        int(self.bfs_local), 0)
+                        int(self.bfs_local), int(self.bfs_local_max))
 
 
 @dataclass
