@@ -163,6 +163,11 @@ int mfx_solve_dynamic(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
 int mfx_solve_dynamic_device(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *d_us,
                              const int64_t *d_vs, const int64_t *d_caps, const mfx_params *p,
                              mfx_result *r);
+/* solve_dynamic_pushpull (dynamic.py:292-377): the O2 push and pull
+ * pipelines on the two sides of the prior cut, then ordinary rounds. */
+int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                               const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
+                               mfx_result *r);
 /* apply_updates (dynamic.py:91-111) alone. */
 int mfx_apply_updates(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
                       const int64_t *vs, const int64_t *new_caps);

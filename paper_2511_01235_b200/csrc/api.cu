@@ -66,6 +66,7 @@ Workspace::~Workspace() {
   dfree(heavy);
   dfree(mark);
   dfree(bmark);
+  dfree(reg);
   dfree(stamp);
   dfree(vbin);
   dfree(rdirty);
@@ -142,6 +143,7 @@ cudaError_t ensure_workspace(Topology &t) {
   }
   if ((e = cudaMalloc(&w.vbin, n))) return e;
   if ((e = launch_vbin(t, w.vbin))) return e;
+  if ((e = cudaMalloc(&w.reg, n))) return e;
   if ((e = cudaMalloc(&w.bmark, sizeof(int) * n))) return e;
   if ((e = cudaMemsetAsync(w.bmark, 0, sizeof(int) * n, t.stream))) return e;
   if ((e = cudaMalloc(&w.mark, sizeof(unsigned) * n))) return e;
@@ -822,6 +824,80 @@ int mfx_solve_dynamic_device(mfx_graph *g, mfx_state *st, int64_t k, const int64
                              const int64_t *d_vs, const int64_t *d_caps, const mfx_params *p,
                              mfx_result *r) {
   return solve_dynamic_common(g, st, k, nullptr, nullptr, nullptr, d_us, d_vs, d_caps, p, r);
+}
+
+// solve_dynamic_pushpull (dynamic.py:292-377): regions from the prior cut,
+// batch pre-phase, A->B saturation, the two region-restricted pipelines as
+// one device round loop, then ordinary dynamic rounds for what crosses.
+int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                               const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
+                               mfx_result *r) {
+  Topology &T = *g->g.topo;
+  memset(r, 0, sizeof(*r));
+  if (st->s.topo != g->g.topo) return fail(MFX_VALUE_ERROR, "state belongs to another graph");
+  SolveConfig cfg;
+  int rc = resolve_config(T, p, cfg);
+  if (rc) return rc;
+  CK(cudaSetDevice(T.device));
+  if ((rc = require_terminated(st, "solve_dynamic_pushpull"))) return rc;
+  {  // the prior heights must carry a cut certificate: s in A, t in B
+    int hs = 0, ht = 0;
+    CK(cudaMemcpy(&hs, st->s.h + st->s.s, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&ht, st->s.h + st->s.t, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hs != T.n || ht == T.n)
+      return fail(MFX_SOLVER_ERROR,
+                  "prior state carries no usable cut certificate; run a full solve first");
+  }
+  CK(ensure_batch_capacity(T, k));
+  int launches = 0;
+  CK(cudaEventRecord(T.ev[0], T.stream));
+  const int64_t *d_us = nullptr, *d_vs = nullptr, *d_caps = nullptr;
+  if (k > 0) {
+    int64_t *d = T.ws.d_batch;
+    CK(cudaMemcpyAsync(d, us, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + k, vs, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    CK(cudaMemcpyAsync(d + 2 * k, new_caps, sizeof(int64_t) * k, cudaMemcpyHostToDevice, T.stream));
+    d_us = d;
+    d_vs = d + k;
+    d_caps = d + 2 * k;
+  }
+  CK(launch_pp_setup(g->g, st->s, false, nullptr));  // regions before the batch
+  ++launches;
+  if (!st->s.excess_consistent) {
+    CK(launch_recompute_excess(g->g, st->s));
+    ++launches;
+  }
+  CK(launch_batch(g->g, &st->s, k, d_us, d_vs, d_caps, true, true, &launches));
+  CK(launch_saturate(g->g, st->s, T.ws.d_err));
+  CK(launch_pp_setup(g->g, st->s, true, T.ws.d_err));  // _saturate_crossing
+  launches += 2;
+  CK(cudaEventRecord(T.ev[1], T.stream));
+  cfg.what = WHAT_SOLVE;
+  cfg.gate = T.ws.d_err;
+  cfg.pushpull = true;
+  CK(launch_solve(g->g, st->s, cfg, &launches));
+  cfg.pushpull = false;  // final pass: overflow on the B side meets deficits on the A side
+  cfg.reset_counters = false;
+  cfg.dyn_bases = 1;
+  cfg.forbidden = st->s.s;
+  CK(launch_solve(g->g, st->s, cfg, &launches));
+  CK(cudaEventRecord(T.ev[2], T.stream));
+  CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaMemcpyAsync(st->host_err, T.ws.d_err, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
+                     T.stream));
+  CK(cudaEventRecord(T.ev[3], T.stream));
+  CK(cudaEventSynchronize(T.ev[3]));
+  CK(cudaGetLastError());
+  if ((rc = batch_error(st->host_err, k, us, vs, new_caps, d_us, d_vs, d_caps))) return rc;
+  fill_result(st, r);
+  r->updates = k;
+  r->ms_update = ev_ms(T.ev[0], T.ev[1]);
+  r->ms_solve = ev_ms(T.ev[1], T.ev[2]);
+  r->ms_total = ev_ms(T.ev[0], T.ev[3]);
+  r->launches = launches;
+  st->s.excess_consistent = true;
+  st->s.terminated_known = r->status == 0;
+  return solve_status(st, r);
 }
 
 int mfx_apply_updates(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,

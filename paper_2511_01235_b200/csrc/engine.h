@@ -23,6 +23,7 @@ struct Workspace {
   int *heavy = nullptr;  // heavy rows scratch, capacity n
   unsigned *mark = nullptr;  // wave stamps, n
   int *bmark = nullptr;      // BFS epoch stamps (next-frontier dedupe), n
+  uint8_t *reg = nullptr;    // push-pull regions (1 = prior cut's A side), n
   unsigned *stamp = nullptr; // current wave stamp (1 word)
   uint8_t *vbin = nullptr;   // degree class per vertex, n
   int *rdirty = nullptr;     // NBIN: used extent of each R list (reset to -1 before reuse)
@@ -96,9 +97,13 @@ struct SolveConfig {
   unsigned long long ceiling = ~0ull;
   bool reset_counters = true;
   const long long *gate = nullptr;  // batch error block: skip the solve if the batch failed
+  bool pushpull = false;  // O2 pipelines (region-restricted push / pull rounds)
 };
 
 cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg, int *launches);
+// push-pull set-up: crossing = false -> regions from the terminated heights;
+// true -> push every A->B residual across the prior cut (gated by a batch)
+cudaError_t launch_pp_setup(const GraphObj &g, StateObj &st, bool crossing, const long long *gate);
 cudaError_t ensure_workspace(Topology &t);
 cudaError_t ensure_batch_capacity(Topology &t, int64_t k);
 

@@ -48,6 +48,7 @@ struct SolveArgs {
   int bfs_local;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int flags;         // bit 0: BFS relaxes with the atomic alone (no pre-load of h[v])
   int bfs_local_max; // CTA-local sub-levels only when the frontier <= this many items per CTA
+  const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
   int what;
@@ -232,7 +233,11 @@ __device__ __forceinline__ long long warp_incl_scan(long long v, int lane) {
   return v;
 }
 
-template <typename CapT>
+// PP = the push-pull pipelines of O2 (dynamic.py:178-377): the prior cut's
+// A side (reg 1) pulls deficits from its supply, the B side (reg 0) pushes
+// overflow to the sink and its deficits, every scan stays inside the vertex's
+// own region, and the two pipelines run as one device round loop.
+template <typename CapT, bool PP = false>
 struct Kern {
   const SolveArgs<CapT> &a;
   Sync &sy;
@@ -275,6 +280,7 @@ struct Kern {
   }
 
   __device__ __forceinline__ int vbin(int v) const { return __ldg(a.vbin + v); }
+  __device__ __forceinline__ int region(int v) const { return PP ? (int)__ldg(a.reg + v) : 0; }
 
   // ---- warp-synchronous list appends (every lane of the warp must call) ----
   __device__ __forceinline__ void stage(int qi, bool pred, int v, int *counter, int *buf, int base,
@@ -420,11 +426,12 @@ struct Kern {
   // Discovery through slot i (valid lanes) of a frontier vertex at label
   // nl - 1: the reverse residual cf[rev i] is read as pc[i] - cf[i] from the
   // same row.
-  __device__ __forceinline__ void discover_slot(bool valid, int i, int nl) {
+  __device__ __forceinline__ void discover_slot(bool valid, int i, int nl, int ru = 0) {
     int v = valid ? __ldg(a.adj + i) : 0;
     bool low = false, first = false;
-    if (valid && v != a.forbidden) {
-      CapT r = __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i));
+    if (valid && v != a.forbidden && (!PP || region(v) == ru)) {
+      CapT f = (CapT)ldcg((const CapT *)(a.cf + i));
+      CapT r = (PP && ru == 1) ? f : __ldg(a.pc + i) - f;  // pull side: forward residual
       if (r > 0 && (nocheck || ldcg(a.h + v) > nl)) low = relax(v, nl, first);
     }
     discovered(low, first, v, nl);
@@ -445,7 +452,8 @@ struct Kern {
       if (first) eu = ldcg(a.ex + u);
       lc.bytes += Bytes<CapT>::kVertex;
     }
-    const bool act = first && u != a.s && u != a.t && eu > 0;
+    const int ru = valid ? region(u) : 0;
+    const bool act = first && u != a.s && u != a.t && (ru == 1 ? eu < 0 : eu > 0);
     act_cnt += act;
     if (act && a.async) a.mark[u] = ep_next;  // queued for the push phase = owned
     append_binned(1, act && !a.topology, u, bin_of(d), a.ctrl->live + C_RNEXT, a.R, rb_, a.rcap);
@@ -480,6 +488,13 @@ struct Kern {
       vv[k] = k < d ? __ldg(a.adj + lo + k) : -1;
       rr[k] = k < d ? __ldg(a.pc + lo + k) - (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
     }
+    if (PP) {  // pull side: forward residuals; either side: own region only
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) {
+        if (k < d && ru == 1) rr[k] = (CapT)ldcg((const CapT *)(a.cf + lo + k));
+        if (k < d && region(vv[k]) != ru) rr[k] = 0;
+      }
+    }
     bool low[kBin0Max], fst[kBin0Max];
     if (nocheck) {
 #pragma unroll
@@ -513,7 +528,7 @@ struct Kern {
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int nl = ldcg(a.h + u) + 1;
       if (lane == 0) lc.bytes += (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-      for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl);
+      for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl, region(u));
     }
     __syncthreads();
     if (threadIdx.x == 0) *hq_cnt = 0;
@@ -585,7 +600,14 @@ struct Kern {
     for (int v0 = gwarp * 32; v0 < n; v0 += gwarps * 32) {
       int v = v0 + lane;
       bool valid = v < n;
-      bool base = valid && (v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0));
+      bool base;
+      if (PP) {  // push side: sink + deficits; pull side: source + overflow
+        long long ev = valid ? ldcg(a.ex + v) : 0;
+        base = valid && (region(v) == 0 ? (v == a.t || (v != a.s && ev < 0))
+                                        : (v == a.s || (v != a.t && ev > 0)));
+      } else {
+        base = valid && (v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0));
+      }
       if (v == a.forbidden) base = false;
       if (valid) a.h[v] = base ? 0 : n;
       disc_cnt += base;
@@ -634,7 +656,7 @@ struct Kern {
         int nl = ldcg(a.h + u) + 1;
         if (lane == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl);
+        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl, region(u));
       }
       // bin 2: CTA per row
       for (int j = blockIdx.x; j < cnt[2]; j += gridDim.x) {
@@ -645,7 +667,7 @@ struct Kern {
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i0 = lo; i0 < hi; i0 += blockDim.x) {
           int i = i0 + threadIdx.x;
-          discover_slot(i < hi, i, nl);
+          discover_slot(i < hi, i, nl, region(u));
         }
       }
       // bin 3: whole grid per row
@@ -657,7 +679,7 @@ struct Kern {
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i0 = lo + gwarp * 32; i0 < hi; i0 += gthreads) {
           int i = i0 + lane;
-          discover_slot(i < hi, i, nl);
+          discover_slot(i < hi, i, nl, region(u));
         }
       }
       drain_heavy();
@@ -721,11 +743,14 @@ struct Kern {
     const int n = a.n;
     int lo = 0, d = 0, hu = n;
     long long eu = 0;
+    const int ru = (PP && valid) ? region(u) : 0;
+    const bool pull = PP && ru == 1;  // pull side: deficit = -excess, reversed residuals
     if (valid) {
       lo = __ldg(a.off + u);
       d = __ldg(a.off + u + 1) - lo;
       hu = ldcg(a.h + u);
       eu = ldcg(a.ex + u);
+      if (pull) eu = -eu;
       lc.bytes += Bytes<CapT>::kVertex;
     }
     const bool live = eu > 0 && hu < n;
@@ -737,6 +762,13 @@ struct Kern {
       vv[k] = k < d ? __ldg(a.adj + lo + k) : 0;
       rv[k] = k < d ? __ldg(a.rev + lo + k) : 0;
       cc[k] = k < d ? (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
+    }
+    if (PP) {
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) {
+        if (k < d && pull) cc[k] = __ldg(a.pc + lo + k) - cc[k];  // cf(v -> u)
+        if (k < d && region(vv[k]) != ru) cc[k] = 0;
+      }
     }
     int bb[kBin0Max];  // degree classes of the heads, in flight with their heights
 #pragma unroll
@@ -776,11 +808,18 @@ struct Kern {
               long long dd = eu < (long long)cc[k] ? eu : (long long)cc[k];
               cc[k] -= (CapT)dd;
               eu -= dd;
-              atomic_add(a.cf + lo + k, (CapT)(-dd));
-              atomic_add(a.cf + rv[k], (CapT)dd);
-              own_old = atomic_add(a.ex + u, -dd);
+              if (pull) {  // pull dd along (v, u) (kernels.py:96-143)
+                atomic_add(a.cf + rv[k], (CapT)(-dd));
+                atomic_add(a.cf + lo + k, (CapT)dd);
+                own_old = -atomic_add(a.ex + u, dd);
+                oldv[k] = -atomic_add(a.ex + vv[k], -dd);
+              } else {
+                atomic_add(a.cf + lo + k, (CapT)(-dd));
+                atomic_add(a.cf + rv[k], (CapT)dd);
+                own_old = atomic_add(a.ex + u, -dd);
+                oldv[k] = add_excess(vv[k], dd);
+              }
               own_d = dd;
-              oldv[k] = add_excess(vv[k], dd);
               pushed |= 1u << k;
             }
           own_atomic = true;
@@ -825,6 +864,8 @@ struct Kern {
     const int n = a.n;
     const int tid = G == 32 ? lane : threadIdx.x;
     int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
+    const int ru = region(u);
+    const bool pull = PP && ru == 1;  // pull side: deficit = -excess, reversed residuals
     int hu;
     long long eu;
     if (G == 32) {
@@ -840,6 +881,7 @@ struct Kern {
       hu = (int)s_red[0];
       eu = s_red[1];
     }
+    if (pull) eu = -eu;
     bool any_push = false;
     long long last_old = 0, last_total = 0;
     for (int cnt = 0; cnt < a.kc; ++cnt) {
@@ -854,6 +896,10 @@ struct Kern {
           int i = i0 + r * G;
           c4[r] = i < hi ? (CapT)ldcg((const CapT *)(a.cf + i)) : (CapT)0;
           v4[r] = i < hi ? __ldg(a.adj + i) : 0;
+          if (PP && i < hi) {
+            if (pull) c4[r] = __ldg(a.pc + i) - c4[r];
+            if (region(v4[r]) != ru) c4[r] = 0;
+          }
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -899,10 +945,11 @@ struct Kern {
         int v = 0, vb = 0;
         if (i < hi && i >= first) {
           c = (long long)ldcg((const CapT *)(a.cf + i));
+          if (pull) c = (long long)__ldg(a.pc + i) - c;
           if (c > 0) {
             v = __ldg(a.adj + i);
             vb = vbin(v);  // in flight with the height
-            if (ldcg(a.h + v) != bh) c = 0;
+            if (ldcg(a.h + v) != bh || (PP && region(v) != ru)) c = 0;
           }
         }
         long long incl = warp_incl_scan(c, lane), tot;
@@ -925,9 +972,16 @@ struct Kern {
         long long amt = room <= 0 ? 0 : (room < c ? room : c);
         bool act = false;
         if (amt > 0) {
-          atomic_add(a.cf + i, (CapT)(-amt));
-          atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
-          long long old = add_excess(v, amt);
+          long long old;
+          if (pull) {  // pull amt along (v, u)
+            atomic_add(a.cf + __ldg(a.rev + i), (CapT)(-amt));
+            atomic_add(a.cf + i, (CapT)amt);
+            old = -atomic_add(a.ex + v, -amt);
+          } else {
+            atomic_add(a.cf + i, (CapT)(-amt));
+            atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
+            old = add_excess(v, amt);
+          }
           act = old <= 0 && v != a.s && v != a.t;
           lc.pushes++;
           lc.bytes += Bytes<CapT>::kPush;
@@ -938,7 +992,7 @@ struct Kern {
       }
       long long moved = carry < eu ? carry : eu;
       if (tid == 0 && moved > 0) {
-        last_old = atomic_add(a.ex + u, -moved);
+        last_old = pull ? -atomic_add(a.ex + u, moved) : atomic_add(a.ex + u, -moved);
         last_total = moved;
       }
       any_push = any_push || moved > 0;
@@ -963,19 +1017,39 @@ struct Kern {
   // =========================================================================
   // repair (kernels.py:70-93): saturate steep residual edges h(u) > h(v)+1
   // =========================================================================
-  __device__ __forceinline__ void repair_slot(int u, int hu, int i) {
-    if (ldcg((const CapT *)(a.cf + i)) > 0) {
+  __device__ __forceinline__ void repair_slot(int u, int hu, int i, int ru = 0) {
+    CapT f = (CapT)ldcg((const CapT *)(a.cf + i));
+    const bool pull = PP && ru == 1;
+    if (pull) f = __ldg(a.pc + i) - f;  // cf(v -> u)
+    if (f > 0) {
       int v = __ldg(a.adj + i);
-      if (hu > ldcg(a.h + v) + 1) {
-        CapT amt = atomic_exch(a.cf + i, (CapT)0);
-        if (amt > 0) {
-          atomic_add(a.cf + __ldg(a.rev + i), amt);
-          atomic_add(a.ex + u, -(long long)amt);
-          add_excess(v, (long long)amt);
-          lc.repairs++;
-          lc.bytes += Bytes<CapT>::kPush;
-        }
+      if ((!PP || region(v) == ru) && hu > ldcg(a.h + v) + 1) {
+        if (pull) repair_pull(u, v, i);
+        else repair_push(u, v, i, i);
       }
+    }
+  }
+
+  // saturate slot i of u (kernels.py:87-91)
+  __device__ __forceinline__ void repair_push(int u, int v, int i, int i2) {
+    CapT amt = atomic_exch(a.cf + i, (CapT)0);
+    if (amt > 0) {
+      atomic_add(a.cf + __ldg(a.rev + i2), amt);
+      atomic_add(a.ex + u, -(long long)amt);
+      add_excess(v, (long long)amt);
+      lc.repairs++;
+      lc.bytes += Bytes<CapT>::kPush;
+    }
+  }
+  // force-pull the full residual of (v, u) (kernels.py:146-165)
+  __device__ __forceinline__ void repair_pull(int u, int v, int i) {
+    CapT amt = atomic_exch(a.cf + __ldg(a.rev + i), (CapT)0);
+    if (amt > 0) {
+      atomic_add(a.cf + i, amt);
+      atomic_add(a.ex + u, (long long)amt);
+      atomic_add(a.ex + v, -(long long)amt);
+      lc.repairs++;
+      lc.bytes += Bytes<CapT>::kPush;
     }
   }
 
@@ -985,6 +1059,7 @@ struct Kern {
       if (u < 0) continue;  // reserved slot never filled (queue overflow)
       int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
       int hu = ldcg(a.h + u);
+      const int ru = region(u);
       lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kSlot;
       int vv[kBin0Max], hv[kBin0Max];
       CapT cc[kBin0Max];
@@ -993,19 +1068,20 @@ struct Kern {
         vv[k] = k < d ? __ldg(a.adj + lo + k) : 0;
         cc[k] = k < d ? (CapT)ldcg((const CapT *)(a.cf + lo + k)) : (CapT)0;
       }
+    if (PP) {
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) {
+        if (k < d && ru == 1) cc[k] = __ldg(a.pc + lo + k) - cc[k];  // cf(v -> u)
+        if (k < d && region(vv[k]) != ru) cc[k] = 0;
+      }
+    }
 #pragma unroll
       for (int k = 0; k < kBin0Max; ++k) hv[k] = cc[k] > 0 ? ldcg(a.h + vv[k]) : INT_MAX - 1;
 #pragma unroll
       for (int k = 0; k < kBin0Max; ++k) {
         if (cc[k] > 0 && hu > hv[k] + 1) {
-          CapT amt = atomic_exch(a.cf + lo + k, (CapT)0);
-          if (amt > 0) {
-            atomic_add(a.cf + __ldg(a.rev + lo + k), amt);
-            atomic_add(a.ex + u, -(long long)amt);
-            add_excess(vv[k], (long long)amt);
-            lc.repairs++;
-            lc.bytes += Bytes<CapT>::kPush;
-          }
+          if (PP && ru == 1) repair_pull(u, vv[k], lo + k);
+          else repair_push(u, vv[k], lo + k, lo + k);
         }
       }
     }
@@ -1015,7 +1091,7 @@ struct Kern {
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int hu = ldcg(a.h + u);
       if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-      for (int i = lo + lane; i < hi; i += 32) repair_slot(u, hu, i);
+      for (int i = lo + lane; i < hi; i += 32) repair_slot(u, hu, i, region(u));
     }
     for (int b = 2; b < NBIN; ++b) {
       for (int j = blockIdx.x; j < end[b]; j += gridDim.x) {
@@ -1025,7 +1101,7 @@ struct Kern {
         int hu = ldcg(a.h + u);
         if (threadIdx.x == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) repair_slot(u, hu, i);
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) repair_slot(u, hu, i, region(u));
       }
     }
   }
@@ -1061,8 +1137,9 @@ struct Kern {
         for (int j = base[b] + blockIdx.x; j < lim[b]; j += gridDim.x)
           push_coop<kBlock, false>(ldcg(a.R[b] + j), next, nbase, s_red);
       stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
-      sink_flush();
-      flush_counters(a.ctrl, lc, scr);
+      // (the sink's excess and the counters are published once per round:
+      // nothing reads them between waves, and the ceiling check may lag a
+      // round)
       grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_PUSH);
       ++waves;
       int tot = 0;
@@ -1318,7 +1395,7 @@ struct Kern {
 #define MFX_MIN_BLOCKS 2
 #endif
 
-template <typename CapT>
+template <typename CapT, bool PP>
 __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     solve_kernel(const __grid_constant__ SolveArgs<CapT> a) {
   __shared__ int s_snap[C_NCTR];
@@ -1349,35 +1426,33 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
   sy.s_snap = s_snap;
   sy.s_abort = &s_abort;
   __syncthreads();
-  Kern<CapT> k(a, sy, lc, wq, &s_sink);
+  Kern<CapT, PP> k(a, sy, lc, wq, &s_sink);
   unsigned stamp = *(volatile unsigned *)a.stamp;  // persistent wave stamp
   unsigned bstamp = ((volatile unsigned *)a.stamp)[1];  // persistent BFS epoch stamp
   if (a.what == WHAT_BARRIER) {  // barrier latency microbenchmark (kc iterations)
     for (int i = 0; i < a.kc && !s_abort; ++i) grid_sync(a.ctrl, sy, 0, 0, 0, PH_FINAL);
-  } else if (a.what == WHAT_BFS) {
-    k.bfs(stamp + 1, bstamp, a.bfs_local);
-    if (k.gtid == 0) a.ctrl->active = (long long)s_snap[C_ACTIVE];
-    flush_counters(a.ctrl, lc, scr);
-  } else if (a.what == WHAT_ROUND) {
-    int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
-    if (a.async) k.push_round_async(stamp, scr);
-    else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
   } else {
-    bool final = true;
-    if (a.what == WHAT_SOLVE) {
-      for (;;) {
-        int L = k.bfs(stamp + 1, bstamp, a.bfs_local);
+    // One call site per phase routine: everything inlines into the kernel
+    // and the Kern state stays in registers (a second call site of bfs or
+    // push_round made nvcc outline it and spill the whole object to local
+    // memory).
+    const bool do_bfs = a.what == WHAT_SOLVE || a.what == WHAT_BFS;
+    const bool do_push = a.what == WHAT_SOLVE || a.what == WHAT_ROUND;
+    int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
+    for (; do_bfs || do_push;) {
+      if (do_bfs) {
+        L = k.bfs(stamp + 1, bstamp, a.bfs_local);
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
-        if (act == 0 || s_abort) break;
-        if (a.async) k.push_round_async(stamp, scr);
-        else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
-        if (s_abort) break;
+        if (act == 0 || s_abort || !do_push) break;
       }
-      flush_counters(a.ctrl, lc, scr);
-      final = !s_abort;
+      if (a.async) k.push_round_async(stamp, scr);
+      else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
+      if (s_abort || !do_bfs) break;
     }
-    if (final) k.finalize((long long *)scr);
+    flush_counters(a.ctrl, lc, scr);
+    bool final = a.what == WHAT_FINAL || (a.what == WHAT_SOLVE && !s_abort);
+    if (final && !PP) k.finalize((long long *)scr);  // (the pipelines end in ordinary rounds)
   }
   if (k.gtid == 0) {  // persistent stamps (every thread advanced identical copies)
     a.stamp[0] = stamp;
@@ -1389,6 +1464,78 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     for (int i = 0; i < PH_N; ++i) a.ctrl->phase_ns[i] += sy.ph[i];
     if (sy.trace) a.ctrl->trace_n = sy.trace_n;
   }
+}
+
+// push-pull set-up (dynamic.py:178-192, 316-318): the prior cut's A side =
+// {h == n} from the terminated state, and every A->B residual pushed across
+template <typename CapT>
+__global__ void pp_region_kernel(const int *h, int n, uint8_t *reg) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    reg[v] = h[v] == n;
+}
+
+// Slot-parallel (the source row of C2 alone holds 2.1 M slots): the tail of a
+// candidate slot (residual into B) is found by binary search of the row
+// offsets, and a warp whose slots share one tail adds its excess change once.
+template <typename CapT>
+__global__ void pp_crossing_kernel(const int *__restrict__ off, const int *__restrict__ adj,
+                                   const int *__restrict__ rev, const uint8_t *__restrict__ reg,
+                                   CapT *cf, long long *ex, int n, int S, const long long *gate) {
+  if (gate && (gate[0] != LLONG_MAX || gate[1] != LLONG_MAX || gate[3] != LLONG_MAX ||
+               gate[4] != LLONG_MAX))
+    return;
+  for (int i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; i0 < S;
+       i0 += gridDim.x * blockDim.x) {
+    const int i = i0 + (threadIdx.x & 31);
+    CapT c = 0;
+    int u = -1;
+    if (i < S) {
+      c = cf[i];
+      if (c > 0 && !reg[adj[i]]) {
+        int lo = 0, hi = n;  // last row with off[row] <= i
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (off[mid] <= i) lo = mid;
+          else hi = mid;
+        }
+        u = reg[lo] ? lo : -1;
+      }
+    }
+    if (u >= 0) {
+      cf[i] = 0;
+      atomic_add(cf + rev[i], c);
+      atomic_add(ex + adj[i], (long long)c);
+    }
+    const unsigned any = __ballot_sync(0xffffffffu, u >= 0);
+    if (!any) continue;
+    const int u0 = __shfl_sync(0xffffffffu, u, __ffs(any) - 1);
+    if (__all_sync(0xffffffffu, u < 0 || u == u0)) {
+      long long tot = warp_sum(u >= 0 ? (long long)c : 0ll);
+      if ((threadIdx.x & 31) == 0) atomic_add(ex + u0, -tot);
+    } else if (u >= 0) {
+      atomic_add(ex + u, -(long long)c);
+    }
+  }
+}
+
+template <typename CapT>
+static cudaError_t launch_pp_setup_t(const GraphObj &g, StateObj &st, bool crossing,
+                                     const long long *gate) {
+  Topology &T = *g.topo;
+  cudaError_t e = ensure_workspace(T);
+  if (e) return e;
+  int grid = T.num_sms * 8;
+  if (!crossing) pp_region_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(st.h, T.n, T.ws.reg);
+  else
+    pp_crossing_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(T.off, T.adj, T.rev, T.ws.reg,
+                                                           (CapT *)st.cf, st.ex, T.n, T.S, gate);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pp_setup(const GraphObj &g, StateObj &st, bool crossing, const long long *gate) {
+  if (g.topo->cap_bytes == 8) return launch_pp_setup_t<long long>(g, st, crossing, gate);
+  return launch_pp_setup_t<int>(g, st, crossing, gate);
 }
 
 __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long ceiling,
@@ -1462,15 +1609,22 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.gate = cfg.gate;
   a.trace = W.trace;
   a.trace_cap = W.trace_cap;
+  a.reg = cfg.pushpull ? W.reg : nullptr;
+  if (cfg.pushpull) {
+    a.async = 0;
+    a.forbidden = -1;
+  }
 
   ctrl_begin_kernel<<<1, 1, 0, T.stream>>>(st.ctrl, cfg.timeout_s, cfg.ceiling,
                                           cfg.reset_counters ? 1 : 0);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
-  static int occ_cache[2] = {0, 0};
-  int &occ = occ_cache[sizeof(CapT) == 8];
+  const void *fn = cfg.pushpull ? (const void *)solve_kernel<CapT, true>
+                                : (const void *)solve_kernel<CapT, false>;
+  static int occ_cache[4] = {0, 0, 0, 0};
+  int &occ = occ_cache[(sizeof(CapT) == 8) * 2 + (cfg.pushpull ? 1 : 0)];
   if (occ == 0) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, solve_kernel<CapT>, kBlock, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
   }
@@ -1478,7 +1632,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   if (cfg.blocks_per_sm > 0 && cfg.blocks_per_sm < bps) bps = cfg.blocks_per_sm;
   dim3 grid(T.num_sms * bps), block(kBlock);
   void *args[] = {(void *)&a};
-  e = cudaLaunchCooperativeKernel((const void *)solve_kernel<CapT>, grid, block, args, 0, T.stream);
+  e = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, T.stream);
   if (launches) *launches += 2;
   count_launch(2);
   return e;

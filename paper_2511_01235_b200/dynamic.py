@@ -108,6 +108,26 @@ def solve_dynamic(st: SolverState, g: BiCsrGraph, batch: UpdateBatch,
     return _result(r, st, g)
 
 
+def solve_dynamic_pushpull(st: SolverState, g: BiCsrGraph, batch: UpdateBatch,
+                           params: SolverParams | None = None) -> FlowResult:
+    """Dynamic recompute with the push and pull pipelines of O2
+    (dynamic.py:292-377): the prior terminal heights give the cut (A =
+    {h == n}); after the batch every A->B residual is pushed across, the B
+    side pushes overflow to the sink and its deficits while the A side pulls
+    its deficits from the source and its overflow (region-restricted, one
+    device round loop for both), then ordinary rounds connect what is left.
+    Same flow value as :func:`solve_dynamic`."""
+    params = params or SolverParams()
+    params.validate()
+    p = params.to_c()
+    us, vs, cs = batch.arrays()
+    r = L.Result()
+    L.check(L.load().mfx_solve_dynamic_pushpull(g.handle, st.handle, us.size, L.ptr64(us),
+                                                L.ptr64(vs), L.ptr64(cs), ctypes.byref(p),
+                                                ctypes.byref(r)))
+    return _result(r, st, g)
+
+
 def solve_dynamic_device(st: SolverState, g: BiCsrGraph, k: int, d_us: int, d_vs: int,
                          d_caps: int, params: SolverParams | None = None) -> FlowResult:
     """solve_dynamic with the batch already resident in device memory (raw
@@ -133,5 +153,5 @@ def updated_edge_list(g: BiCsrGraph, batch: UpdateBatch) -> EdgeListGraph:
 
 
 __all__ = ["BatchError", "UpdateBatch", "apply_updates", "recompute_excess", "dynamic_prephase",
-           "backward_bfs_dynamic", "solve_dynamic", "solve_dynamic_device", "updated_edge_list",
+           "backward_bfs_dynamic", "solve_dynamic", "solve_dynamic_device", "solve_dynamic_pushpull", "updated_edge_list",
            "SolverError"]

@@ -79,6 +79,7 @@ def main():
     base = g.copy()
     for spec in args.knobs:
         kn = parse_knobs(spec)
+        pp = bool(kn.pop("pp", 0))  # O2 push-pull dynamic solves
         p = mfx.SolverParams(**kn)
         gg = base.copy()
         mfx.solve_static(gg, s, t, p)  # warm
@@ -93,7 +94,8 @@ def main():
         st = r.state
         dyn = []
         for bu, bv, bc in chain:
-            rr = mfx.solve_dynamic(st, gg, mfx.UpdateBatch(bu, bv, bc), p)
+            solve = mfx.solve_dynamic_pushpull if pp else mfx.solve_dynamic
+            rr = solve(st, gg, mfx.UpdateBatch(bu, bv, bc), p)
             flows.append(rr.flow_value)
             dd = rr.device
             dyn.append((dd["ms_total"], rr.rounds, dd["bfs_levels"], dd["waves"], dd["ns_bfs"] / 1e6,

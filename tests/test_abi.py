@@ -63,3 +63,20 @@ def test_no_cpu_fallback_when_library_missing(tmp_path, monkeypatch):
 def test_version_and_launch_counter(lib):
     assert lib.mfx_version() == 1
     assert lib.mfx_launch_count() >= 0
+
+
+def test_solve_kernel_state_stays_in_registers():
+    """Regression guard (SASS of the persistent solve kernel): a phase
+    routine outlined by nvcc drags the whole Kern object into local memory
+    (a 25x local-load/store blow-up measured at 1.7x slower solves)."""
+    import subprocess
+    from paper_2511_01235_b200 import _lib
+    for pp in (0, 1):
+        fn = f"_ZN3mfx12solve_kernelIiLb{pp}EEEvNS_9SolveArgsIT_EE"
+        sass = subprocess.run(["cuobjdump", "-sass", "-fun", fn, _lib.LIB_PATH],
+                              capture_output=True, text=True).stdout
+        assert "Function" in sass, fn
+        local = len(re.findall(r"\b(?:STL|LDL)\b", sass))
+        calls = len(re.findall(r"\bCALL\b", sass))
+        assert local < 300, (fn, local)
+        assert calls <= 16, (fn, calls)  # the grid barrier is the only out-of-line routine
