@@ -391,7 +391,9 @@ def bench_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/batch",
         "n_gpus": world, "steps": len(times), "warmup": 0, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic", "config": config_block(args, world),
+        "data": "synthetic",
+        "config": dict(config_block(args, world), parallelism=f"{cores} host threads (numba)"
+                       if kind == "reference" else "1 host thread (C oracle port)"),
         "static_maxflow_edges_per_s": round(m_orig / static_s, 1), "static_ms": round(1e3 * static_s, 1),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/batch", "cores": cores, "kind": kind,
                          "sample": sample},
