@@ -90,6 +90,7 @@ struct SolveConfig {
   int async_budget = 16;  // items per initially active vertex before a global relabel
   int flags = 0;          // mfx_params.flags (bit 0: BFS without h pre-load)
   int bfs_local_max = 64; // ... while the frontier holds <= this many items per CTA
+  int lq_cap = kLQ;       // CTA-local queue capacity per sub-level
   int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;

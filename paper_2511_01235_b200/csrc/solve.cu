@@ -48,6 +48,7 @@ struct SolveArgs {
   int bfs_local;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int flags;         // bit 0: BFS relaxes with the atomic alone (no pre-load of h[v])
   int bfs_local_max; // CTA-local sub-levels only when the frontier <= this many items per CTA
+  int lq_cap;        // CTA-local queue capacity per sub-level (<= kLQ; the rest spills)
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -409,7 +410,7 @@ struct Kern {
         if (lane == leader) pos0 = atomicAdd(lq_cnt + lq_nx, __popc(m));
         pos0 = __shfl_sync(FULL, pos0, leader);
         int p = pos0 + __popc(m & lanemask_lt());
-        if (low && p < kLQ) {
+        if (low && p < a.lq_cap) {
           lqb[lq_nx * kLQ + p] = item;
           glob = false;
         }
@@ -692,7 +693,7 @@ struct Kern {
         int c = s_lqc[cur];
         __syncthreads();
         if (c == 0) break;
-        if (c > kLQ) c = kLQ;
+        if (c > a.lq_cap) c = a.lq_cap;
         if (threadIdx.x == 0) s_lqc[cur] = 0;  // cur becomes the receiver after next
         lq_nx = cur ^ 1;
         loc_ok = sub < local_levels;
@@ -1583,6 +1584,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.bfs_local = cfg.bfs_local;
   a.flags = cfg.flags;
   a.bfs_local_max = cfg.bfs_local_max;
+  a.lq_cap = cfg.lq_cap < 1 ? 1 : cfg.lq_cap > kLQ ? kLQ : cfg.lq_cap;
   a.bmark = W.bmark;
   a.topology = cfg.topology;
   a.what = cfg.what;
