@@ -150,6 +150,33 @@ cudaError_t ensure_workspace(Topology &t) {
   return cudaMemsetAsync(w.mark, 0, sizeof(unsigned) * n, t.stream);
 }
 
+// Variant choice: graphs with most slots in long rows (R-MAT: 91 % in rows of
+// >= 32 slots) gain from 4x the resident warps; grids and roads (short rows,
+// long BFS) lose to the spills of the 64-register build.  $MFX_VARIANT = 256 |
+// 512 overrides.
+static int choose_variant(Topology &t) {
+  if (t.variant >= 0) return t.variant;
+  int v = 0;
+  if (const char *e = getenv("MFX_VARIANT")) {
+    v = atoi(e) == 512 ? 1 : 0;
+  } else {
+    int pm = 0;
+    if (long_row_permille(t, &pm) == cudaSuccess && pm >= 500) v = 1;
+  }
+  t.variant = v;
+  return v;
+}
+
+cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg, int *launches) {
+  if (choose_variant(*g.topo)) return v512::launch_solve(g, st, cfg, launches);
+  return v256::launch_solve(g, st, cfg, launches);
+}
+
+cudaError_t launch_pp_setup(const GraphObj &g, StateObj &st, bool crossing, const long long *gate) {
+  if (choose_variant(*g.topo)) return v512::launch_pp_setup(g, st, crossing, gate);
+  return v256::launch_pp_setup(g, st, crossing, gate);
+}
+
 cudaError_t ensure_batch_capacity(Topology &t, int64_t k) {
   Workspace &w = t.ws;
   if (k <= w.kcap && w.d_batch) return cudaSuccess;

@@ -52,6 +52,7 @@ struct Topology {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};
   int num_sms = 0;
+  int variant = -1;  // solve-kernel build: 0 = v256, 1 = v512 (-1: not chosen yet)
   Workspace ws;
   ~Topology();
 };
@@ -101,10 +102,21 @@ struct SolveConfig {
   bool pushpull = false;  // O2 pipelines (region-restricted push / pull rounds)
 };
 
+// Dispatch to the solve-kernel build chosen for the graph (Topology::variant).
 cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg, int *launches);
 // push-pull set-up: crossing = false -> regions from the terminated heights;
 // true -> push every A->B residual across the prior cut (gated by a batch)
 cudaError_t launch_pp_setup(const GraphObj &g, StateObj &st, bool crossing, const long long *gate);
+namespace v256 {
+cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg, int *launches);
+cudaError_t launch_pp_setup(const GraphObj &g, StateObj &st, bool crossing, const long long *gate);
+}  // namespace v256
+namespace v512 {
+cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg, int *launches);
+cudaError_t launch_pp_setup(const GraphObj &g, StateObj &st, bool crossing, const long long *gate);
+}  // namespace v512
+// fraction (in 1/1000) of the slots that sit in rows longer than kBin0Max
+cudaError_t long_row_permille(const Topology &t, int *permille);
 cudaError_t ensure_workspace(Topology &t);
 cudaError_t ensure_batch_capacity(Topology &t, int64_t k);
 

@@ -28,7 +28,16 @@
 
 #include "engine.h"
 
+#ifndef MFX_SOLVE_NS
+#define MFX_SOLVE_NS v256
+#endif
+
 namespace mfx {
+// Compiled twice (Makefile): v256 = 256-thread CTAs, 2 per SM, no register
+// cap (latency-bound grids and roads); v512 = 512-thread CTAs, 2 per SM,
+// 64 registers (4x the resident warps, for graphs whose slots sit mostly in
+// long rows, e.g. R-MAT).  api.cu picks per graph (Topology::variant).
+namespace MFX_SOLVE_NS {
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -1645,4 +1654,5 @@ cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg
   return launch_solve_t<int>(g, st, cfg, launches);
 }
 
+}  // namespace MFX_SOLVE_NS
 }  // namespace mfx

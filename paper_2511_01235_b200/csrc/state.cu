@@ -91,6 +91,32 @@ __global__ void vbin_kernel(const int *off, int n, uint8_t *vbin) {
     vbin[v] = (uint8_t)bin_of(off[v + 1] - off[v]);
 }
 
+__global__ void long_rows_kernel(const int *off, int n, unsigned long long *acc) {
+  unsigned long long x = 0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int d = off[v + 1] - off[v];
+    if (d > kBin0Max) x += (unsigned long long)d;
+  }
+  x = warp_sum(x);
+  if ((threadIdx.x & 31) == 0 && x) atomicAdd(acc, x);
+}
+
+cudaError_t long_row_permille(const Topology &t, int *permille) {
+  *permille = 0;
+  if (t.S <= 0) return cudaSuccess;
+  unsigned long long *d = nullptr, h = 0;
+  cudaError_t e = cudaMalloc(&d, sizeof(h));
+  if (e) return e;
+  cudaMemsetAsync(d, 0, sizeof(h), t.stream);
+  long_rows_kernel<<<grid_for(t.n, t.num_sms), kBlock, 0, t.stream>>>(t.off, t.n, d);
+  count_launch();
+  e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, t.stream);
+  if (!e) e = cudaStreamSynchronize(t.stream);
+  cudaFree(d);
+  *permille = (int)(1000.0 * (double)h / (double)t.S);
+  return e;
+}
+
 cudaError_t launch_vbin(const Topology &t, uint8_t *vbin) {
   if (t.n == 0) return cudaSuccess;
   vbin_kernel<<<grid_for(t.n, t.num_sms), kBlock, 0, t.stream>>>(t.off, t.n, vbin);

@@ -68,15 +68,17 @@ def test_version_and_launch_counter(lib):
 def test_solve_kernel_state_stays_in_registers():
     """Regression guard (SASS of the persistent solve kernel): a phase
     routine outlined by nvcc drags the whole Kern object into local memory
-    (a 25x local-load/store blow-up measured at 1.7x slower solves)."""
+    (a 25x local-load/store blow-up measured at 1.7x slower solves).  The
+    64-register v512 build spills by design; its budget is separate."""
     import subprocess
     from paper_2511_01235_b200 import _lib
-    for pp in (0, 1):
-        fn = f"_ZN3mfx12solve_kernelIiLb{pp}EEEvNS_9SolveArgsIT_EE"
-        sass = subprocess.run(["cuobjdump", "-sass", "-fun", fn, _lib.LIB_PATH],
-                              capture_output=True, text=True).stdout
-        assert "Function" in sass, fn
-        local = len(re.findall(r"\b(?:STL|LDL)\b", sass))
-        calls = len(re.findall(r"\bCALL\b", sass))
-        assert local < 300, (fn, local)
-        assert calls <= 16, (fn, calls)  # the grid barrier is the only out-of-line routine
+    for ns, budget in (("v256", 300), ("v512", 1500)):
+        for pp in (0, 1):
+            fn = f"_ZN3mfx{len(ns)}{ns}12solve_kernelIiLb{pp}EEEvNS0_9SolveArgsIT_EE"
+            sass = subprocess.run(["cuobjdump", "-sass", "-fun", fn, _lib.LIB_PATH],
+                                  capture_output=True, text=True).stdout
+            assert "Function" in sass, fn
+            local = len(re.findall(r"\b(?:STL|LDL)\b", sass))
+            calls = len(re.findall(r"\bCALL\b", sass))
+            assert local < budget, (fn, local)
+            assert calls <= 16, (fn, calls)  # the grid barrier is the only out-of-line routine
