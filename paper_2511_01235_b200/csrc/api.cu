@@ -639,6 +639,8 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   if (p->bfs_local_max > 0) cfg.bfs_local_max = p->bfs_local_max;
   if (const char *bm = getenv("MFX_BFS_LOCAL_MAX")) cfg.bfs_local_max = atoi(bm);
   if (const char *lc = getenv("MFX_LQ_CAP")) cfg.lq_cap = atoi(lc);
+  if (const char *ti = getenv("MFX_TAIL_ITEMS")) cfg.tail_items = atoi(ti);
+  if (const char *tc = getenv("MFX_TAIL_CAP")) cfg.tail_cap = atoi(tc);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;

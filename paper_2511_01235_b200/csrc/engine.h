@@ -92,6 +92,8 @@ struct SolveConfig {
   int flags = 0;          // mfx_params.flags (bit 0: BFS without h pre-load)
   int bfs_local_max = 64; // ... while the frontier holds <= this many items per CTA
   int lq_cap = kLQ;       // CTA-local queue capacity per sub-level
+  int tail_items = 0;     // push: extra waves past the budget while a wave holds <= tail_items
+  int tail_cap = 0;       //   ... up to tail_cap waves per round
   int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;

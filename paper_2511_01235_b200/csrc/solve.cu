@@ -58,6 +58,8 @@ struct SolveArgs {
   int flags;         // bit 0: BFS relaxes with the atomic alone (no pre-load of h[v])
   int bfs_local_max; // CTA-local sub-levels only when the frontier <= this many items per CTA
   int lq_cap;        // CTA-local queue capacity per sub-level (<= kLQ; the rest spills)
+  int tail_items;    // push: after the wave budget, continue while a wave holds <= this many
+  int tail_cap;      //   ... up to this many waves in the round
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -101,7 +103,11 @@ struct Local {
 
 // per-warp staging queues in shared memory: q0 = next frontier (bin 0),
 // q1 = next push wave / active list (bin 0)
-constexpr int kWQ = 64;
+#ifndef MFX_WQ
+#define MFX_WQ 64
+#endif
+constexpr int kWQ = MFX_WQ;         // per-warp staging capacity (per queue)
+constexpr int kFlush = kWQ - 32;    // publish once this many items are staged
 struct WarpQ {
   int cnt[2];
   int item[2][kWQ];
@@ -301,16 +307,16 @@ struct Kern {
     if (pred) q->item[qi][c + __popc(b & lanemask_lt())] = v;
     c += __popc(b);
     __syncwarp();
-    if (c >= 32) {  // publish 32 staged items with one atomic
+    if (c >= kFlush) {  // publish everything staged with one atomic
       int g = 0;
-      if (lane == 0) g = atomicAdd(counter, 32);
+      if (lane == 0) g = atomicAdd(counter, c);
       g = __shfl_sync(FULL, g, 0);
-      int p = base + g + lane;
-      if (p < cap) buf[p] = q->item[qi][lane];
-      else a.ctrl->overflow = 1;
-      __syncwarp();
-      if (lane < c - 32) q->item[qi][lane] = q->item[qi][lane + 32];
-      c -= 32;
+      for (int k = lane; k < c; k += 32) {
+        int p = base + g + k;
+        if (p < cap) buf[p] = q->item[qi][k];
+        else a.ctrl->overflow = 1;
+      }
+      c = 0;
     }
     __syncwarp();
     if (lane == 0) q->cnt[qi] = c;
@@ -323,9 +329,9 @@ struct Kern {
     int g = 0;
     if (lane == 0) g = atomicAdd(counter, c);
     g = __shfl_sync(FULL, g, 0);
-    if (lane < c) {
-      int p = base + g + lane;
-      if (p < cap) buf[p] = q->item[qi][lane];
+    for (int k = lane; k < c; k += 32) {
+      int p = base + g + k;
+      if (p < cap) buf[p] = q->item[qi][k];
       else a.ctrl->overflow = 1;
     }
     __syncwarp();
@@ -651,6 +657,8 @@ struct Kern {
       // levels); wide levels stay grid-wide so no CTA serialises a share of
       // them (R-MAT hubs)
       loc_ok = local_levels > 0 && tot <= a.bfs_local_max * (int)gridDim.x;
+      // flags bit 1: thin (latency-bound) epochs relax by atomic alone
+      nocheck = (a.flags & 1) != 0 || ((a.flags & 2) != 0 && loc_ok);
       int *const *Fc = (E & 1) ? a.F1 : a.F0;
       Fn_ = (E & 1) ? a.F0 : a.F1;
       // bin 0: thread per item (warp-uniform trip count)
@@ -1158,7 +1166,10 @@ struct Kern {
         cnt[b] = sy.s_snap[C_RNEXT + b];
         tot += cnt[b];
       }
-      if (tot == 0 || waves >= max_waves || *sy.s_abort) break;
+      // past the budget, keep going while the waves stay small (a thin wave
+      // costs ~1 % of a global relabel) up to tail_cap waves
+      if (tot == 0 || *sy.s_abort) break;
+      if (waves >= max_waves && (tot > a.tail_items || waves >= a.tail_cap)) break;
     }
     int end[NBIN];
     for (int b = 0; b < NBIN; ++b) {
@@ -1594,6 +1605,8 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.flags = cfg.flags;
   a.bfs_local_max = cfg.bfs_local_max;
   a.lq_cap = cfg.lq_cap < 1 ? 1 : cfg.lq_cap > kLQ ? kLQ : cfg.lq_cap;
+  a.tail_items = cfg.tail_items;
+  a.tail_cap = cfg.tail_cap;
   a.bmark = W.bmark;
   a.topology = cfg.topology;
   a.what = cfg.what;
