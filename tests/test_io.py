@@ -97,3 +97,27 @@ def test_parse_updates_matches_reference(name):
         want = GOLD[name]["ok"]
         assert out.us.tolist() == want["us"] and out.vs.tolist() == want["vs"]
         assert out.new_caps.tolist() == want["caps"]
+
+
+@pytest.mark.gpu
+def test_run_benchmark_schema_and_plot_data(tmp_path):
+    """Reference bench.py run_benchmark schema on the GPU engine: three modes
+    per spec, identical verified flows, gnuplot tables per kind."""
+    import paper_2511_01235_b200 as mf
+    us, vs, caps, s, t = mf.random_graph(400, 4000, seed=3)
+    g = mf.EdgeListGraph(400, us, vs, caps)
+    specs = [mf.BatchSpec(5.0, "mixed", 0), mf.BatchSpec(10.0, "inc", 1), mf.BatchSpec(5.0, "dec", 2)]
+    recs = mf.run_benchmark(g, s, t, specs, reps=2, instance="r400")
+    assert [r.mode for r in recs] == list(mf.BENCH_MODES) * 3
+    for i in range(0, 9, 3):
+        assert len({r.flow_value for r in recs[i:i + 3]}) == 1
+        assert all(r.verified and r.total_ms > 0 for r in recs[i:i + 3])
+    paths = mf.write_plot_data(recs, tmp_path)
+    assert sorted(os.path.basename(p) for p in paths) == ["dec.dat", "inc.dat", "mixed.dat"]
+    lines = open(paths[0]).read().splitlines()
+    assert lines[0] == "# pct dynamic pushpull static" and len(lines) == 2
+    mio.write_results(tmp_path / "r.csv", recs)
+    back = mio.read_results(tmp_path / "r.csv")  # (times round-trip at 3 decimals)
+    assert [(r.mode, r.flow_value, r.verified) for r in back] == \
+        [(r.mode, r.flow_value, r.verified) for r in recs]
+    assert all(abs(a.total_ms - b.total_ms) < 1e-3 for a, b in zip(back, recs))
