@@ -53,6 +53,7 @@ enum CtrIdx {
   C_HUGE = 11,   // huge rows (finalize)
   C_REACHED = 12, // vertices reached by the global relabel (bases + first discoveries)
   C_DEPTH = 13,  // largest BFS label set (max-combined, not summed)
+  C_EHOLD = 14,  // vertices holding excess when the global relabel started
   C_NCTR = 16
 };
 

@@ -571,8 +571,9 @@ struct Kern {
   // Returns the BFS depth (levels incl. level 0 = max label + 1); the active
   // set is left in R (wave 0).  ep: ownership stamp the following
   // asynchronous push phase will use; bstamp: persistent epoch stamp.
-  __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels) {
+  __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels, bool early) {
     const int n = a.n;
+    int holders = 0;  // vertices (not s, t) with positive excess
     __shared__ int zero[NBIN];
     __shared__ int rb[NBIN];
     __shared__ int s_lq[2][kLQ];
@@ -622,7 +623,9 @@ struct Kern {
         base = valid && (region(v) == 0 ? (v == a.t || (v != a.s && ev < 0))
                                         : (v == a.s || (v != a.t && ev > 0)));
       } else {
-        base = valid && (v == a.t || (a.dyn_bases && v != a.s && ldcg(a.ex + v) < 0));
+        long long ev = valid ? ldcg(a.ex + v) : 0;
+        base = valid && (v == a.t || (a.dyn_bases && v != a.s && ev < 0));
+        holders += valid && v != a.s && v != a.t && ev > 0;
       }
       if (v == a.forbidden) base = false;
       if (valid) a.h[v] = base ? 0 : n;
@@ -635,9 +638,11 @@ struct Kern {
       append_binned(1, topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap);
     }
     level_flush(a.F0, zero);
+    holders = warp_sum(holders);
+    if (lane == 0 && holders) atomicAdd(a.ctrl->live + C_EHOLD, holders);
     lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
     const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
-    const unsigned amask = (1u << C_ACTIVE) | (1u << C_REACHED) | (1u << C_DEPTH);
+    const unsigned amask = (1u << C_ACTIVE) | (1u << C_REACHED) | (1u << C_DEPTH) | (1u << C_EHOLD);
     grid_sync(a.ctrl, sy, fmask | (1u << C_BASES), rmask | amask, rmask | amask, PH_BFS);
     int E = 0;
     for (;;) {
@@ -649,6 +654,12 @@ struct Kern {
         tot += cnt[b];
       }
       if (tot == 0 || *sy.s_abort) break;
+      // Early exit (solve rounds only): every vertex holding excess has been
+      // expanded, so the round's active list is complete; vertices beyond
+      // keep h = n, which no push can cross, and the solve's last global
+      // relabel (no holder left) always runs to the end, so the certificate
+      // still comes from exact distances.
+      if (early && sy.s_snap[C_EHOLD] > 0 && sy.s_snap[C_ACTIVE] >= sy.s_snap[C_EHOLD]) break;
       if (threadIdx.x < NBIN) rb[threadIdx.x] = sy.s_snap[C_RNEXT + threadIdx.x];
       __syncthreads();
       rb_ = rb;
@@ -1462,7 +1473,10 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
     for (; do_bfs || do_push;) {
       if (do_bfs) {
-        L = k.bfs(stamp + 1, bstamp, a.bfs_local);
+        // (flags bit 2 enables the early exit -- measured no faster on C1-C4;
+        // the bit-exact global relabel entry point, WHAT_BFS, never takes it)
+        L = k.bfs(stamp + 1, bstamp, a.bfs_local,
+                  a.what == WHAT_SOLVE && !a.topology && !PP && (a.flags & 4) != 0);
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
         if (act == 0 || s_abort || !do_push) break;

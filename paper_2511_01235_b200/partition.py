@@ -190,6 +190,7 @@ class PartitionedGraph:
                  device_edges=None):
         self.lib = L.load()
         self.calls = 0
+        self.phase_s = {}  # host-observed seconds per phase kind (synchronous calls)
         self.group = group or LocalGroup(1)
         self.n = int(n)
         self.source, self.sink = int(source), int(sink)
@@ -261,7 +262,9 @@ class PartitionedGraph:
         a[:len(args)] = args
         out = np.zeros(8, np.int64)
         self.calls += 1  # one phase = a few launches + up to 64 B of counters read back
+        t0 = time.perf_counter()
         L.check(self.lib.mfx_part_phase(self.handles[r], phase, L.ptr64(a), L.ptr64(out)))
+        self.phase_s[phase] = self.phase_s.get(phase, 0.0) + time.perf_counter() - t0
         return out
 
     def _phase_all(self, phase, args=None):

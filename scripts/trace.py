@@ -64,6 +64,34 @@ def report(tag, st, g, res):
                       f"mean {d[k].mean():7.1f} us, items/phase {w[k].mean():9.0f}")
 
 
+def rounds_view(tag, st, g):
+    """Per round: BFS epochs + time, then the push waves' item counts."""
+    ph, items, dt = fetch(st, g)
+    keep = ph != 7
+    ph, items, dt = ph[keep], items[keep], dt[keep]
+    work = np.concatenate([[0], items[:-1]])
+    print(f"-- {tag}: per-round sequence")
+    i, rnd = 0, 0
+    while i < len(ph):
+        j = i
+        while j < len(ph) and ph[j] == 0:
+            j += 1
+        bfs_us = dt[i:j].sum() / 1e3
+        k = j
+        while k < len(ph) and ph[k] == 1:
+            k += 1
+        waves = work[j:k]
+        push_us = dt[j:k].sum() / 1e3
+        rep = dt[k:k + 1].sum() / 1e3 if k < len(ph) and ph[k] == 2 else 0.0
+        print(f"  round {rnd}: bfs {j - i} epochs {bfs_us:8.1f} us | {k - j} waves {push_us:8.1f} us "
+              f"items first/max/last {waves[:1].tolist()}/{int(waves.max()) if len(waves) else 0}/"
+              f"{waves[-1:].tolist()} | repair {rep:6.1f} us")
+        i = k + (1 if k < len(ph) and ph[k] == 2 else 0)
+        rnd += 1
+        if j == i and k == j:
+            break
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--side", type=int, default=2048)
@@ -80,6 +108,7 @@ def main():
     bu, bv, bc, _ = gen.fast_batch(n, el.us, el.vs, el.caps, s, t, 10000, "mixed", 0)
     rr = mfx.solve_dynamic(r.state, g, mfx.UpdateBatch(bu, bv, bc), p)
     report("dynamic", rr.state, g, rr)
+    rounds_view("dynamic", rr.state, g)
 
 
 if __name__ == "__main__":
