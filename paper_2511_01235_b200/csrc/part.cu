@@ -43,6 +43,7 @@ namespace mfx {
 
 constexpr int kMaxParts = 8;
 constexpr int kPartHeavy = 2048;  // rows above this are expanded / pushed by a whole CTA
+constexpr int kPartHuge = 65536;  // finalize: rows above this are walked by the whole grid
 constexpr int kPartBlock = 256;
 
 // per-part device counters (int32, written by every part)
@@ -104,6 +105,10 @@ struct PartObj {
   int *rev = nullptr;
   uint8_t *orig = nullptr;
   int *bases = nullptr;
+  int *heavy = nullptr;         // rows longer than kPartHeavy
+  int nheavy = 0;
+  int *huge = nullptr;          // rows longer than kPartHuge
+  int nhuge = 0;
   unsigned long long *stat = nullptr;
   long long *err = nullptr;
   int *slot_first = nullptr;
@@ -143,7 +148,7 @@ PartObj::~PartObj() {
       }
   for (int b = 0; b < B_NBUF; ++b)
     if (buf[b]) cudaFree(buf[b]);
-  for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)stat, (void *)err,
+  for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)heavy, (void *)huge, (void *)stat, (void *)err,
                   (void *)slot_first, (void *)bslot, (void *)bbuf})
     if (p) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
@@ -533,28 +538,32 @@ __global__ void part_repair_kernel(PeerTab T, int me, int e0, int e1, const int 
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int gwarps = (gridDim.x * blockDim.x) >> 5;
   unsigned long long reps = 0;
-  for (int bin = 0; bin < 2; ++bin) {
-    int e = bin ? e1 : e0;
-    for (int j = gwarp; j < e; j += gwarps) {
-      int u = T.R[me][bin][j];
-      int lo = T.off[me][u], hi = T.off[me][u + 1];
-      int hu = vol_ld(T.h[me] + u);
-      for (int i = lo + lane; i < hi; i += 32) {
-        if (vol_ld(T.cf[me] + i) <= 0) continue;
-        int v = T.adj[me][i];
-        int p = owner_of(T, v);
-        int vl = v - T.lo[p];
-        if (hu > vol_ld(T.h[p] + vl) + 1) {
-          int amt = atomicExch(T.cf[me] + i, 0);
-          if (amt > 0) {
-            sys_add(T.cf[p] + rev[i], amt);
-            sys_add(T.ex[me] + u, -(long long)amt);
-            sys_add(T.ex[p] + vl, (long long)amt);
-            ++reps;
-          }
-        }
+  auto slot = [&](int u, int hu, int i) {
+    if (vol_ld(T.cf[me] + i) <= 0) return;
+    int v = T.adj[me][i];
+    int p = owner_of(T, v);
+    int vl = v - T.lo[p];
+    if (hu > vol_ld(T.h[p] + vl) + 1) {
+      int amt = atomicExch(T.cf[me] + i, 0);
+      if (amt > 0) {
+        sys_add(T.cf[p] + rev[i], amt);
+        sys_add(T.ex[me] + u, -(long long)amt);
+        sys_add(T.ex[p] + vl, (long long)amt);
+        ++reps;
       }
     }
+  };
+  for (int j = gwarp; j < e0; j += gwarps) {  // warp per light row
+    int u = T.R[me][0][j];
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    int hu = vol_ld(T.h[me] + u);
+    for (int i = lo + lane; i < hi; i += 32) slot(u, hu, i);
+  }
+  for (int j = blockIdx.x; j < e1; j += gridDim.x) {  // CTA per heavy row
+    int u = T.R[me][1][j];
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    int hu = vol_ld(T.h[me] + u);
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) slot(u, hu, i);
   }
   reps = warp_sum(reps);
   if (lane == 0 && reps) atomicAdd(stat + PS_REPAIR, reps);
@@ -563,27 +572,53 @@ __global__ void part_repair_kernel(PeerTab T, int me, int e0, int e1, const int 
 // flow over the local bases (dynamic.py:141-143) and the local part of the cut
 // (solver.py:178-184): original slots from A = {h == n} into B
 __global__ void part_final_kernel(PeerTab T, int me, int nl, int nb, const int *bases,
-                                  const uint8_t *orig, unsigned long long *stat) {
+                                  const uint8_t *orig, const int *heavy, int nheavy,
+                                  const int *huge, int nhuge, unsigned long long *stat) {
   const int n = T.n, lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int gwarps = (gridDim.x * blockDim.x) >> 5;
   long long f = 0, c = 0;
   PGS_LOOP(j, nb) f += vol_ld(T.ex[me] + bases[j]);
-  for (int u = gwarp; u < nl; u += gwarps) {
+  auto slot = [&](int i) {
+    if (!orig[i]) return;
+    int v = T.adj[me][i];
+    int p = owner_of(T, v);
+    if (vol_ld(T.h[p] + (v - T.lo[p])) != n) c += T.cap0[me][i];
+  };
+  for (int u = gwarp; u < nl; u += gwarps) {  // warp per light A-side row
     if (vol_ld(T.h[me] + u) != n) continue;
     int lo = T.off[me][u], hi = T.off[me][u + 1];
-    for (int i = lo + lane; i < hi; i += 32) {
-      if (!orig[i]) continue;
-      int v = T.adj[me][i];
-      int p = owner_of(T, v);
-      if (vol_ld(T.h[p] + (v - T.lo[p])) != n) c += T.cap0[me][i];
-    }
+    if (hi - lo > kPartHeavy) continue;
+    for (int i = lo + lane; i < hi; i += 32) slot(i);
+  }
+  for (int j = blockIdx.x; j < nheavy; j += gridDim.x) {  // CTA per heavy A-side row
+    int u = heavy[j];
+    if (vol_ld(T.h[me] + u) != n) continue;
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    if (hi - lo > kPartHuge) continue;
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) slot(i);
+  }
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  for (int j = 0; j < nhuge; ++j) {  // whole grid per huge A-side row (hubs)
+    int u = huge[j];
+    if (vol_ld(T.h[me] + u) != n) continue;
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    for (int i = lo + gtid; i < hi; i += gthreads) slot(i);
   }
   f = warp_sum(f);
   c = warp_sum(c);
   if (lane == 0) {
     if (f) atomicAdd(stat + PS_FLOW, (unsigned long long)f);
     if (c) atomicAdd(stat + PS_CUT, (unsigned long long)c);
+  }
+}
+
+__global__ void part_heavy_list_kernel(const int *off, int nl, int *list, int *cnt, int *huge,
+                                       int *hcnt) {
+  PGS_LOOP(u, nl) {
+    int d = off[u + 1] - off[u];
+    if (d > kPartHeavy) list[atomicAdd(cnt, 1)] = (int)u;
+    if (d > kPartHuge) huge[atomicAdd(hcnt, 1)] = (int)u;
   }
 }
 
@@ -884,6 +919,8 @@ static int part_build(PartObj &o, long long m, const int64_t *d_us, const int64_
   PCK(cudaMalloc(&o.rev, sizeof(int) * SS));
   PCK(cudaMalloc(&o.orig, SS));
   PCK(cudaMalloc(&o.bases, sizeof(int) * NL));
+  PCK(cudaMalloc(&o.heavy, sizeof(int) * NL));
+  PCK(cudaMalloc(&o.huge, sizeof(int) * NL));
   PCK(cudaMalloc(&o.stat, sizeof(unsigned long long) * PS_N));
   PCK(cudaMalloc(&o.err, sizeof(long long) * PE_N));
   PCK(cudaMalloc(&o.slot_first, sizeof(int) * SS));
@@ -967,6 +1004,25 @@ int mfx_part_create(int64_t n, int nparts, int rank, const int64_t *bounds, int6
   if (rc) {
     delete P;
     return rc;
+  }
+  {  // rows long enough for whole-grid treatment in repair / finalize
+    int *cnt = nullptr;
+    cudaError_t e2 = cudaMalloc(&cnt, 2 * sizeof(int));
+    if (!e2) e2 = cudaMemsetAsync(cnt, 0, 2 * sizeof(int), o.stream);
+    if (!e2 && o.nl > 0)
+      part_heavy_list_kernel<<<pgrid(o.nl, o.num_sms), kPartBlock, 0, o.stream>>>(
+          (const int *)o.buf[B_OFF], o.nl, o.heavy, cnt, o.huge, cnt + 1);
+    int hc[2] = {0, 0};
+    if (!e2) e2 = cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, o.stream);
+    if (!e2) e2 = cudaStreamSynchronize(o.stream);
+    o.nheavy = hc[0];
+    o.nhuge = hc[1];
+    if (cnt) cudaFree(cnt);
+    count_launch();
+    if (e2) {
+      delete P;
+      PCK(e2);
+    }
   }
   tab_set_self(o, rank);
   *out = P;
@@ -1171,7 +1227,8 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
     }
     case MFX_PH_FINAL: {  // args: #bases -> out[0] flow partial, out[1] cut partial
       PCK(cudaMemsetAsync(o.stat + PS_FLOW, 0, 2 * sizeof(unsigned long long), st));
-      part_final_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.nl, (int)args[0], o.bases, o.orig, o.stat);
+      part_final_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.nl, (int)args[0], o.bases, o.orig,
+                                                  o.heavy, o.nheavy, o.huge, o.nhuge, o.stat);
       count_launch();
       break;
     }
