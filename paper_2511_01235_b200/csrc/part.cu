@@ -109,6 +109,10 @@ struct PartObj {
   int nheavy = 0;
   int *huge = nullptr;          // rows longer than kPartHuge
   int nhuge = 0;
+  // hub push scratch (capacity nhuge)
+  int *hub_list = nullptr, *hub_cnt = nullptr;
+  unsigned long long *hub_best = nullptr;
+  long long *hub_taken = nullptr, *hub_snap = nullptr;
   unsigned long long *stat = nullptr;
   long long *err = nullptr;
   int *slot_first = nullptr;
@@ -148,7 +152,8 @@ PartObj::~PartObj() {
       }
   for (int b = 0; b < B_NBUF; ++b)
     if (buf[b]) cudaFree(buf[b]);
-  for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)heavy, (void *)huge, (void *)stat, (void *)err,
+  for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)heavy, (void *)huge, (void *)hub_list, (void *)hub_cnt,
+                  (void *)hub_best, (void *)hub_taken, (void *)hub_snap, (void *)stat, (void *)err,
                   (void *)slot_first, (void *)bslot, (void *)bbuf})
     if (p) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
@@ -516,18 +521,119 @@ __device__ void part_push_row(const PeerTab &T, int me, int u, int kc, unsigned 
 
 __global__ void part_push_kernel(PeerTab T, int me, int b0, int e0, int b1, int e1, int kc,
                                  unsigned stamp, int s, int t, int rcap, const int *rev,
-                                 unsigned long long *stat) {
+                                 unsigned long long *stat, int *hub_list, int *hub_cnt,
+                                 unsigned long long *hub_best, long long *hub_taken) {
   __shared__ long long s_red[kPartBlock / 32 + 2];
   unsigned long long loc[PS_N] = {};
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int gwarps = (gridDim.x * blockDim.x) >> 5;
   for (int j = b0 + gwarp; j < e0; j += gwarps)
     part_push_row<32>(T, me, T.R[me][0][j], kc, stamp, s, t, rcap, rev, loc, s_red);
-  for (int j = b1 + blockIdx.x; j < e1; j += gridDim.x)
-    part_push_row<kPartBlock>(T, me, T.R[me][1][j], kc, stamp, s, t, rcap, rev, loc, s_red);
+  for (int j = b1 + blockIdx.x; j < e1; j += gridDim.x) {
+    const int u = T.R[me][1][j];
+    if (T.off[me][u + 1] - T.off[me][u] > kPartHuge) {  // hub: whole grid, next kernels
+      if (threadIdx.x == 0) {
+        const int q = atomicAdd(hub_cnt, 1);
+        hub_list[q] = u;
+        hub_best[q] = ~0ull;
+        hub_taken[q] = 0;
+      }
+      continue;
+    }
+    part_push_row<kPartBlock>(T, me, u, kc, stamp, s, t, rcap, rev, loc, s_red);
+  }
   for (int k = 0; k < 4; ++k) {
     unsigned long long x = warp_sum(loc[k]);
     if ((threadIdx.x & 31) == 0 && x) atomicAdd(stat + k, x);
+  }
+}
+
+// One push-or-relabel step for hub rows (> kPartHuge slots) with the whole
+// grid: (1) first-minimum (height, slot) over the residual slots by a 64-bit
+// atomicMin, with u's height and excess snapshotted once; (2) relabel from
+// the scan, or push along every slot at the minimum height, each slot
+// claiming its share of the snapshot excess through an atomic ticket.
+__global__ void part_hub_scan_kernel(PeerTab T, int me, const int *hub_list, const int *hub_cnt,
+                                     unsigned long long *hub_best, long long *hub_snap) {
+  const int nh = *hub_cnt;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  for (int j = 0; j < nh; ++j) {
+    const int u = hub_list[j];
+    const int lo = T.off[me][u], hi = T.off[me][u + 1];
+    if (gtid == 0) {
+      hub_snap[2 * j] = vol_ld(T.h[me] + u);
+      hub_snap[2 * j + 1] = vol_ld(T.ex[me] + u);
+    }
+    unsigned long long best = ~0ull;
+    for (int i = lo + gtid; i < hi; i += gthreads) {
+      if (vol_ld(T.cf[me] + i) > 0) {
+        const int v = T.adj[me][i];
+        const int p = owner_of(T, v);
+        const unsigned hv = (unsigned)vol_ld(T.h[p] + (v - T.lo[p]));
+        const unsigned long long key = ((unsigned long long)hv << 32) | (unsigned)(i - lo);
+        best = key < best ? key : best;
+      }
+    }
+    best = warp_min_u64(best);
+    if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(hub_best + j, best);
+  }
+}
+
+__global__ void part_hub_push_kernel(PeerTab T, int me, const int *hub_list, const int *hub_cnt,
+                                     const unsigned long long *hub_best, const long long *hub_snap,
+                                     long long *hub_taken, unsigned stamp, int s, int t, int rcap,
+                                     const int *rev, unsigned long long *stat) {
+  const int n = T.n, nh = *hub_cnt;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  unsigned long long pushes = 0;
+  for (int j = 0; j < nh; ++j) {
+    const int u = hub_list[j];
+    const int hu = (int)hub_snap[2 * j];
+    const long long eu = hub_snap[2 * j + 1];
+    const unsigned long long best = hub_best[j];
+    if (eu <= 0 || hu >= n) continue;
+    if (best == ~0ull || hu <= (int)(best >> 32)) {  // relabel (kernels.py:49-53, 62-66)
+      if (gtid == 0) {
+        const int nh2 = best == ~0ull ? n : ((int)(best >> 32) + 1 > n ? n : (int)(best >> 32) + 1);
+        T.h[me][u] = nh2;
+        atomicAdd(stat + PS_RELABEL, 1ull);
+        if (nh2 < n) part_activate(T, T.lo[me] + u, stamp, s, t, rcap);
+      }
+      continue;
+    }
+    const int bh = (int)(best >> 32);
+    const int lo = T.off[me][u], hi = T.off[me][u + 1];
+    for (int i = lo + gtid; i < hi; i += gthreads) {
+      const long long c = vol_ld(T.cf[me] + i);
+      if (c <= 0) continue;
+      const int v = T.adj[me][i];
+      const int p = owner_of(T, v);
+      if (vol_ld(T.h[p] + (v - T.lo[p])) != bh) continue;
+      const long long before = atomicAdd((unsigned long long *)(hub_taken + j),
+                                         (unsigned long long)c);
+      long long amt = eu - before;
+      amt = amt < 0 ? 0 : (amt < c ? amt : c);
+      if (amt <= 0) continue;
+      atomicAdd(T.cf[me] + i, (int)-amt);
+      sys_add(T.cf[p] + rev[i], (int)amt);
+      const long long old = sys_add(T.ex[p] + (v - T.lo[p]), amt);
+      sys_add(T.ex[me] + u, -amt);
+      ++pushes;
+      if (old <= 0) part_activate(T, v, stamp, s, t, rcap);
+    }
+  }
+  pushes = warp_sum(pushes);
+  if ((threadIdx.x & 31) == 0 && pushes) atomicAdd(stat + PS_PUSH, pushes);
+}
+
+// still overflowing after its step: the hub joins the next wave
+__global__ void part_hub_tail_kernel(PeerTab T, int me, const int *hub_list, const int *hub_cnt,
+                                     unsigned stamp, int s, int t, int rcap) {
+  const int nh = *hub_cnt;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
+    const int u = hub_list[j];
+    if (vol_ld(T.h[me] + u) < T.n && vol_ld(T.ex[me] + u) > 0)
+      part_activate(T, T.lo[me] + u, stamp, s, t, rcap);
   }
 }
 
@@ -1018,6 +1124,12 @@ int mfx_part_create(int64_t n, int nparts, int rank, const int64_t *bounds, int6
     o.nheavy = hc[0];
     o.nhuge = hc[1];
     if (cnt) cudaFree(cnt);
+    const size_t H = (size_t)(o.nhuge > 0 ? o.nhuge : 1);
+    if (!e2) e2 = cudaMalloc(&o.hub_list, sizeof(int) * H);
+    if (!e2) e2 = cudaMalloc(&o.hub_cnt, sizeof(int));
+    if (!e2) e2 = cudaMalloc(&o.hub_best, sizeof(unsigned long long) * H);
+    if (!e2) e2 = cudaMalloc(&o.hub_taken, sizeof(long long) * H);
+    if (!e2) e2 = cudaMalloc(&o.hub_snap, sizeof(long long) * 2 * H);
     count_launch();
     if (e2) {
       delete P;
@@ -1210,10 +1322,19 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
       int b0 = (int)args[0], e0 = (int)std::min<int64_t>(args[1], o.rcap);
       int b1 = (int)args[2], e1 = (int)std::min<int64_t>(args[3], o.rcap);
       if (e0 > b0 || e1 > b1) {
+        PCK(cudaMemsetAsync(o.hub_cnt, 0, sizeof(int), st));
         part_push_kernel<<<G, kPartBlock, 0, st>>>(T, me, b0, e0, b1, e1, (int)args[4],
                                                    (unsigned)args[5], o.s, o.t, o.rcap, o.rev,
-                                                   o.stat);
-        count_launch();
+                                                   o.stat, o.hub_list, o.hub_cnt, o.hub_best,
+                                                   o.hub_taken);
+        part_hub_scan_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.hub_list, o.hub_cnt, o.hub_best,
+                                                       o.hub_snap);
+        part_hub_push_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.hub_list, o.hub_cnt, o.hub_best,
+                                                       o.hub_snap, o.hub_taken, (unsigned)args[5],
+                                                       o.s, o.t, o.rcap, o.rev, o.stat);
+        part_hub_tail_kernel<<<o.num_sms, kPartBlock, 0, st>>>(T, me, o.hub_list, o.hub_cnt,
+                                                               (unsigned)args[5], o.s, o.t, o.rcap);
+        count_launch(4);
       }
       break;
     }
