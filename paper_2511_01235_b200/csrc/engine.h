@@ -94,6 +94,7 @@ struct SolveConfig {
   int lq_cap = kLQ;       // CTA-local queue capacity per sub-level
   int tail_items = 0;     // push: extra waves past the budget while a wave holds <= tail_items
   int tail_cap = 0;       //   ... up to tail_cap waves per round
+  int coop_kc = 0;        // steps per visit of a long row (0: kc); each step rescans the row
   int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;

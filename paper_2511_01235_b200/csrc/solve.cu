@@ -60,6 +60,7 @@ struct SolveArgs {
   int lq_cap;        // CTA-local queue capacity per sub-level (<= kLQ; the rest spills)
   int tail_items;    // push: after the wave budget, continue while a wave holds <= this many
   int tail_cap;      //   ... up to this many waves in the round
+  int coop_kc;       // push/relabel steps per visit of a cooperative (long) row
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -913,7 +914,7 @@ struct Kern {
     if (pull) eu = -eu;
     bool any_push = false;
     long long last_old = 0, last_total = 0;
-    for (int cnt = 0; cnt < a.kc; ++cnt) {
+    for (int cnt = 0; cnt < a.coop_kc; ++cnt) {  // (each step rescans the row)
       if (eu <= 0 || hu >= n) break;
       // ---- pass 1: (height, slot) argmin over residual slots, 4-way ILP
       unsigned long long best = ~0ull;
@@ -1620,6 +1621,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.bfs_local_max = cfg.bfs_local_max;
   a.lq_cap = cfg.lq_cap < 1 ? 1 : cfg.lq_cap > kLQ ? kLQ : cfg.lq_cap;
   a.tail_items = cfg.tail_items;
+  a.coop_kc = cfg.coop_kc > 0 ? (cfg.coop_kc < cfg.kc ? cfg.coop_kc : cfg.kc) : cfg.kc;
   a.tail_cap = cfg.tail_cap;
   a.bmark = W.bmark;
   a.topology = cfg.topology;
