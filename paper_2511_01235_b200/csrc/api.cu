@@ -648,6 +648,8 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   if (const char *ti = getenv("MFX_TAIL_ITEMS")) cfg.tail_items = atoi(ti);
   if (const char *tc = getenv("MFX_TAIL_CAP")) cfg.tail_cap = atoi(tc);
   if (const char *ck = getenv("MFX_COOP_KC")) cfg.coop_kc = atoi(ck);
+  if (const char *wm = getenv("MFX_WALK_MAX")) cfg.walk_max = atoi(wm);  // (< 0: off)
+  if (const char *wd = getenv("MFX_WALK_DEPTH")) cfg.walk_depth = atoi(wd);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;
@@ -832,6 +834,10 @@ static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const in
   cfg.dyn_bases = 1;
   cfg.forbidden = st->s.s;
   cfg.gate = T.ws.d_err;
+  // after an update batch a handful of vertices far down long-diameter
+  // graphs carry the excess: walk it to the bases (road 1024^2: 57 -> 35 ms)
+  if (cfg.walk_max == 0) cfg.walk_max = 4096;
+  if (cfg.walk_depth == 0) cfg.walk_depth = 1024;
   CK(launch_solve(g->g, st->s, cfg, &launches));
   CK(cudaEventRecord(T.ev[2], T.stream));
   CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));

@@ -116,6 +116,12 @@ __device__ __forceinline__ long long atomic_exch(long long *p, long long v) {
   return (long long)atomicExch((unsigned long long *)p, (unsigned long long)v);
 }
 
+__device__ __forceinline__ int atomic_cas(int *p, int cmp, int v) { return atomicCAS(p, cmp, v); }
+__device__ __forceinline__ long long atomic_cas(long long *p, long long cmp, long long v) {
+  return (long long)atomicCAS((unsigned long long *)p, (unsigned long long)cmp,
+                              (unsigned long long)v);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

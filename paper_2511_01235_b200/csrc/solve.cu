@@ -61,6 +61,8 @@ struct SolveArgs {
   int tail_items;    // push: after the wave budget, continue while a wave holds <= this many
   int tail_cap;      //   ... up to this many waves in the round
   int coop_kc;       // push/relabel steps per visit of a cooperative (long) row
+  int walk_max;      // excess walk after a global relabel with <= this many active vertices
+  int walk_depth;    // ... at least this many BFS levels deep
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -472,7 +474,8 @@ struct Kern {
     const int ru = valid ? region(u) : 0;
     const bool act = first && u != a.s && u != a.t && (ru == 1 ? eu < 0 : eu > 0);
     act_cnt += act;
-    if (act && a.async) a.mark[u] = ep_next;  // queued for the push phase = owned
+    // queued for the push phase: owned (async) / listed for wave 0 (walk dedupe)
+    if (act && (a.async || a.walk_max > 0)) a.mark[u] = ep_next;
     append_binned(1, act && !a.topology, u, bin_of(d), a.ctrl->live + C_RNEXT, a.R, rb_, a.rcap);
     const bool heavy = valid && d > kBin0Max;
     if (__any_sync(FULL, heavy)) {
@@ -1136,6 +1139,76 @@ struct Kern {
     }
   }
 
+  // =========================================================================
+  // excess walk (thin active sets): right after an exact global relabel,
+  // carry each active vertex's excess down the BFS layers (h(v) == h(u) - 1)
+  // to a base in one pass -- a waves-only round moves excess one hop per
+  // grid barrier, so a few far-away active vertices would need several
+  // rounds (a full global relabel each) for a ~100-hop path.  Each step
+  // claims min(carry, cf) by CAS, so concurrent walkers never overdraw a
+  // slot; pushes go downhill along exact labels (no relabel, the labeling
+  // stays valid).  A walker stops at a base, at a long row (left to the
+  // waves) or where the slots below were taken; what it leaves behind is
+  // ordinary excess for the waves and the next global relabel.
+  // =========================================================================
+  // s0: the stamp that marks wave 0 of this round (the BFS set it on every
+  // listed active vertex); a walker that stops short lists its stopping
+  // vertex for wave 0 too, once.
+  __device__ void walk(int cnt0, unsigned s0) {
+    for (int j = gtid; j < cnt0; j += gthreads) {
+      int u = ldcg(a.R[0] + j);
+      if (u < 0) continue;
+      int hu = ldcg(a.h + u);
+      long long carry = ldcg(a.ex + u);
+      int d = 0;
+      bool moved = false;
+      for (int step = 0; step < a.n && hu > 0 && hu < a.n && carry > 0; ++step) {
+        const int lo = __ldg(a.off + u);
+        d = __ldg(a.off + u + 1) - lo;
+        if (d > kBin0Max) break;
+        int pick = -1, v = 0;
+        CapT c = 0;
+        for (int k = 0; k < d && pick < 0; ++k) {
+          CapT ck = (CapT)ldcg((const CapT *)(a.cf + lo + k));
+          if (ck > 0) {
+            int w = __ldg(a.adj + lo + k);
+            if (ldcg(a.h + w) == hu - 1) {
+              pick = lo + k;
+              v = w;
+              c = ck;
+            }
+          }
+        }
+        if (pick < 0) break;
+        long long take = 0;
+        for (CapT cur = c;;) {  // claim
+          take = carry < (long long)cur ? carry : (long long)cur;
+          if (take <= 0) break;
+          CapT prev = atomic_cas(a.cf + pick, cur, (CapT)(cur - (CapT)take));
+          if (prev == cur) break;
+          cur = prev;
+        }
+        if (take <= 0) break;
+        atomic_add(a.cf + __ldg(a.rev + pick), (CapT)take);
+        atomic_add(a.ex + u, -take);
+        add_excess(v, take);
+        lc.pushes++;
+        lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kSlot +
+                    Bytes<CapT>::kPush;
+        carry = take;
+        u = v;
+        hu -= 1;
+        moved = true;
+      }
+      if (moved && hu > 0 && hu < a.n && u != a.t && atomicMax(a.mark + u, s0) < s0) {
+        const int b = bin_of(d > 0 ? d : __ldg(a.off + u + 1) - __ldg(a.off + u));
+        const int p = sy.s_snap[C_RNEXT + b] + atomicAdd(a.ctrl->live + C_RNEXT + b, 1);
+        if (p < a.rcap) a.R[b][p] = u;
+        else a.ctrl->overflow = 1;
+      }
+    }
+  }
+
   // one round's push phase + repair; wave 0 = the active list in R
   __device__ void push_round(unsigned &stamp, unsigned long long *scr, int max_waves) {
     __shared__ int nbase[NBIN];
@@ -1480,7 +1553,17 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
                   a.what == WHAT_SOLVE && !a.topology && !PP && (a.flags & 4) != 0);
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
+        // with the walk enabled the BFS stamped the listed active vertices
+        // with stamp + 1 (wave 0); this round's wave stamps start above it
+        const bool marked = !PP && !a.async && a.walk_max > 0;
+        if (marked) ++stamp;
         if (act == 0 || s_abort || !do_push) break;
+        if (marked && !a.topology && act <= a.walk_max && L >= a.walk_depth) {
+          k.walk(s_snap[C_RNEXT], stamp);
+          k.sink_flush();
+          // stopping vertices join wave 0 (accumulate the list counters)
+          grid_sync(a.ctrl, sy, 0, 0xFu << C_RNEXT, 0, PH_PUSH);
+        }
       }
       if (a.async) k.push_round_async(stamp, scr);
       else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
@@ -1621,6 +1704,8 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.bfs_local_max = cfg.bfs_local_max;
   a.lq_cap = cfg.lq_cap < 1 ? 1 : cfg.lq_cap > kLQ ? kLQ : cfg.lq_cap;
   a.tail_items = cfg.tail_items;
+  a.walk_max = cfg.walk_max;
+  a.walk_depth = cfg.walk_depth;
   a.coop_kc = cfg.coop_kc > 0 ? (cfg.coop_kc < cfg.kc ? cfg.coop_kc : cfg.kc) : cfg.kc;
   a.tail_cap = cfg.tail_cap;
   a.bmark = W.bmark;
