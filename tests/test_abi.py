@@ -82,3 +82,17 @@ def test_solve_kernel_state_stays_in_registers():
             calls = len(re.findall(r"\bCALL\b", sass))
             assert local < budget, (fn, local)
             assert calls <= 16, (fn, calls)  # the grid barrier is the only out-of-line routine
+
+
+def test_integration_stub_structs_match_the_abi():
+    """The reference-side ctypes stub in INTEGRATION.md declares the same
+    mfx_params / mfx_result layouts as the package binding."""
+    import ctypes
+    from paper_2511_01235_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = text[text.index("class _Params"):text.index("_ERR = {")]
+    ns = {"ctypes": ctypes}
+    exec(code, ns)
+    for stub, ours in ((ns["_Params"], _lib.Params), (ns["_Result"], _lib.Result)):
+        assert [(n, t) for n, t in stub._fields_] == [(n, t) for n, t in ours._fields_]
+        assert ctypes.sizeof(stub) == ctypes.sizeof(ours)
