@@ -386,7 +386,7 @@ static void push_rounds(int64_t n, const int64_t *offsets, const int64_t *adj,
                         int64_t *height, int64_t s, int64_t t, int64_t kc,
                         int dynamic, int topology, orc_result *r)
 {
-    int64_t *bases = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    int64_t *bases = (int64_t *)calloc((size_t)(n + 1), sizeof(int64_t));
     int64_t *work = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
     int64_t counts[2] = {0, 0};
     for (;;) {
