@@ -83,6 +83,8 @@ def rounds_view(tag, st, g):
         waves = work[j:k]
         push_us = dt[j:k].sum() / 1e3
         rep = dt[k:k + 1].sum() / 1e3 if k < len(ph) and ph[k] == 2 else 0.0
+        ep = " ".join(f"{int(work[q])}:{dt[q] / 1e3:.0f}" for q in range(i, j))
+        print(f"    bfs epochs (items:us) {ep}")
         print(f"  round {rnd}: bfs {j - i} epochs {bfs_us:8.1f} us | {k - j} waves {push_us:8.1f} us "
               f"items first/max/last {waves[:1].tolist()}/{int(waves.max()) if len(waves) else 0}/"
               f"{waves[-1:].tolist()} | repair {rep:6.1f} us")
