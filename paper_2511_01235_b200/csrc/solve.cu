@@ -280,9 +280,12 @@ struct Kern {
   }
   __device__ __forceinline__ void sink_flush() {  // whole CTA, before a grid barrier
     __syncthreads();
-    if (threadIdx.x == 0 && *s_sink) {
-      atomic_add(a.ex + a.t, *s_sink);
-      *s_sink = 0;
+    if (threadIdx.x == 0) {  // (only thread 0 touches s_sink here)
+      const long long x = *s_sink;
+      if (x) {
+        atomic_add(a.ex + a.t, x);
+        *s_sink = 0;
+      }
     }
   }
 
