@@ -97,6 +97,7 @@ struct SolveConfig {
   int coop_kc = 0;        // steps per visit of a long row (0: kc); each step rescans the row
   int walk_max = 0;       // excess walk when a global relabel finds <= walk_max active vertices
   int walk_depth = 0;     // ... and the BFS is at least walk_depth levels deep
+  int max_ctas = 0;       // cap on the persistent grid (0: every SM at full occupancy)
   int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;
