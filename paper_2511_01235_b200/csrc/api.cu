@@ -651,6 +651,7 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   if (const char *wm = getenv("MFX_WALK_MAX")) cfg.walk_max = atoi(wm);  // (< 0: off)
   if (const char *wd = getenv("MFX_WALK_DEPTH")) cfg.walk_depth = atoi(wd);
   if (const char *mc = getenv("MFX_MAX_CTAS")) cfg.max_ctas = atoi(mc);
+  if (const char *tl = getenv("MFX_TAIL_LOCAL")) cfg.tail_local = atoi(tl);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;

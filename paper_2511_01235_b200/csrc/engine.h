@@ -98,6 +98,7 @@ struct SolveConfig {
   int walk_max = 0;       // excess walk when a global relabel finds <= walk_max active vertices
   int walk_depth = 0;     // ... and the BFS is at least walk_depth levels deep
   int max_ctas = 0;       // cap on the persistent grid (0: every SM at full occupancy)
+  int tail_local = 256;   // push waves of <= tail_local short-row items run in CTA 0 alone
   int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;

@@ -86,6 +86,10 @@ struct Ctrl {
   int aq_pad;
   unsigned long long async_items;  // items processed by asynchronous push phases
   unsigned long long epochs;       // grid barriers spent in global relabels
+  // push waves run by CTA 0 alone (thin waves): state for the other CTAs
+  int tail_base[NBIN];
+  int tail_waves;
+  unsigned tail_stamp;
 };
 
 // ---- small device helpers -------------------------------------------------

@@ -63,6 +63,7 @@ struct SolveArgs {
   int coop_kc;       // push/relabel steps per visit of a cooperative (long) row
   int walk_max;      // excess walk after a global relabel with <= this many active vertices
   int walk_depth;    // ... at least this many BFS levels deep
+  int tail_local;    // push waves of <= this many items run in CTA 0 alone (0: off)
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -1212,6 +1213,66 @@ struct Kern {
     }
   }
 
+  // Thin waves (<= tail_local items, no CTA-wide rows) run in CTA 0 alone,
+  // wave after wave with __syncthreads between them instead of a grid
+  // barrier, while the rest of the grid waits at the next barrier.  A single
+  // CTA processing a wave is one schedule of it; the wave stamps keep every
+  // vertex in at most one wave at a time exactly as in grid mode.  Leaves
+  // the pending wave's counts in the live counters (snapshotted by the
+  // barrier) and publishes base / waves / stamp for the other CTAs.
+  __device__ void tail_waves(int *base, int *cnt, int &waves, unsigned &stamp, int max_waves,
+                             int *nbase, long long *s_red) {
+    __shared__ int s_cnt[NBIN];
+    __shared__ int s_go;
+    for (;;) {
+      const unsigned next = ++stamp;
+      __syncthreads();
+      if (threadIdx.x < NBIN) nbase[threadIdx.x] = base[threadIdx.x] + cnt[threadIdx.x];
+      __syncthreads();
+      int lim[NBIN];
+      for (int b = 0; b < NBIN; ++b) {
+        lim[b] = base[b] + cnt[b];
+        if (lim[b] > a.rcap) lim[b] = a.rcap;
+      }
+      for (int j0 = base[0] + wib * 32; j0 < lim[0]; j0 += kWarps * 32) {
+        const int j = j0 + lane;
+        const bool valid = j < lim[0];
+        push_thread<false>(valid, valid ? ldcg(a.R[0] + j) : 0, next, nbase);
+      }
+      for (int j = base[1] + wib; j < lim[1]; j += kWarps)
+        push_coop<32, false>(ldcg(a.R[1] + j), next, nbase, s_red);
+      stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
+      __threadfence();  // this wave's list appends before the counts are read
+      __syncthreads();
+      ++waves;
+      if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int b = 0; b < NBIN; ++b) {
+          s_cnt[b] = ldcg(a.ctrl->live + C_RNEXT + b);
+          tot += s_cnt[b];
+        }
+        const bool go = tot > 0 && tot <= a.tail_local && s_cnt[1] <= kWarps && s_cnt[2] == 0 &&
+                        s_cnt[3] == 0 && waves < max_waves;
+        if (go) {  // consumed here: the next wave appends from zero
+          for (int b = 0; b < NBIN; ++b) a.ctrl->live[C_RNEXT + b] = 0;
+          __threadfence();
+        }
+        s_go = go;
+      }
+      __syncthreads();
+      for (int b = 0; b < NBIN; ++b) {
+        base[b] += cnt[b];
+        cnt[b] = s_cnt[b];
+      }
+      if (!s_go) break;
+    }
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < NBIN; ++b) a.ctrl->tail_base[b] = base[b];
+      a.ctrl->tail_waves = waves;
+      a.ctrl->tail_stamp = stamp;
+    }
+  }
+
   // one round's push phase + repair; wave 0 = the active list in R
   __device__ void push_round(unsigned &stamp, unsigned long long *scr, int max_waves) {
     __shared__ int nbase[NBIN];
@@ -1223,6 +1284,23 @@ struct Kern {
     }
     int waves = 0;
     for (;;) {
+      // (only short rows: a warp-wide row in CTA 0 alone would idle the grid)
+      if (a.tail_local > 0 && cnt[0] + cnt[1] <= a.tail_local && cnt[1] <= kWarps &&
+          cnt[2] == 0 && cnt[3] == 0 && cnt[0] + cnt[1] > 0) {
+        if (blockIdx.x == 0) tail_waves(base, cnt, waves, stamp, max_waves, nbase, s_red);
+        grid_sync(a.ctrl, sy, 0xFu << C_RNEXT, 0, 0, PH_PUSH);
+        int tot = 0;
+        for (int b = 0; b < NBIN; ++b) {  // adopt CTA 0's wave state
+          base[b] = ldcg(a.ctrl->tail_base + b);
+          cnt[b] = sy.s_snap[C_RNEXT + b];
+          tot += cnt[b];
+        }
+        waves = ldcg(&a.ctrl->tail_waves);
+        stamp = (unsigned)ldcg((const int *)&a.ctrl->tail_stamp);
+        if (tot == 0 || *sy.s_abort) break;
+        if (waves >= max_waves && (tot > a.tail_items || waves >= a.tail_cap)) break;
+        continue;
+      }
       unsigned next = ++stamp;
       __syncthreads();
       if (threadIdx.x < NBIN) nbase[threadIdx.x] = base[threadIdx.x] + cnt[threadIdx.x];
@@ -1709,6 +1787,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.tail_items = cfg.tail_items;
   a.walk_max = cfg.walk_max;
   a.walk_depth = cfg.walk_depth;
+  a.tail_local = cfg.tail_local;
   a.coop_kc = cfg.coop_kc > 0 ? (cfg.coop_kc < cfg.kc ? cfg.coop_kc : cfg.kc) : cfg.kc;
   a.tail_cap = cfg.tail_cap;
   a.bmark = W.bmark;
