@@ -359,7 +359,8 @@ __device__ __forceinline__ void part_discover(const PeerTab &T, int me, int i, i
 }
 
 __global__ void part_bfs_expand_kernel(PeerTab T, int me, int L, int cur, int cnt0, int cnt1,
-                                       int s, int t, int forbidden, int rcap) {
+                                       int s, int t, int forbidden, int rcap, const int *huge,
+                                       int nhuge) {
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int gwarps = (gridDim.x * blockDim.x) >> 5;
@@ -372,8 +373,18 @@ __global__ void part_bfs_expand_kernel(PeerTab T, int me, int L, int cur, int cn
   for (int j = blockIdx.x; j < cnt1; j += gridDim.x) {  // CTA per heavy row
     int u = F1[j];
     int lo = T.off[me][u], hi = T.off[me][u + 1];
+    if (hi - lo > kPartHuge) continue;  // hubs: below
     for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
       part_discover(T, me, i, L, cur, s, t, forbidden, rcap);
+  }
+  // hubs of this level (the frontier of a level-synchronous BFS is {h == L}):
+  // the whole grid per row
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  for (int j = 0; j < nhuge; ++j) {
+    const int u = huge[j];
+    if (vol_ld(T.h[me] + u) != L) continue;
+    const int lo = T.off[me][u], hi = T.off[me][u + 1];
+    for (int i = lo + gtid; i < hi; i += gthreads) part_discover(T, me, i, L, cur, s, t, forbidden, rcap);
   }
 }
 
@@ -1305,7 +1316,7 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
       if (args[2] + args[3] > 0) {
         part_bfs_expand_kernel<<<G, kPartBlock, 0, st>>>(T, me, (int)args[0], (int)args[1],
                                                          (int)args[2], (int)args[3], o.s, o.t,
-                                                         forbidden, o.rcap);
+                                                         forbidden, o.rcap, o.huge, o.nhuge);
         count_launch();
       }
       break;
