@@ -105,6 +105,7 @@ struct PartObj {
   int *rev = nullptr;
   uint8_t *orig = nullptr;
   int *bases = nullptr;
+  int *src = nullptr;           // local row of every slot (slot-parallel finalize)
   int *heavy = nullptr;         // rows longer than kPartHeavy
   int nheavy = 0;
   int *huge = nullptr;          // rows longer than kPartHuge
@@ -152,7 +153,7 @@ PartObj::~PartObj() {
       }
   for (int b = 0; b < B_NBUF; ++b)
     if (buf[b]) cudaFree(buf[b]);
-  for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)heavy, (void *)huge, (void *)hub_list, (void *)hub_cnt,
+  for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)src, (void *)heavy, (void *)huge, (void *)hub_list, (void *)hub_cnt,
                   (void *)hub_best, (void *)hub_taken, (void *)hub_snap, (void *)stat, (void *)err,
                   (void *)slot_first, (void *)bslot, (void *)bbuf})
     if (p) cudaFree(p);
@@ -688,39 +689,17 @@ __global__ void part_repair_kernel(PeerTab T, int me, int e0, int e1, const int 
 
 // flow over the local bases (dynamic.py:141-143) and the local part of the cut
 // (solver.py:178-184): original slots from A = {h == n} into B
-__global__ void part_final_kernel(PeerTab T, int me, int nl, int nb, const int *bases,
-                                  const uint8_t *orig, const int *heavy, int nheavy,
-                                  const int *huge, int nhuge, unsigned long long *stat) {
+__global__ void part_final_kernel(PeerTab T, int me, long long S, int nb, const int *bases,
+                                  const uint8_t *orig, const int *src,
+                                  unsigned long long *stat) {
   const int n = T.n, lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int gwarps = (gridDim.x * blockDim.x) >> 5;
   long long f = 0, c = 0;
   PGS_LOOP(j, nb) f += vol_ld(T.ex[me] + bases[j]);
-  auto slot = [&](int i) {
-    if (!orig[i]) return;
-    int v = T.adj[me][i];
-    int p = owner_of(T, v);
+  PGS_LOOP(i, S) {  // slot-parallel: original slots from A = {h == n} into B
+    if (!orig[i] || vol_ld(T.h[me] + src[i]) != n) continue;
+    const int v = T.adj[me][i];
+    const int p = owner_of(T, v);
     if (vol_ld(T.h[p] + (v - T.lo[p])) != n) c += T.cap0[me][i];
-  };
-  for (int u = gwarp; u < nl; u += gwarps) {  // warp per light A-side row
-    if (vol_ld(T.h[me] + u) != n) continue;
-    int lo = T.off[me][u], hi = T.off[me][u + 1];
-    if (hi - lo > kPartHeavy) continue;
-    for (int i = lo + lane; i < hi; i += 32) slot(i);
-  }
-  for (int j = blockIdx.x; j < nheavy; j += gridDim.x) {  // CTA per heavy A-side row
-    int u = heavy[j];
-    if (vol_ld(T.h[me] + u) != n) continue;
-    int lo = T.off[me][u], hi = T.off[me][u + 1];
-    if (hi - lo > kPartHuge) continue;
-    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) slot(i);
-  }
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
-  for (int j = 0; j < nhuge; ++j) {  // whole grid per huge A-side row (hubs)
-    int u = huge[j];
-    if (vol_ld(T.h[me] + u) != n) continue;
-    int lo = T.off[me][u], hi = T.off[me][u + 1];
-    for (int i = lo + gtid; i < hi; i += gthreads) slot(i);
   }
   f = warp_sum(f);
   c = warp_sum(c);
@@ -728,6 +707,13 @@ __global__ void part_final_kernel(PeerTab T, int me, int nl, int nb, const int *
     if (f) atomicAdd(stat + PS_FLOW, (unsigned long long)f);
     if (c) atomicAdd(stat + PS_CUT, (unsigned long long)c);
   }
+}
+
+__global__ void part_src_kernel(const int *off, int nl, int *src) {
+  const int lane = threadIdx.x & 31;
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nl;
+       u += (gridDim.x * blockDim.x) >> 5)
+    for (int i = off[u] + lane; i < off[u + 1]; i += 32) src[i] = u;
 }
 
 __global__ void part_heavy_list_kernel(const int *off, int nl, int *list, int *cnt, int *huge,
@@ -1037,6 +1023,7 @@ static int part_build(PartObj &o, long long m, const int64_t *d_us, const int64_
   PCK(cudaMalloc(&o.orig, SS));
   PCK(cudaMalloc(&o.bases, sizeof(int) * NL));
   PCK(cudaMalloc(&o.heavy, sizeof(int) * NL));
+  PCK(cudaMalloc(&o.src, sizeof(int) * SS));
   PCK(cudaMalloc(&o.huge, sizeof(int) * NL));
   PCK(cudaMalloc(&o.stat, sizeof(unsigned long long) * PS_N));
   PCK(cudaMalloc(&o.err, sizeof(long long) * PE_N));
@@ -1126,9 +1113,13 @@ int mfx_part_create(int64_t n, int nparts, int rank, const int64_t *bounds, int6
     int *cnt = nullptr;
     cudaError_t e2 = cudaMalloc(&cnt, 2 * sizeof(int));
     if (!e2) e2 = cudaMemsetAsync(cnt, 0, 2 * sizeof(int), o.stream);
-    if (!e2 && o.nl > 0)
+    if (!e2 && o.nl > 0) {
       part_heavy_list_kernel<<<pgrid(o.nl, o.num_sms), kPartBlock, 0, o.stream>>>(
           (const int *)o.buf[B_OFF], o.nl, o.heavy, cnt, o.huge, cnt + 1);
+      part_src_kernel<<<o.num_sms * 8, kPartBlock, 0, o.stream>>>((const int *)o.buf[B_OFF], o.nl,
+                                                                   o.src);
+      count_launch();
+    }
     int hc[2] = {0, 0};
     if (!e2) e2 = cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, o.stream);
     if (!e2) e2 = cudaStreamSynchronize(o.stream);
@@ -1359,8 +1350,8 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
     }
     case MFX_PH_FINAL: {  // args: #bases -> out[0] flow partial, out[1] cut partial
       PCK(cudaMemsetAsync(o.stat + PS_FLOW, 0, 2 * sizeof(unsigned long long), st));
-      part_final_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.nl, (int)args[0], o.bases, o.orig,
-                                                  o.heavy, o.nheavy, o.huge, o.nhuge, o.stat);
+      part_final_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.S, (int)args[0], o.bases, o.orig, o.src,
+                                                  o.stat);
       count_launch();
       break;
     }
