@@ -265,21 +265,28 @@ struct Kern {
   WarpQ *q;  // this warp's staging queues
   int gtid, gthreads, gwarp, gwarps, lane, wib;
   int act_cnt;  // active discoveries counted by this lane in the current level
-  long long *s_sink;  // per-CTA sum of excess pushed into the sink this phase
+  long long *s_sink;  // per-CTA sum of excess pushed into the sink this round
+  long long sink_acc; // this thread's share, not yet added to s_sink
 
   // Excess arriving at v.  The sink receives pushes from up to every pixel of
   // the grid config in the same wave; a global atomic on ex[t] per push
-  // serialises at one L2 slice, so the sink's share is summed in shared
-  // memory and published once per CTA per phase (sink_flush).  Returns the
-  // previous excess of v (for the sink: a positive dummy, it never activates).
+  // serialises at one L2 slice and even a shared-memory atomic per push
+  // serialises a CTA, so each thread sums the sink's share in a register and
+  // sink_flush publishes it once per round (nothing reads ex[t] before the
+  // round ends: t never pushes and the global relabel takes it as a base by
+  // identity).  Returns the previous excess of v (for the sink: a positive
+  // dummy, it never activates).
   __device__ __forceinline__ long long add_excess(int v, long long d) {
     if (v == a.t) {
-      atomicAdd((unsigned long long *)s_sink, (unsigned long long)d);
+      sink_acc += d;
       return 1;
     }
     return atomic_add(a.ex + v, d);
   }
   __device__ __forceinline__ void sink_flush() {  // whole CTA, before a grid barrier
+    const long long w = warp_sum(sink_acc);
+    sink_acc = 0;
+    if (lane == 0 && w) atomicAdd((unsigned long long *)s_sink, (unsigned long long)w);
     __syncthreads();
     if (threadIdx.x == 0) {  // (only thread 0 touches s_sink here)
       const long long x = *s_sink;
@@ -294,6 +301,7 @@ struct Kern {
       : a(a_), sy(sy_), lc(lc_), s_sink(sink) {
     gtid = blockIdx.x * blockDim.x + threadIdx.x;
     gthreads = gridDim.x * blockDim.x;
+    sink_acc = 0;
     lane = threadIdx.x & 31;
     wib = threadIdx.x >> 5;
     gwarp = gtid >> 5;
