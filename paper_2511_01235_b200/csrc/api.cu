@@ -709,6 +709,7 @@ int mfx_global_relabel(mfx_state *st, const mfx_graph *g, int dynamic_bases, int
   CK(cudaSetDevice(T.device));
   SolveConfig cfg;
   cfg.what = WHAT_BFS;
+  if (const char *fl = getenv("MFX_FLAGS")) cfg.flags = atoi(fl);  // (tests: forced retry)
   cfg.dyn_bases = dynamic_bases ? 1 : 0;
   cfg.forbidden = dynamic_bases ? st->s.s : -1;
   CK(launch_solve(g->g, st->s, cfg, nullptr));

@@ -596,9 +596,16 @@ struct Kern {
     __shared__ int s_lqc[2];
     __shared__ int s_hq[kHQ];
     __shared__ int s_hqc;
+    // A frontier list that overflowed (label-correcting duplicates beyond
+    // the per-epoch dedupe: not observed, but not excluded either) would
+    // leave the labels incomplete, so the relabel is then redone in strict
+    // level-synchronous mode, which lists every vertex at most once.
+    int E_all = 0;  // epochs over the attempts
+    for (int attempt = 0;; ++attempt) {
     ep_next = ep;
     disc_cnt = 0;
     max_lab = 0;
+    holders = 0;
     loc_ok = false;
     nocheck = (a.flags & 1) != 0;
     lqb = &s_lq[0][0];
@@ -755,10 +762,19 @@ struct Kern {
     }
     __syncthreads();
     if (threadIdx.x < 2) s_lqc[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_hqc = 0;
+    E_all += E;
+    // (read after the last barrier: uniform; flags bit 3 forces the retry, for tests)
+    const bool ovf = ldcg(&a.ctrl->overflow) != 0 || ((a.flags & 8) != 0 && attempt == 0);
+    if (!ovf || local_levels == 0 || *sy.s_abort || attempt > 0) break;
+    local_levels = 0;
+    early = false;
+    __syncthreads();
+    }
     const int depth = sy.s_snap[C_DEPTH] + 1;
     if (gtid == 0) {
       a.ctrl->levels += depth;
-      a.ctrl->epochs += E;
+      a.ctrl->epochs += E_all;
       a.ctrl->last_levels = depth;
       a.ctrl->reached = sy.s_snap[C_REACHED];
       for (int b = 0; b < NBIN; ++b) a.rdirty[b] = sy.s_snap[C_RNEXT + b];

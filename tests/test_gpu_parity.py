@@ -336,3 +336,21 @@ def test_edge_indices_and_reverse(mf):
         assert mf.reverse_edge(g, mf.reverse_edge(g, i)) == i
     with pytest.raises(mf.GraphError):
         mf.reverse_edge(g, g.m)
+
+
+@pytest.mark.parametrize("name", ["rand3", "grid64", "rmat12", "C1"])
+def test_global_relabel_strict_retry_path(mf, name, monkeypatch):
+    """The safety net of the label-correcting global relabel (a frontier
+    overflow redoes it in strict mode; device_flags bit 3 forces that path):
+    heights stay bit-exact and flows stay the reference's."""
+    rec = G.rec[name]
+    n, us, vs, caps, s, t = instance(name)
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    p = mf.SolverParams(device_flags=8)
+    res = mf.solve_static(g, s, t, p)
+    assert res.flow_value == rec["static_flow"] == res.certificate.cut_capacity
+    monkeypatch.setenv("MFX_FLAGS", "8")
+    st = mf.init_residuals(g, s, t)
+    mf.saturate_source(st, g)
+    mf.backward_bfs(st, g)
+    assert sha(st.height) == rec["bfs_sat_sha"]
