@@ -636,29 +636,40 @@ struct Kern {
       a.ctrl->aq_stop = 0;
       a.ctrl->overflow = 0;  // dropped items are re-found by this global relabel
     }
-    // reset + seed bases (kernels.py:184-193); topology mode seeds wave 0
-    for (int v0 = gwarp * 32; v0 < n; v0 += gwarps * 32) {
-      int v = v0 + lane;
-      bool valid = v < n;
-      bool base;
-      if (PP) {  // push side: sink + deficits; pull side: source + overflow
-        long long ev = valid ? ldcg(a.ex + v) : 0;
-        base = valid && (region(v) == 0 ? (v == a.t || (v != a.s && ev < 0))
-                                        : (v == a.s || (v != a.t && ev > 0)));
-      } else {
-        long long ev = valid ? ldcg(a.ex + v) : 0;
-        base = valid && (v == a.t || (a.dyn_bases && v != a.s && ev < 0));
-        holders += valid && v != a.s && v != a.t && ev > 0;
+    // reset + seed bases (kernels.py:184-193); topology mode seeds wave 0.
+    // Four warp-strided chunks per iteration with their excess loads in
+    // flight together (the loop is a latency chain otherwise).
+    const int vstride = gwarps * 32;
+    for (int v0 = gwarp * 32; v0 < n; v0 += 4 * vstride) {
+      long long evs[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int v = v0 + r * vstride + lane;
+        evs[r] = v < n ? ldcg(a.ex + v) : 0;
       }
-      if (v == a.forbidden) base = false;
-      if (valid) a.h[v] = base ? 0 : n;
-      disc_cnt += base;
-      int b = base ? vbin(v) : 0;
-      append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
-      direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
-      bool topo = valid && a.topology && v != a.s && v != a.t;
-      int tb = topo ? vbin(v) : 0;
-      append_binned(1, topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int v = v0 + r * vstride + lane;
+        const bool valid = v < n;
+        const long long ev = evs[r];
+        bool base;
+        if (PP) {  // push side: sink + deficits; pull side: source + overflow
+          base = valid && (region(v) == 0 ? (v == a.t || (v != a.s && ev < 0))
+                                          : (v == a.s || (v != a.t && ev > 0)));
+        } else {
+          base = valid && (v == a.t || (a.dyn_bases && v != a.s && ev < 0));
+          holders += valid && v != a.s && v != a.t && ev > 0;
+        }
+        if (v == a.forbidden) base = false;
+        if (valid) a.h[v] = base ? 0 : n;
+        disc_cnt += base;
+        int b = base ? vbin(v) : 0;
+        append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
+        direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
+        bool topo = valid && a.topology && v != a.s && v != a.t;
+        int tb = topo ? vbin(v) : 0;
+        append_binned(1, topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap);
+      }
     }
     level_flush(a.F0, zero);
     holders = warp_sum(holders);
