@@ -264,6 +264,7 @@ struct Kern {
   Local &lc;
   WarpQ *q;  // this warp's staging queues
   int gtid, gthreads, gwarp, gwarps, lane, wib;
+  int swarp;  // warp index with CTAs fastest: thin lists spread over every SM
   int act_cnt;  // active discoveries counted by this lane in the current level
   long long *s_sink;  // per-CTA sum of excess pushed into the sink this round
   long long sink_acc; // this thread's share, not yet added to s_sink
@@ -306,6 +307,7 @@ struct Kern {
     wib = threadIdx.x >> 5;
     gwarp = gtid >> 5;
     gwarps = gthreads >> 5;
+    swarp = wib * (int)gridDim.x + (int)blockIdx.x;
     q = wq + wib;
     act_cnt = 0;
   }
@@ -466,6 +468,39 @@ struct Kern {
       if (r > 0 && (nocheck || ldcg(a.h + v) > nl)) low = relax(v, nl, first);
     }
     discovered(low, first, v, nl);
+  }
+
+  // K slots i, i + stride, ... (< hi) per lane of a long row: every load of
+  // the K slots is issued before any result is consumed, so a row scan is
+  // not a chain of one-slot round trips.  Warp-uniform trip count.
+  template <int K>
+  __device__ __forceinline__ void discover_slots(int i, int stride, int hi, int nl, int ru) {
+    int vv[K];
+    CapT rr[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = i + k * stride;
+      const bool valid = j < hi;
+      vv[k] = valid ? __ldg(a.adj + j) : -1;
+      CapT f = valid ? (CapT)ldcg((const CapT *)(a.cf + j)) : (CapT)0;
+      rr[k] = !valid ? (CapT)0 : (PP && ru == 1) ? f : __ldg(a.pc + j) - f;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (vv[k] == a.forbidden || (PP && vv[k] >= 0 && region(vv[k]) != ru)) rr[k] = 0;
+    int hv[K];
+    if (!nocheck) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) hv[k] = rr[k] > 0 ? ldcg(a.h + vv[k]) : -1;
+    }
+    bool low[K], fst[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      fst[k] = false;
+      low[k] = rr[k] > 0 && (nocheck || hv[k] > nl) && relax(vv[k], nl, fst[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) discovered(low[k], fst[k], vv[k], nl);
   }
 
   // Thread per item: the row (<= kBin0Max slots) is expanded with every load
@@ -701,19 +736,22 @@ struct Kern {
       // CTA-local sub-levels only while the frontier is thin (latency-bound
       // levels); wide levels stay grid-wide so no CTA serialises a share of
       // them (R-MAT hubs)
+      // them (R-MAT hubs)
       loc_ok = local_levels > 0 && tot <= a.bfs_local_max * (int)gridDim.x;
       // flags bit 1: thin (latency-bound) epochs relax by atomic alone
       nocheck = (a.flags & 1) != 0 || ((a.flags & 2) != 0 && loc_ok);
       int *const *Fc = (E & 1) ? a.F1 : a.F0;
       Fn_ = (E & 1) ? a.F0 : a.F1;
-      // bin 0: thread per item (warp-uniform trip count)
-      for (int j0 = gwarp * 32; j0 < cnt[0]; j0 += gwarps * 32) {
+      // bin 0: thread per item (warp-uniform trip count).  Chunks of 32 go
+      // round-robin over the CTAs first (swarp), so a thin frontier, and with
+      // it the CTA-local sub-levels grown from it, spreads over every SM.
+      for (int j0 = swarp * 32; j0 < cnt[0]; j0 += gwarps * 32) {
         int j = j0 + lane;
         bool valid = j < cnt[0];
         expand_item(valid, valid ? ldcg(Fc[0] + j) : 0);
       }
       // bin 1: warp per row
-      for (int j = gwarp; j < cnt[1]; j += gwarps) {
+      for (int j = swarp; j < cnt[1]; j += gwarps) {
         int u = ldcg(Fc[1] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         int nl = ldcg(a.h + u) + 1;
@@ -728,10 +766,8 @@ struct Kern {
         int nl = ldcg(a.h + u) + 1;
         if (threadIdx.x == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i0 = lo; i0 < hi; i0 += blockDim.x) {
-          int i = i0 + threadIdx.x;
-          discover_slot(i < hi, i, nl, region(u));
-        }
+        for (int i0 = lo; i0 < hi; i0 += 4 * blockDim.x)
+          discover_slots<4>(i0 + threadIdx.x, blockDim.x, hi, nl, region(u));
       }
       // bin 3: whole grid per row
       for (int j = 0; j < cnt[3]; ++j) {
@@ -740,10 +776,8 @@ struct Kern {
         int nl = ldcg(a.h + u) + 1;
         if (gtid == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i0 = lo + gwarp * 32; i0 < hi; i0 += gthreads) {
-          int i = i0 + lane;
-          discover_slot(i < hi, i, nl, region(u));
-        }
+        for (int i0 = lo + gwarp * 32; i0 < hi; i0 += 4 * gthreads)
+          discover_slots<4>(i0 + lane, gthreads, hi, nl, region(u));
       }
       drain_heavy();
       hq_ok = false;
@@ -1287,7 +1321,8 @@ struct Kern {
           tot += s_cnt[b];
         }
         const bool go = tot > 0 && tot <= a.tail_local && s_cnt[1] <= kWarps && s_cnt[2] == 0 &&
-                        s_cnt[3] == 0 && waves < max_waves;
+                        s_cnt[3] == 0 &&
+                        (waves < max_waves || (tot <= a.tail_items && waves < a.tail_cap));
         if (go) {  // consumed here: the next wave appends from zero
           for (int b = 0; b < NBIN; ++b) a.ctrl->live[C_RNEXT + b] = 0;
           __threadfence();

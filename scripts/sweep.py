@@ -3,7 +3,10 @@ several solver knobs; prints per-setting timing and phase split, and checks
 every setting agrees on every flow.
 
     python scripts/sweep.py --graph grid --side 2048 --batch 10000 --batches 3 \
-        --knobs 'max_waves=0' 'max_waves=8' 'wave_mult=4,wave_add=32'
+        --knobs 'max_waves=0' 'max_waves=8' 'wave_mult=4,wave_add=32' 'MFX_TAIL_LOCAL=0'
+
+Knobs are SolverParams fields, or MFX_* environment knobs (read per solve;
+MFX_VARIANT is fixed per graph at its first solve, so it needs its own run).
 """
 import argparse
 import json
@@ -34,6 +37,9 @@ def instance(kind, side, scale):
         us, vs, caps, s, t = gen.random_graph(10000, 100000, 0)
         return 10000, us, vs, caps, s, t
     raise ValueError(kind)
+
+
+ENV_SET = set()
 
 
 def parse_knobs(spec):
@@ -80,6 +86,12 @@ def main():
     for spec in args.knobs:
         kn = parse_knobs(spec)
         pp = bool(kn.pop("pp", 0))  # O2 push-pull dynamic solves
+        for k in ENV_SET:
+            os.environ.pop(k, None)
+        ENV_SET.clear()
+        for k in [k for k in kn if k.startswith("MFX_")]:  # engine env knobs
+            os.environ[k] = str(kn.pop(k))
+            ENV_SET.add(k)
         p = mfx.SolverParams(**kn)
         gg = base.copy()
         mfx.solve_static(gg, s, t, p)  # warm
