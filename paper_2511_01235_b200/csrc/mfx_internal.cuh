@@ -90,6 +90,8 @@ struct Ctrl {
   int tail_base[NBIN];
   int tail_waves;
   unsigned tail_stamp;
+  // trace mode only: vertices expanded per BFS epoch (sum, max over CTAs), by epoch parity
+  unsigned dbg_sum[2], dbg_max[2];
 };
 
 // ---- small device helpers -------------------------------------------------

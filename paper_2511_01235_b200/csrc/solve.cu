@@ -403,15 +403,20 @@ struct Kern {
   static constexpr int kFirstBit = (int)0x80000000;
   static constexpr int kIdMask = 0x7fffffff;
   static constexpr int kHQ = 256;  // CTA heavy-row list
+  static constexpr int kRing = 2 * kLQ;  // (power of two)
+  static constexpr int kEmpty = -1;      // (not an item: ids are < 2^31 - 1)
+  enum { RQ_TAIL = 0, RQ_HEAD = 1, RQ_RD = 2, RQ_DONE = 3 };
   unsigned ep_next;  // ownership stamp of the coming asynchronous push phase
   unsigned bst;      // this epoch's stamp for next-frontier dedupe
   int disc_cnt;      // first discoveries (+ bases) by this lane
+  int xc;            // trace mode: vertices this lane expanded in the epoch
   int max_lab;       // largest label this lane set
   bool loc_ok;       // discoveries may go to the CTA-local queue
   bool nocheck;      // relax with the atomic alone (no h[v] pre-load)
-  int lq_nx;         // CTA-local queue receiving discoveries
-  int *lqb;          // CTA-local queues (shared memory, 2 x kLQ)
-  int *lq_cnt;       // their fill counters (shared memory)
+  int *ring;         // CTA-local work ring (shared memory, kRing slots, kEmpty = free)
+  unsigned *rq;      // its counters: RQ_TAIL reserved, RQ_HEAD claimed, RQ_RD released, RQ_DONE
+  int ring_cap;      // slots the ring may hold at once (<= kRing)
+  int lcap;          // largest label a discovery may carry into the ring this epoch
   int *hq;           // CTA heavy-row list (shared memory, kHQ)
   int *hq_cnt;
   bool hq_ok;        // long rows may go to the CTA's heavy-row list
@@ -422,6 +427,75 @@ struct Kern {
     int old = atomicMin(a.h + v, nl);
     first = old == a.n;
     return nl < old;
+  }
+
+  // k ring slots, or -1 when the ring lacks room (slots are free once
+  // released, RQ_RD, which follows the claim order).  One lane.
+  __device__ __forceinline__ int ring_reserve(int k) {
+    volatile unsigned *vq = rq;
+    for (;;) {
+      unsigned t = vq[RQ_TAIL], r = vq[RQ_RD];
+      if ((int)(t + k - r) > ring_cap) return -1;
+      if (atomicCAS(rq + RQ_TAIL, t, t + k) == t) return (int)t;
+    }
+  }
+
+  // CTA-local BFS over the ring, asynchronous: each warp claims up to 32
+  // queued items, expands them (its discoveries join the ring) and marks
+  // them done; no barrier between BFS levels, the atomicMin relaxation makes
+  // the order immaterial (label-correcting).  Ends when every reserved item
+  // is done (done is read before tail; an expansion reserves its discoveries
+  // before its item counts as done).  Whole CTA.
+  __device__ void ring_drain() {
+    volatile unsigned *vq = rq;
+    volatile int *vr = ring;
+    for (;;) {
+      unsigned h = 0;
+      int c = 0;
+      bool fin = false;
+      if (lane == 0) {
+        for (;;) {
+          h = vq[RQ_HEAD];
+          unsigned t = vq[RQ_TAIL];
+          if (h == t) break;
+          c = (int)(t - h) < 32 ? (int)(t - h) : 32;
+          if (atomicCAS(rq + RQ_HEAD, h, h + c) == h) break;
+          c = 0;
+        }
+        if (c == 0) {
+          unsigned d = vq[RQ_DONE];
+          __threadfence_block();
+          fin = d == vq[RQ_TAIL];
+        }
+      }
+      c = __shfl_sync(FULL, c, 0);
+      if (c == 0) {
+        if (__shfl_sync(FULL, (int)fin, 0)) break;
+        __nanosleep(64);
+        continue;
+      }
+      h = __shfl_sync(FULL, h, 0);
+      int item = 0;
+      if (lane < c) {  // a reserved slot is written right after its reservation
+        const int q = (int)((h + lane) & (kRing - 1));
+        while ((item = vr[q]) == kEmpty) {
+        }
+        vr[q] = kEmpty;
+      }
+      __syncwarp();
+      if (lane == 0) {  // release in claim order
+        while (vq[RQ_RD] != h) {
+        }
+        __threadfence_block();
+        vq[RQ_RD] = h + c;
+      }
+      expand_item(lane < c, item);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        atomicAdd(rq + RQ_DONE, (unsigned)c);
+      }
+    }
   }
 
   // Label of v lowered (low) to nl; first = v was unreached.  Warp-synchronous.
@@ -435,15 +509,15 @@ struct Kern {
     }
     const int item = v | (first ? kFirstBit : 0);
     bool glob = low;
-    if (loc_ok) {  // expand it in this CTA's next sub-level
-      unsigned m = __ballot_sync(FULL, low);
+    if (loc_ok) {  // expanded by this CTA within the epoch (ring), label permitting
+      const bool want = low && nl <= lcap;
+      unsigned m = __ballot_sync(FULL, want);
       if (m) {
         int leader = __ffs(m) - 1, pos0 = 0;
-        if (lane == leader) pos0 = atomicAdd(lq_cnt + lq_nx, __popc(m));
+        if (lane == leader) pos0 = ring_reserve(__popc(m));
         pos0 = __shfl_sync(FULL, pos0, leader);
-        int p = pos0 + __popc(m & lanemask_lt());
-        if (low && p < a.lq_cap) {
-          lqb[lq_nx * kLQ + p] = item;
+        if (want && pos0 >= 0) {  // (no room: the global next frontier)
+          ring[(pos0 + __popc(m & lanemask_lt())) & (kRing - 1)] = item;
           glob = false;
         }
       }
@@ -509,6 +583,7 @@ struct Kern {
   __device__ __forceinline__ void expand_item(bool valid, int item) {
     const int u = item & kIdMask;
     const bool first = valid && item < 0;
+    xc += valid;
     int lo = 0, d = 0, hu = a.n;
     long long eu = 0;
     if (valid) {
@@ -619,6 +694,30 @@ struct Kern {
     if (lane == 0 && m) atomicMax(a.ctrl->live + C_DEPTH, m);
   }
 
+  // Trace mode: per-epoch expansion counts (sum and max over CTAs), recorded
+  // by CTA 0 after the epoch's barrier as a phase-6 trace entry.  Whole CTA.
+  __device__ void epoch_stats(int E, bool before) {
+    __shared__ unsigned s_xc;
+    Ctrl *c = a.ctrl;
+    if (before) {
+      if (threadIdx.x == 0) s_xc = 0;
+      __syncthreads();
+      int w = warp_sum(xc);
+      if (lane == 0 && w) atomicAdd(&s_xc, (unsigned)w);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        atomicAdd(c->dbg_sum + (E & 1), s_xc);
+        atomicMax(c->dbg_max + (E & 1), s_xc);
+      }
+    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned sum = __ldcg(c->dbg_sum + (E & 1)), mx = __ldcg(c->dbg_max + (E & 1));
+      c->dbg_sum[E & 1] = 0;
+      c->dbg_max[E & 1] = 0;
+      if (sy.trace && sy.trace_n < sy.trace_cap)
+        sy.trace[sy.trace_n++] = (6ull << 60) | ((unsigned long long)(mx & 0xFFFFFFFu) << 32) | sum;
+    }
+  }
+
   // Returns the BFS depth (levels incl. level 0 = max label + 1); the active
   // set is left in R (wave 0).  ep: ownership stamp the following
   // asynchronous push phase will use; bstamp: persistent epoch stamp.
@@ -627,8 +726,8 @@ struct Kern {
     int holders = 0;  // vertices (not s, t) with positive excess
     __shared__ int zero[NBIN];
     __shared__ int rb[NBIN];
-    __shared__ int s_lq[2][kLQ];
-    __shared__ int s_lqc[2];
+    __shared__ int s_ring[kRing];
+    __shared__ unsigned s_rq[4];
     __shared__ int s_hq[kHQ];
     __shared__ int s_hqc;
     // A frontier list that overflowed (label-correcting duplicates beyond
@@ -643,16 +742,18 @@ struct Kern {
     holders = 0;
     loc_ok = false;
     nocheck = (a.flags & 1) != 0;
-    lqb = &s_lq[0][0];
-    lq_cnt = s_lqc;
-    lq_nx = 0;
+    ring = s_ring;
+    rq = s_rq;
+    ring_cap = 2 * a.lq_cap < kRing ? 2 * a.lq_cap : kRing;
+    lcap = 0;
+    for (int q = threadIdx.x; q < kRing; q += blockDim.x) s_ring[q] = kEmpty;
     hq = s_hq;
     hq_cnt = &s_hqc;
     hq_ok = true;
     rb_ = zero;
     Fn_ = a.F0;
     if (threadIdx.x < NBIN) zero[threadIdx.x] = 0;
-    if (threadIdx.x < 2) s_lqc[threadIdx.x] = 0;
+    if (threadIdx.x < 4) s_rq[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_hqc = 0;
     __syncthreads();
     // empty the R lists (async consumers wait on -1 slots) and the async counters
@@ -733,11 +834,13 @@ struct Kern {
       __syncthreads();
       rb_ = rb;
       bst = ++bstamp;
+      xc = 0;
       // CTA-local sub-levels only while the frontier is thin (latency-bound
       // levels); wide levels stay grid-wide so no CTA serialises a share of
       // them (R-MAT hubs)
       // them (R-MAT hubs)
       loc_ok = local_levels > 0 && tot <= a.bfs_local_max * (int)gridDim.x;
+      lcap = sy.s_snap[C_DEPTH] + local_levels;  // (labels so far <= C_DEPTH)
       // flags bit 1: thin (latency-bound) epochs relax by atomic alone
       nocheck = (a.flags & 1) != 0 || ((a.flags & 2) != 0 && loc_ok);
       int *const *Fc = (E & 1) ? a.F1 : a.F0;
@@ -755,6 +858,7 @@ struct Kern {
         int u = ldcg(Fc[1] + j);
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         int nl = ldcg(a.h + u) + 1;
+        xc += lane == 0;
         if (lane == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
         for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl, region(u));
@@ -781,32 +885,17 @@ struct Kern {
       }
       drain_heavy();
       hq_ok = false;
-      // CTA-local sub-levels over this CTA's own discoveries
-      const bool local_epoch = loc_ok;
-      for (int sub = 1; sub <= local_levels && local_epoch; ++sub) {
-        __syncthreads();
-        const int cur = lq_nx;
-        int c = s_lqc[cur];
-        __syncthreads();
-        if (c == 0) break;
-        if (c > a.lq_cap) c = a.lq_cap;
-        if (threadIdx.x == 0) s_lqc[cur] = 0;  // cur becomes the receiver after next
-        lq_nx = cur ^ 1;
-        loc_ok = sub < local_levels;
-        for (int j0 = wib * 32; j0 < c; j0 += kWarps * 32) {
-          int j = j0 + lane;
-          bool valid = j < c;
-          expand_item(valid, valid ? lqb[cur * kLQ + j] : 0);
-        }
-      }
+      // this CTA's own discoveries, asynchronously, up to label lcap
+      if (loc_ok) ring_drain();
       hq_ok = true;
       loc_ok = false;
       level_flush(Fn_, rb);
+      if (a.trace) epoch_stats(E, true);
       grid_sync(a.ctrl, sy, fmask, rmask | amask, 0, PH_BFS);
+      if (a.trace) epoch_stats(E, false);
       ++E;
     }
     __syncthreads();
-    if (threadIdx.x < 2) s_lqc[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_hqc = 0;
     E_all += E;
     // (read after the last barrier: uniform; flags bit 3 forces the retry, for tests)

@@ -1,6 +1,7 @@
 """Small, deterministic workload for ncu: build C2 (or a smaller grid), one
 warm-up static solve, one static solve, then `--batches` dynamic batches.
-Launch order of mfx::solve_kernel: [warm static, static, dyn 1, dyn 2, ...].
+Launch order of mfx::solve_kernel: [warm static, static, dyn 1, dyn 2, ...,
+relabel 1, ...].
 
     ncu --set full -k regex:solve_kernel --launch-skip 2 --launch-count 1 \
         python scripts/profile_target.py      # profiles dynamic batch 1
@@ -21,6 +22,8 @@ def main():
     ap.add_argument("--side", type=int, default=2048)
     ap.add_argument("--batch", type=int, default=10000)
     ap.add_argument("--batches", type=int, default=2)
+    ap.add_argument("--relabels", type=int, default=0,
+                    help="then this many dynamic global relabels (WHAT_BFS launches)")
     args = ap.parse_args()
     us, vs, caps, s, t = gen.grid_graph(args.side, args.side, 0)
     n = args.side * args.side + 2
@@ -37,6 +40,8 @@ def main():
         rr = mfx.solve_dynamic(st, g, mfx.UpdateBatch(bu, bv, bc))
         out.append((f"dyn{i}", rr.flow_value, rr.device["ms_solve"]))
         st = rr.state
+    for i in range(args.relabels):  # BFS alone on the last state (dynamic bases)
+        out.append((f"relabel{i}", mfx.backward_bfs_dynamic(st, g), 0.0))
     for row in out:
         print(*row)
 

@@ -47,6 +47,8 @@ def report(tag, st, g, res):
             print(f"    state {int(states[i])} done {int(d[i])} tail {int(t[i])}")
         keep = ~raw
         ph, items, dt = ph[keep], items[keep], dt[keep]
+    keep = ph != 6  # epoch expansion stats (rounds_view)
+    ph, items, dt = ph[keep], items[keep], dt[keep]
     print(f"== {tag}: {res.device['ms_solve']:.2f} ms, rounds {res.rounds}, "
           f"levels {res.device['bfs_levels']}, waves {res.device['waves']}, barriers {len(ph)}")
     # item count of entry i is the work of the phase that ends at entry i+1
@@ -65,10 +67,20 @@ def report(tag, st, g, res):
 
 
 def rounds_view(tag, st, g):
-    """Per round: BFS epochs + time, then the push waves' item counts."""
+    """Per round: BFS epochs + time (+ vertices expanded: sum / max per CTA,
+    from the phase-6 entries), then the push waves' item counts."""
     ph, items, dt = fetch(st, g)
     keep = ph != 7
     ph, items, dt = ph[keep], items[keep], dt[keep]
+    # a phase-6 entry follows its epoch's barrier entry
+    xs = {}
+    out = []
+    for q in range(len(ph)):
+        if ph[q] == 6:
+            xs[len(out) - 1] = (int(dt[q]), int(items[q]))
+        else:
+            out.append(q)
+    ph, items, dt = ph[out], items[out], dt[out]
     work = np.concatenate([[0], items[:-1]])
     print(f"-- {tag}: per-round sequence")
     i, rnd = 0, 0
@@ -83,7 +95,8 @@ def rounds_view(tag, st, g):
         waves = work[j:k]
         push_us = dt[j:k].sum() / 1e3
         rep = dt[k:k + 1].sum() / 1e3 if k < len(ph) and ph[k] == 2 else 0.0
-        ep = " ".join(f"{int(work[q])}:{dt[q] / 1e3:.0f}" for q in range(i, j))
+        ep = " ".join(f"{int(work[q])}:{dt[q] / 1e3:.0f}"
+                      + (f"[{xs[q][0]}/{xs[q][1]}]" if q in xs else "") for q in range(i, j))
         print(f"    bfs epochs (items:us) {ep}")
         print(f"  round {rnd}: bfs {j - i} epochs {bfs_us:8.1f} us | {k - j} waves {push_us:8.1f} us "
               f"items first/max/last {waves[:1].tolist()}/{int(waves.max()) if len(waves) else 0}/"
