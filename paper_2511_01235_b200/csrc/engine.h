@@ -99,7 +99,7 @@ struct SolveConfig {
   int walk_depth = 0;     // ... and the BFS is at least walk_depth levels deep
   int max_ctas = 0;       // cap on the persistent grid (0: every SM at full occupancy)
   int tail_local = 256;   // push waves of <= tail_local short-row items run in CTA 0 alone
-  int bfs_local = 32;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
+  int bfs_local = 128;    // CTA-local BFS levels per grid barrier (0 = level-synchronous)
   int topology = 0;
   double timeout_s = 600.0;
   int blocks_per_sm = 0;

@@ -45,8 +45,9 @@ class SolverParams:
     value does not depend on it.  Device knobs: ``max_waves`` (push waves per
     round before the next global relabel, 0 = until the active list drains),
     ``timeout_s`` (device watchdog; 0 = $MFX_TIMEOUT_S or 600 s), ``blocks_per_sm`` (persistent grid),
-    ``bfs_local`` (CTA-local BFS sub-levels per grid barrier in the global
-    relabel; 0 = default 32, < 0 = strict level-synchronous BFS).
+    ``bfs_local`` (BFS levels a CTA may run ahead on its own between two grid
+    barriers of the global relabel; 0 = default 128, < 0 = strict
+    level-synchronous BFS).
     """
 
     kernel_cycles: int = 0
