@@ -54,6 +54,7 @@ enum CtrIdx {
   C_REACHED = 12, // vertices reached by the global relabel (bases + first discoveries)
   C_DEPTH = 13,  // largest BFS label set (max-combined, not summed)
   C_EHOLD = 14,  // vertices holding excess when the global relabel started
+  C_STOP = 15,   // set by the barrier leader: this round's push-phase time budget is spent
   C_NCTR = 16
 };
 
@@ -90,6 +91,9 @@ struct Ctrl {
   int tail_base[NBIN];
   int tail_waves;
   unsigned tail_stamp;
+  // push-phase time budget (wave_time): start of the last global relabel,
+  // and the deadline of the current push phase (0: none)
+  unsigned long long bfs_t0, wave_deadline;
   // trace mode only: vertices expanded per BFS epoch (sum, max over CTAs), by epoch parity
   unsigned dbg_sum[2], dbg_max[2];
 };

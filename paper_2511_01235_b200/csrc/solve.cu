@@ -64,6 +64,7 @@ struct SolveArgs {
   int walk_max;      // excess walk after a global relabel with <= this many active vertices
   int walk_depth;    // ... at least this many BFS levels deep
   int tail_local;    // push waves of <= this many items run in CTA 0 alone (0: off)
+  int wave_time;     // push phase time budget, eighths of the last BFS's time (0: off)
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -166,8 +167,11 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
           vc->snap[i] = 0;
         }
       }
+      const unsigned long long now = globaltimer();
+      const unsigned long long wdl = vc->wave_deadline;
+      vc->snap[C_STOP] = phase == PH_PUSH && wdl != 0 && now > wdl;
       if (!ab) {
-        if (globaltimer() > sy.deadline) {
+        if (now > sy.deadline) {
           vc->abort = 1;
           vc->status = 6;
         } else if (p + r > sy.ceiling) {
@@ -735,6 +739,7 @@ struct Kern {
     // leave the labels incomplete, so the relabel is then redone in strict
     // level-synchronous mode, which lists every vertex at most once.
     int E_all = 0;  // epochs over the attempts
+    if (gtid == 0) a.ctrl->bfs_t0 = globaltimer();  // (push-phase time budget)
     for (int attempt = 0;; ++attempt) {
     ep_next = ep;
     disc_cnt = 0;
@@ -1411,7 +1416,8 @@ struct Kern {
         }
         const bool go = tot > 0 && tot <= a.tail_local && s_cnt[1] <= kWarps && s_cnt[2] == 0 &&
                         s_cnt[3] == 0 &&
-                        (waves < max_waves || (tot <= a.tail_items && waves < a.tail_cap));
+                        (waves < max_waves || (tot <= a.tail_items && waves < a.tail_cap)) &&
+                        !(a.wave_time > 0 && globaltimer() > a.ctrl->wave_deadline);
         if (go) {  // consumed here: the next wave appends from zero
           for (int b = 0; b < NBIN; ++b) a.ctrl->live[C_RNEXT + b] = 0;
           __threadfence();
@@ -1442,6 +1448,11 @@ struct Kern {
       cnt[b] = sy.s_snap[C_RNEXT + b];
     }
     int waves = 0;
+    if (gtid == 0) {  // (read by the wave barriers' leaders)
+      const unsigned long long now = globaltimer();
+      a.ctrl->wave_deadline =
+          a.wave_time > 0 ? now + (now - a.ctrl->bfs_t0) * (unsigned long long)a.wave_time / 8 : 0;
+    }
     for (;;) {
       // (only short rows: a warp-wide row in CTA 0 alone would idle the grid)
       if (a.tail_local > 0 && cnt[0] + cnt[1] <= a.tail_local && cnt[1] <= kWarps &&
@@ -1456,7 +1467,7 @@ struct Kern {
         }
         waves = ldcg(&a.ctrl->tail_waves);
         stamp = (unsigned)ldcg((const int *)&a.ctrl->tail_stamp);
-        if (tot == 0 || *sy.s_abort) break;
+        if (tot == 0 || *sy.s_abort || sy.s_snap[C_STOP]) break;
         if (waves >= max_waves && (tot > a.tail_items || waves >= a.tail_cap)) break;
         continue;
       }
@@ -1493,7 +1504,7 @@ struct Kern {
       }
       // past the budget, keep going while the waves stay small (a thin wave
       // costs ~1 % of a global relabel) up to tail_cap waves
-      if (tot == 0 || *sy.s_abort) break;
+      if (tot == 0 || *sy.s_abort || sy.s_snap[C_STOP]) break;
       if (waves >= max_waves && (tot > a.tail_items || waves >= a.tail_cap)) break;
     }
     int end[NBIN];
@@ -1947,6 +1958,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.walk_max = cfg.walk_max;
   a.walk_depth = cfg.walk_depth;
   a.tail_local = cfg.tail_local;
+  a.wave_time = cfg.wave_time;
   a.coop_kc = cfg.coop_kc > 0 ? (cfg.coop_kc < cfg.kc ? cfg.coop_kc : cfg.kc) : cfg.kc;
   a.tail_cap = cfg.tail_cap;
   a.bmark = W.bmark;
