@@ -127,6 +127,7 @@ struct Sync {
   int *s_abort;
   unsigned long long deadline, ceiling;  // read once at kernel start
   unsigned long long t_last;             // block 0: phase timing
+  unsigned long long t_tail;             // block 0: last tail-wave timestamp (trace)
   unsigned long long ph[PH_N];
   unsigned long long *trace;  // block 0: (phase << 60 | items << 32 | dt_ns) per barrier
   int trace_cap, trace_n;
@@ -1387,6 +1388,7 @@ struct Kern {
                              int *nbase, long long *s_red) {
     __shared__ int s_cnt[NBIN];
     __shared__ int s_go;
+    if (threadIdx.x == 0) sy.t_tail = globaltimer();
     for (;;) {
       const unsigned next = ++stamp;
       __syncthreads();
@@ -1413,6 +1415,12 @@ struct Kern {
         for (int b = 0; b < NBIN; ++b) {
           s_cnt[b] = ldcg(a.ctrl->live + C_RNEXT + b);
           tot += s_cnt[b];
+        }
+        if (sy.trace && sy.trace_n < sy.trace_cap) {  // (CTA 0 holds the trace) phase-5 entry per wave
+          const unsigned long long now = globaltimer();
+          sy.trace[sy.trace_n++] = (5ull << 60) | ((unsigned long long)(tot & 0xFFFFFFF) << 32) |
+                                   ((now - sy.t_tail) & 0xFFFFFFFFull);
+          sy.t_tail = now;
         }
         const bool go = tot > 0 && tot <= a.tail_local && s_cnt[1] <= kWarps && s_cnt[2] == 0 &&
                         s_cnt[3] == 0 &&

@@ -47,7 +47,7 @@ def report(tag, st, g, res):
             print(f"    state {int(states[i])} done {int(d[i])} tail {int(t[i])}")
         keep = ~raw
         ph, items, dt = ph[keep], items[keep], dt[keep]
-    keep = ph != 6  # epoch expansion stats (rounds_view)
+    keep = (ph != 6) & (ph != 5)  # epoch expansion stats / tail waves (rounds_view)
     ph, items, dt = ph[keep], items[keep], dt[keep]
     print(f"== {tag}: {res.device['ms_solve']:.2f} ms, rounds {res.rounds}, "
           f"levels {res.device['bfs_levels']}, waves {res.device['waves']}, barriers {len(ph)}")
@@ -74,11 +74,18 @@ def rounds_view(tag, st, g):
     ph, items, dt = ph[keep], items[keep], dt[keep]
     # a phase-6 entry follows its epoch's barrier entry
     xs = {}
+    tails = {}  # CTA-0 tail waves (items after the wave : us), by the barrier entry that follows
     out = []
+    pend = []
     for q in range(len(ph)):
         if ph[q] == 6:
             xs[len(out) - 1] = (int(dt[q]), int(items[q]))
+        elif ph[q] == 5:
+            pend.append(f"{int(items[q])}:{dt[q] / 1e3:.0f}")
         else:
+            if pend:
+                tails[len(out)] = pend
+                pend = []
             out.append(q)
     ph, items, dt = ph[out], items[out], dt[out]
     work = np.concatenate([[0], items[:-1]])
@@ -101,6 +108,9 @@ def rounds_view(tag, st, g):
         print(f"  round {rnd}: bfs {j - i} epochs {bfs_us:8.1f} us | {k - j} waves {push_us:8.1f} us "
               f"items first/max/last {waves[:1].tolist()}/{int(waves.max()) if len(waves) else 0}/"
               f"{waves[-1:].tolist()} | repair {rep:6.1f} us")
+        tw = [w for q in range(j, k + 1) for w in tails.get(q, [])]
+        if tw:
+            print(f"    tail waves (items:us) {len(tw)}: " + " ".join(tw[:40]) + (" ..." if len(tw) > 40 else ""))
         i = k + (1 if k < len(ph) and ph[k] == 2 else 0)
         rnd += 1
         if j == i and k == j:
