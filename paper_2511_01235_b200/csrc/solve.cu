@@ -982,6 +982,9 @@ struct Kern {
     // or exhausts u), so the old head excess per slot fits in registers and
     // the activation tests wait for all atomics together after the loop.
     long long oldv[kBin0Max];
+    unsigned clm[kBin0Max];
+#pragma unroll
+    for (int k = 0; k < kBin0Max; ++k) clm[k] = ~0u;
     unsigned pushed = 0;
     long long e_after = eu;  // u's excess after its last push (from the atomic)
     bool own_atomic = false;
@@ -1012,15 +1015,16 @@ struct Kern {
               if (pull) {  // pull dd along (v, u) (kernels.py:96-143)
                 atomic_add(a.cf + rv[k], (CapT)(-dd));
                 atomic_add(a.cf + lo + k, (CapT)dd);
-                own_old = -atomic_add(a.ex + u, dd);
                 oldv[k] = -atomic_add(a.ex + vv[k], -dd);
               } else {
                 atomic_add(a.cf + lo + k, (CapT)(-dd));
                 atomic_add(a.cf + rv[k], (CapT)dd);
-                own_old = atomic_add(a.ex + u, -dd);
                 oldv[k] = add_excess(vv[k], dd);
               }
-              own_d = dd;
+              // wave mode: the head is claimed for the next wave right away
+              // (in flight with the push, not after its result)
+              if (!Async && vv[k] != a.s && vv[k] != a.t) clm[k] = atomicMax(a.mark + vv[k], stamp);
+              own_d += dd;
               pushed |= 1u << k;
             }
           own_atomic = true;
@@ -1033,13 +1037,30 @@ struct Kern {
         }
       }
     }
-    if (own_atomic) e_after = own_old - own_d;
+    // u's own excess drops once by everything it pushed (one atomic, not one
+    // per push: a per-push atomic whose result lands in the same register
+    // made every push step wait for the previous one).  Nothing reads ex[u]
+    // for a decision meanwhile: concurrent pushers into u only need "was u
+    // already holding excess", which it was.
+    if (own_atomic) {
+      own_old = pull ? -atomic_add(a.ex + u, own_d) : atomic_add(a.ex + u, -own_d);
+      e_after = own_old - own_d;
+    }
     // pushes must be visible before a head is handed to another owner
     if (Async) __threadfence();
+    // A pushed head joins the next wave: in wave mode whenever this push
+    // claimed it (a head that already held excess, or got none net, is then
+    // a no-op item; one that was claimed before is listed already); in the
+    // asynchronous phase when it was not holding excess before the push.
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) {
-      bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
-      activate(p, vv[k], bb[k], stamp, nbase);
+      if (Async) {
+        bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
+        activate(p, vv[k], bb[k], stamp, nbase);
+      } else {
+        append_binned(1, (pushed >> k & 1) && clm[k] < stamp, vv[k], bb[k], a.ctrl->live + C_RNEXT,
+                      a.R, nbase, a.rcap);
+      }
     }
     if (Async) {
       // Release ownership, then re-check: a pusher that found u owned did not
@@ -1499,6 +1520,11 @@ struct Kern {
         for (int j = base[b] + blockIdx.x; j < lim[b]; j += gridDim.x)
           push_coop<kBlock, false>(ldcg(a.R[b] + j), next, nbase, s_red);
       stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
+      if (a.trace) {  // trace: CTA 0's own share of the wave done (phase-4 entry)
+        __syncthreads();
+        if (blockIdx.x == 0 && threadIdx.x == 0 && sy.trace_n < sy.trace_cap)
+          sy.trace[sy.trace_n++] = (4ull << 60) | ((globaltimer() - sy.t_last) & 0xFFFFFFFFull);
+      }
       // (the sink's excess and the counters are published once per round:
       // nothing reads them between waves, and the ceiling check may lag a
       // round)

@@ -47,7 +47,7 @@ def report(tag, st, g, res):
             print(f"    state {int(states[i])} done {int(d[i])} tail {int(t[i])}")
         keep = ~raw
         ph, items, dt = ph[keep], items[keep], dt[keep]
-    keep = (ph != 6) & (ph != 5)  # epoch expansion stats / tail waves (rounds_view)
+    keep = (ph != 6) & (ph != 5) & (ph != 4)  # epoch stats / tail waves / CTA-0 wave work (rounds_view)
     ph, items, dt = ph[keep], items[keep], dt[keep]
     print(f"== {tag}: {res.device['ms_solve']:.2f} ms, rounds {res.rounds}, "
           f"levels {res.device['bfs_levels']}, waves {res.device['waves']}, barriers {len(ph)}")
@@ -75,6 +75,7 @@ def rounds_view(tag, st, g):
     # a phase-6 entry follows its epoch's barrier entry
     xs = {}
     tails = {}  # CTA-0 tail waves (items after the wave : us), by the barrier entry that follows
+    work0 = {}  # CTA 0's own work time in a grid-wide wave, by that wave's barrier entry
     out = []
     pend = []
     for q in range(len(ph)):
@@ -82,6 +83,8 @@ def rounds_view(tag, st, g):
             xs[len(out) - 1] = (int(dt[q]), int(items[q]))
         elif ph[q] == 5:
             pend.append(f"{int(items[q])}:{dt[q] / 1e3:.0f}")
+        elif ph[q] == 4:
+            work0[len(out)] = int(dt[q])
         else:
             if pend:
                 tails[len(out)] = pend
@@ -108,6 +111,9 @@ def rounds_view(tag, st, g):
         print(f"  round {rnd}: bfs {j - i} epochs {bfs_us:8.1f} us | {k - j} waves {push_us:8.1f} us "
               f"items first/max/last {waves[:1].tolist()}/{int(waves.max()) if len(waves) else 0}/"
               f"{waves[-1:].tolist()} | repair {rep:6.1f} us")
+        w0 = [work0[q] for q in range(j, k) if q in work0]
+        if w0:
+            print(f"    grid waves: CTA 0 busy {np.mean(w0) / 1e3:.1f} us of {push_us / max(1, len(w0)):.1f} us per wave")
         tw = [w for q in range(j, k + 1) for w in tails.get(q, [])]
         if tw:
             print(f"    tail waves (items:us) {len(tw)}: " + " ".join(tw[:40]) + (" ..." if len(tw) > 40 else ""))
