@@ -779,38 +779,70 @@ struct Kern {
       a.ctrl->overflow = 0;  // dropped items are re-found by this global relabel
     }
     // reset + seed bases (kernels.py:184-193); topology mode seeds wave 0.
-    // Four warp-strided chunks per iteration with their excess loads in
-    // flight together (the loop is a latency chain otherwise).
-    const int vstride = gwarps * 32;
-    for (int v0 = gwarp * 32; v0 < n; v0 += 4 * vstride) {
-      long long evs[4];
+    // A lane takes 8 consecutive vertices: 4 x 16-byte excess loads in
+    // flight together and 2 x 16-byte height stores (the pass is a latency
+    // chain otherwise); the rare bases are appended only when the warp has one.
+    constexpr int V = 8;
+    for (int v0 = gwarp * 32 * V; v0 < n; v0 += gwarps * 32 * V) {
+      const int vb = v0 + lane * V;
+      const bool full = vb + V <= n;
+      long long ev[V];
+      if (full) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int v = v0 + r * vstride + lane;
-        evs[r] = v < n ? ldcg(a.ex + v) : 0;
+        for (int r = 0; r < V; r += 2) {
+          const longlong2 e2 = __ldcg(reinterpret_cast<const longlong2 *>(a.ex + vb + r));
+          ev[r] = e2.x;
+          ev[r + 1] = e2.y;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < V; ++r) ev[r] = vb + r < n ? ldcg(a.ex + vb + r) : 0;
       }
+      unsigned bm = 0;  // bases among this lane's vertices
+      int hv[V];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int v = v0 + r * vstride + lane;
+      for (int r = 0; r < V; ++r) {
+        const int v = vb + r;
         const bool valid = v < n;
-        const long long ev = evs[r];
         bool base;
         if (PP) {  // push side: sink + deficits; pull side: source + overflow
-          base = valid && (region(v) == 0 ? (v == a.t || (v != a.s && ev < 0))
-                                          : (v == a.s || (v != a.t && ev > 0)));
+          base = valid && (region(v) == 0 ? (v == a.t || (v != a.s && ev[r] < 0))
+                                          : (v == a.s || (v != a.t && ev[r] > 0)));
         } else {
-          base = valid && (v == a.t || (a.dyn_bases && v != a.s && ev < 0));
-          holders += valid && v != a.s && v != a.t && ev > 0;
+          base = valid && (v == a.t || (a.dyn_bases && v != a.s && ev[r] < 0));
+          holders += valid && v != a.s && v != a.t && ev[r] > 0;
         }
         if (v == a.forbidden) base = false;
-        if (valid) a.h[v] = base ? 0 : n;
-        disc_cnt += base;
-        int b = base ? vbin(v) : 0;
-        append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
-        direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
-        bool topo = valid && a.topology && v != a.s && v != a.t;
-        int tb = topo ? vbin(v) : 0;
-        append_binned(1, topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap);
+        hv[r] = base ? 0 : n;
+        bm |= (unsigned)base << r;
+      }
+      if (full) {
+        reinterpret_cast<int4 *>(a.h + vb)[0] = make_int4(hv[0], hv[1], hv[2], hv[3]);
+        reinterpret_cast<int4 *>(a.h + vb)[1] = make_int4(hv[4], hv[5], hv[6], hv[7]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < V; ++r)
+          if (vb + r < n) a.h[vb + r] = hv[r];
+      }
+      disc_cnt += __popc(bm);
+      if (__any_sync(FULL, bm != 0)) {
+#pragma unroll
+        for (int r = 0; r < V; ++r) {
+          const bool base = bm >> r & 1;
+          const int v = vb + r;
+          int b = base ? vbin(v) : 0;
+          append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
+          direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
+        }
+      }
+      if (a.topology) {
+#pragma unroll
+        for (int r = 0; r < V; ++r) {
+          const int v = vb + r;
+          bool topo = v < n && v != a.s && v != a.t;
+          int tb = topo ? vbin(v) : 0;
+          append_binned(1, topo, v, tb, a.ctrl->live + C_RNEXT, a.R, zero, a.rcap);
+        }
       }
     }
     level_flush(a.F0, zero);
@@ -819,6 +851,11 @@ struct Kern {
     lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
     const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
     const unsigned amask = (1u << C_ACTIVE) | (1u << C_REACHED) | (1u << C_DEPTH) | (1u << C_EHOLD);
+    if (a.trace) {  // trace: CTA 0's seeding pass done (phase-4 entry)
+      __syncthreads();
+      if (blockIdx.x == 0 && threadIdx.x == 0 && sy.trace_n < sy.trace_cap)
+        sy.trace[sy.trace_n++] = (4ull << 60) | ((globaltimer() - sy.t_last) & 0xFFFFFFFFull);
+    }
     grid_sync(a.ctrl, sy, fmask | (1u << C_BASES), rmask | amask, rmask | amask, PH_BFS);
     int E = 0;
     for (;;) {

@@ -105,6 +105,8 @@ def rounds_view(tag, st, g):
         waves = work[j:k]
         push_us = dt[j:k].sum() / 1e3
         rep = dt[k:k + 1].sum() / 1e3 if k < len(ph) and ph[k] == 2 else 0.0
+        if i in work0:
+            print(f"    seeding: CTA 0 busy {work0[i] / 1e3:.1f} us of {dt[i] / 1e3:.1f} us")
         ep = " ".join(f"{int(work[q])}:{dt[q] / 1e3:.0f}"
                       + (f"[{xs[q][0]}/{xs[q][1]}]" if q in xs else "") for q in range(i, j))
         print(f"    bfs epochs (items:us) {ep}")
