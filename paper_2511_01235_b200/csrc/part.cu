@@ -79,6 +79,9 @@ struct PeerTab {
   int *F[kMaxParts][2][2];  // [part][buffer][bin]
   int *R[kMaxParts][2];     // [part][bin]
   int *ctr[kMaxParts];
+  // own part only: vertices relabeled in the current round (the repair scope);
+  // rl_cnt[1] counts the hub rows (> kPartHuge slots) among them, listed in rl_hub
+  int *rl_list, *rl_flag, *rl_cnt, *rl_hub;
 };
 
 // device buffers of one part; the order here is the IPC export order
@@ -110,6 +113,7 @@ struct PartObj {
   int nheavy = 0;
   int *huge = nullptr;          // rows longer than kPartHuge
   int nhuge = 0;
+  int *rl_list = nullptr, *rl_flag = nullptr, *rl_cnt = nullptr, *rl_hub = nullptr;
   // hub push scratch (capacity nhuge)
   int *hub_list = nullptr, *hub_cnt = nullptr;
   unsigned long long *hub_best = nullptr;
@@ -155,7 +159,8 @@ PartObj::~PartObj() {
     if (buf[b]) cudaFree(buf[b]);
   for (void *p : {(void *)rev, (void *)orig, (void *)bases, (void *)src, (void *)heavy, (void *)huge, (void *)hub_list, (void *)hub_cnt,
                   (void *)hub_best, (void *)hub_taken, (void *)hub_snap, (void *)stat, (void *)err,
-                  (void *)slot_first, (void *)bslot, (void *)bbuf})
+                  (void *)slot_first, (void *)bslot, (void *)bbuf, (void *)rl_list,
+                  (void *)rl_flag, (void *)rl_cnt, (void *)rl_hub})
     if (p) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -393,6 +398,16 @@ __global__ void part_bfs_expand_kernel(PeerTab T, int me, int L, int cur, int cn
 // push wave (kernels.py:19-67): cooperative per row (warp or CTA), pushing
 // along every admissible slot at the minimum residual height in slot order
 // ---------------------------------------------------------------------------
+// u (own, local) was relabeled below n: its row is in this round's repair
+// scope.  A residual slot becomes steep (h(u) > h(v) + 1) only when its tail
+// is raised -- heads only rise within a round, and a push v -> u is decided on
+// h(v) > h(u) -- so the relabeled rows hold every slot the repair can find.
+__device__ __forceinline__ void part_relabeled(const PeerTab &T, int me, int u) {
+  if (atomicExch(T.rl_flag + u, 1) != 0) return;
+  if (T.off[me][u + 1] - T.off[me][u] > kPartHuge) T.rl_hub[atomicAdd(T.rl_cnt + 1, 1)] = u;
+  else T.rl_list[atomicAdd(T.rl_cnt, 1)] = u;
+}
+
 __device__ __forceinline__ void part_activate(const PeerTab &T, int v, unsigned stamp, int s, int t,
                                               int rcap) {
   if (v == s || v == t) return;
@@ -471,6 +486,7 @@ __device__ void part_push_row(const PeerTab &T, int me, int u, int kc, unsigned 
       if (tid == 0) {
         T.h[me][u] = hu;
         loc[PS_RELABEL]++;
+        if (hu < n) part_relabeled(T, me, u);
       }
       continue;
     }
@@ -609,6 +625,7 @@ __global__ void part_hub_push_kernel(PeerTab T, int me, const int *hub_list, con
         const int nh2 = best == ~0ull ? n : ((int)(best >> 32) + 1 > n ? n : (int)(best >> 32) + 1);
         T.h[me][u] = nh2;
         atomicAdd(stat + PS_RELABEL, 1ull);
+        if (nh2 < n) part_relabeled(T, me, u);
         if (nh2 < n) part_activate(T, T.lo[me] + u, stamp, s, t, rcap);
       }
       continue;
@@ -649,12 +666,15 @@ __global__ void part_hub_tail_kernel(PeerTab T, int me, const int *hub_list, con
   }
 }
 
-// repair (kernels.py:70-93) over every vertex that ran in the round
-__global__ void part_repair_kernel(PeerTab T, int me, int e0, int e1, const int *rev,
-                                   unsigned long long *stat) {
+// repair (kernels.py:70-93).  The reference repairs every vertex that ran in
+// the round; only relabeled rows can hold a steep residual slot (see
+// part_relabeled), so the scope is the round's relabel list -- on R-MAT 26
+// the round lists repeat hub rows every wave.  Clears the list's flags.
+__global__ void part_repair_kernel(PeerTab T, int me, const int *rev, unsigned long long *stat) {
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int gwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nr = *T.rl_cnt;
   unsigned long long reps = 0;
   auto slot = [&](int u, int hu, int i) {
     if (vol_ld(T.cf[me] + i) <= 0) return;
@@ -671,17 +691,31 @@ __global__ void part_repair_kernel(PeerTab T, int me, int e0, int e1, const int 
       }
     }
   };
-  for (int j = gwarp; j < e0; j += gwarps) {  // warp per light row
-    int u = T.R[me][0][j];
+  for (int j = gwarp; j < nr; j += gwarps) {  // warp per light row
+    int u = T.rl_list[j];
     int lo = T.off[me][u], hi = T.off[me][u + 1];
+    if (hi - lo > kPartHeavy) continue;
     int hu = vol_ld(T.h[me] + u);
     for (int i = lo + lane; i < hi; i += 32) slot(u, hu, i);
+    if (lane == 0) T.rl_flag[u] = 0;
   }
-  for (int j = blockIdx.x; j < e1; j += gridDim.x) {  // CTA per heavy row
-    int u = T.R[me][1][j];
+  for (int j = blockIdx.x; j < nr; j += gridDim.x) {  // CTA per heavy row
+    int u = T.rl_list[j];
     int lo = T.off[me][u], hi = T.off[me][u + 1];
+    if (hi - lo <= kPartHeavy) continue;
     int hu = vol_ld(T.h[me] + u);
     for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) slot(u, hu, i);
+    if (threadIdx.x == 0) T.rl_flag[u] = 0;
+  }
+  // hub rows (R-MAT 26: millions of slots): the whole grid per row
+  const int nh = T.rl_cnt[1];
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  for (int j = 0; j < nh; ++j) {
+    int u = T.rl_hub[j];
+    int lo = T.off[me][u], hi = T.off[me][u + 1];
+    int hu = vol_ld(T.h[me] + u);
+    for (int i = lo + gtid; i < hi; i += gthreads) slot(u, hu, i);
+    if (gtid == 0) T.rl_flag[u] = 0;
   }
   reps = warp_sum(reps);
   if (lane == 0 && reps) atomicAdd(stat + PS_REPAIR, reps);
@@ -1025,6 +1059,12 @@ static int part_build(PartObj &o, long long m, const int64_t *d_us, const int64_
   PCK(cudaMalloc(&o.heavy, sizeof(int) * NL));
   PCK(cudaMalloc(&o.src, sizeof(int) * SS));
   PCK(cudaMalloc(&o.huge, sizeof(int) * NL));
+  PCK(cudaMalloc(&o.rl_list, sizeof(int) * NL));
+  PCK(cudaMalloc(&o.rl_flag, sizeof(int) * NL));
+  PCK(cudaMalloc(&o.rl_cnt, 2 * sizeof(int)));
+  PCK(cudaMalloc(&o.rl_hub, sizeof(int) * NL));
+  PCK(cudaMemsetAsync(o.rl_flag, 0, sizeof(int) * NL, st));
+  PCK(cudaMemsetAsync(o.rl_cnt, 0, 2 * sizeof(int), st));
   PCK(cudaMalloc(&o.stat, sizeof(unsigned long long) * PS_N));
   PCK(cudaMalloc(&o.err, sizeof(long long) * PE_N));
   PCK(cudaMalloc(&o.slot_first, sizeof(int) * SS));
@@ -1139,6 +1179,10 @@ int mfx_part_create(int64_t n, int nparts, int rank, const int64_t *bounds, int6
     }
   }
   tab_set_self(o, rank);
+  o.tab.rl_list = o.rl_list;
+  o.tab.rl_flag = o.rl_flag;
+  o.tab.rl_cnt = o.rl_cnt;
+  o.tab.rl_hub = o.rl_hub;
   *out = P;
   return MFX_OK;
 }
@@ -1342,8 +1386,9 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
     }
     case MFX_PH_REPAIR: {  // args: e0, e1
       int e0 = (int)std::min<int64_t>(args[0], o.rcap), e1 = (int)std::min<int64_t>(args[1], o.rcap);
-      if (e0 + e1 > 0) {
-        part_repair_kernel<<<G, kPartBlock, 0, st>>>(T, me, e0, e1, o.rev, o.stat);
+      if (e0 + e1 > 0) {  // (the scope is the round's relabel list)
+        part_repair_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.rev, o.stat);
+        PCK(cudaMemsetAsync(o.rl_cnt, 0, 2 * sizeof(int), st));
         count_launch();
       }
       break;
