@@ -270,6 +270,7 @@ struct Kern {
   WarpQ *q;  // this warp's staging queues
   int gtid, gthreads, gwarp, gwarps, lane, wib;
   int swarp;  // warp index with CTAs fastest: thin lists spread over every SM
+  int *rctr;  // next-wave list counters: the global live ones, or CTA 0's own in tail mode
   int act_cnt;  // active discoveries counted by this lane in the current level
   long long *s_sink;  // per-CTA sum of excess pushed into the sink this round
   long long sink_acc; // this thread's share, not yet added to s_sink
@@ -313,6 +314,7 @@ struct Kern {
     gwarp = gtid >> 5;
     gwarps = gthreads >> 5;
     swarp = wib * (int)gridDim.x + (int)blockIdx.x;
+    rctr = a.ctrl->live + C_RNEXT;
     q = wq + wib;
     act_cnt = 0;
   }
@@ -967,7 +969,7 @@ struct Kern {
   __device__ __forceinline__ void activate(bool pred, int v, int b, unsigned stamp,
                                            const int *nbase) {
     if (pred) pred = atomicMax(a.mark + v, stamp) < stamp;
-    append_binned(1, pred, v, b, a.ctrl->live + C_RNEXT, a.R, nbase, a.rcap);
+    append_binned(1, pred, v, b, rctr, a.R, nbase, a.rcap);
   }
 
   // Thread per vertex (rows of <= kBin0Max slots).  The row (head, reverse
@@ -1095,8 +1097,8 @@ struct Kern {
         bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
         activate(p, vv[k], bb[k], stamp, nbase);
       } else {
-        append_binned(1, (pushed >> k & 1) && clm[k] < stamp, vv[k], bb[k], a.ctrl->live + C_RNEXT,
-                      a.R, nbase, a.rcap);
+        append_binned(1, (pushed >> k & 1) && clm[k] < stamp, vv[k], bb[k], rctr, a.R, nbase,
+                      a.rcap);
       }
     }
     if (Async) {
@@ -1446,7 +1448,10 @@ struct Kern {
                              int *nbase, long long *s_red) {
     __shared__ int s_cnt[NBIN];
     __shared__ int s_go;
+    __shared__ int s_rc[NBIN];  // this CTA alone appends: list counters in shared memory
     if (threadIdx.x == 0) sy.t_tail = globaltimer();
+    if (threadIdx.x < NBIN) s_rc[threadIdx.x] = 0;
+    rctr = s_rc;
     for (;;) {
       const unsigned next = ++stamp;
       __syncthreads();
@@ -1464,14 +1469,13 @@ struct Kern {
       }
       for (int j = base[1] + wib; j < lim[1]; j += kWarps)
         push_coop<32, false>(ldcg(a.R[1] + j), next, nbase, s_red);
-      stage_flush(1, a.ctrl->live + C_RNEXT, a.R[0], nbase[0], a.rcap);
-      __threadfence();  // this wave's list appends before the counts are read
-      __syncthreads();
+      stage_flush(1, s_rc, a.R[0], nbase[0], a.rcap);
+      __syncthreads();  // (also orders this CTA's list writes before the next wave reads them)
       ++waves;
       if (threadIdx.x == 0) {
         int tot = 0;
         for (int b = 0; b < NBIN; ++b) {
-          s_cnt[b] = ldcg(a.ctrl->live + C_RNEXT + b);
+          s_cnt[b] = s_rc[b];
           tot += s_cnt[b];
         }
         if (sy.trace && sy.trace_n < sy.trace_cap) {  // (CTA 0 holds the trace) phase-5 entry per wave
@@ -1484,9 +1488,11 @@ struct Kern {
                         s_cnt[3] == 0 &&
                         (waves < max_waves || (tot <= a.tail_items && waves < a.tail_cap)) &&
                         !(a.wave_time > 0 && globaltimer() > a.ctrl->wave_deadline);
-        if (go) {  // consumed here: the next wave appends from zero
-          for (int b = 0; b < NBIN; ++b) a.ctrl->live[C_RNEXT + b] = 0;
-          __threadfence();
+        // consumed here: the next wave appends from zero; else the pending
+        // wave's counts go to the live counters the grid barrier snapshots
+        for (int b = 0; b < NBIN; ++b) {
+          if (!go) a.ctrl->live[C_RNEXT + b] = s_rc[b];
+          s_rc[b] = 0;
         }
         s_go = go;
       }
@@ -1497,6 +1503,7 @@ struct Kern {
       }
       if (!s_go) break;
     }
+    rctr = a.ctrl->live + C_RNEXT;
     if (threadIdx.x == 0) {
       for (int b = 0; b < NBIN; ++b) a.ctrl->tail_base[b] = base[b];
       a.ctrl->tail_waves = waves;
