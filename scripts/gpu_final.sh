@@ -6,7 +6,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | cut -c1-300
 timeout 900 python bench.py --config C5 --steps 3 --warmup 1 > gpurun_out/bench_c5.log 2>&1; tail -1 gpurun_out/bench_c5.log | cut -c1-300
 for g in "grid --side 2048 --batch 10000 --batches 4" "rmat --scale 20 --batch 10000 --batches 3" "rmat --scale 20 --batch 100000 --batches 2" "road --side 1024 --batch 10000 --batches 2" "random --batch 1000 --batches 3"; do
-  X
+  name=$(echo $g | cut -d' ' -f1-5 | tr ' ' '_')
   timeout 300 python scripts/sweep.py --graph $g --knobs '' 'pp=1' > gpurun_out/final_${name}.log 2>&1
 done
 MFX_TIMEOUT_S=300 timeout 900 python scripts/sweep.py --graph road --side 4900 --batch 10000 --batches 2 --knobs '' > gpurun_out/final_C4.log 2>&1
