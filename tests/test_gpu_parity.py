@@ -354,3 +354,37 @@ def test_global_relabel_strict_retry_path(mf, name, monkeypatch):
     mf.saturate_source(st, g)
     mf.backward_bfs(st, g)
     assert sha(st.height) == rec["bfs_sat_sha"]
+
+
+SCHEDULES = [
+    {"MFX_BFS_LOCAL": "16"},                                   # short CTA-local BFS runs
+    {"MFX_BFS_LOCAL": "4096", "MFX_LQ_CAP": "64"},              # long runs, tiny ring (spills)
+    {"MFX_WAVE_TIME": "0"},                                    # no push-phase time budget
+    {"MFX_WAVE_TIME": "2", "MFX_TAIL_LOCAL": "0"},              # tight budget, no CTA-0 tails
+    {"MFX_TAIL_LOCAL": "4096", "MFX_BFS_LOCAL_MAX": "1"},       # large tails, grid-wide BFS
+]
+
+
+@pytest.mark.parametrize("env", SCHEDULES, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("name", ["grid64", "rmat12", "rand3"])
+def test_schedule_knobs_keep_reference_results(mf, name, env, monkeypatch):
+    """The schedule knobs change only the order of work:
+    global-relabel heights stay bit-exact and every chained flow stays the
+    reference's."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rec = G.rec[name]
+    n, us, vs, caps, s, t = instance(name)
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    st = mf.init_residuals(g, s, t)
+    mf.saturate_source(st, g)
+    mf.backward_bfs(st, g)
+    assert sha(st.height) == rec["bfs_sat_sha"]
+    res = mf.solve_static(g, s, t)
+    assert res.flow_value == rec["static_flow"] == res.certificate.cut_capacity
+    st = res.state
+    for entry in rec["chain"]:  # (the batches update g's capacities)
+        bu, bv, bc = chain_batch(g.src, g.adj, g.is_original, g.cap0, n, s, t, entry)
+        r = mf.solve_dynamic(st, g, mf.UpdateBatch(bu, bv, bc))
+        assert r.flow_value == entry["flow"] == r.certificate.cut_capacity, (name, entry["seed"])
+        st = r.state
