@@ -890,13 +890,23 @@ struct Kern {
       nocheck = (a.flags & 1) != 0 || ((a.flags & 2) != 0 && loc_ok);
       int *const *Fc = (E & 1) ? a.F1 : a.F0;
       Fn_ = (E & 1) ? a.F0 : a.F1;
-      // bin 0: thread per item (warp-uniform trip count).  Chunks of 32 go
-      // round-robin over the CTAs first (swarp), so a thin frontier, and with
-      // it the CTA-local sub-levels grown from it, spreads over every SM.
-      for (int j0 = swarp * 32; j0 < cnt[0]; j0 += gwarps * 32) {
-        int j = j0 + lane;
-        bool valid = j < cnt[0];
-        expand_item(valid, valid ? ldcg(Fc[0] + j) : 0);
+      // bin 0: thread per item (warp-uniform trip count).  Wide frontiers in
+      // chunks of 32 dealt over the CTAs first (swarp).
+      if (loc_ok) {
+        // thin frontier: dealt one item at a time over the CTAs, so every
+        // CTA's ring starts from an even share of it
+        const int tid_dealt = (lane * kWarps + wib) * (int)gridDim.x + (int)blockIdx.x;
+        for (int j0 = 0; j0 < cnt[0]; j0 += gthreads) {
+          int j = j0 + tid_dealt;
+          bool valid = j < cnt[0];
+          expand_item(valid, valid ? ldcg(Fc[0] + j) : 0);
+        }
+      } else {
+        for (int j0 = swarp * 32; j0 < cnt[0]; j0 += gwarps * 32) {
+          int j = j0 + lane;
+          bool valid = j < cnt[0];
+          expand_item(valid, valid ? ldcg(Fc[0] + j) : 0);
+        }
       }
       // bin 1: warp per row
       for (int j = swarp; j < cnt[1]; j += gwarps) {
