@@ -64,7 +64,8 @@ typedef struct {
     int32_t wave_add;      /*   + wave_add ((0, 0) -> (2, 4)); if max_waves == 0   */
     int32_t schedule;      /* push phase: 0 waves, 1 asynchronous work queue       */
     int32_t async_budget;  /* async: items per active vertex per round (0 -> 16)   */
-    int32_t bfs_local;     /* CTA-local BFS levels per grid barrier: 0 -> 128,      */
+    int32_t bfs_local;     /* CTA-local BFS levels per grid barrier: 0 -> auto (128 */
+                           /*   on short-row graphs, strict on long-row graphs),    */
                            /*   < 0 -> strict level-synchronous BFS                */
     int32_t bfs_local_max; /* ... used while the frontier <= this many items per   */
                            /*   CTA; 0 -> 64                                        */

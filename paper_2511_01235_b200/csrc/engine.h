@@ -101,7 +101,8 @@ struct SolveConfig {
   int tail_local = 256;   // push waves of <= tail_local short-row items run in CTA 0 alone
   int wave_time = -1;     // > 0: a push phase ends once it has run wave_time/8 x the last BFS's
                           //   time; 0 off; < 0 auto (10 on short-row graphs, off on long-row)
-  int bfs_local = 128;    // CTA-local BFS levels per grid barrier (0 = level-synchronous)
+  int bfs_local = -1;     // CTA-local BFS levels per grid barrier (0 = level-synchronous);
+                          //   < 0 auto: 128 on short-row graphs, 0 on long-row graphs
   int topology = 0;
   double timeout_s = 600.0;
   int blocks_per_sm = 0;

@@ -46,8 +46,8 @@ class SolverParams:
     round before the next global relabel, 0 = until the active list drains),
     ``timeout_s`` (device watchdog; 0 = $MFX_TIMEOUT_S or 600 s), ``blocks_per_sm`` (persistent grid),
     ``bfs_local`` (BFS levels a CTA may run ahead on its own between two grid
-    barriers of the global relabel; 0 = default 128, < 0 = strict
-    level-synchronous BFS).
+    barriers of the global relabel; 0 = auto: 128 on short-row graphs, strict
+    on long-row graphs; < 0 = strict level-synchronous BFS).
     """
 
     kernel_cycles: int = 0
