@@ -394,6 +394,56 @@ __global__ void part_bfs_expand_kernel(PeerTab T, int me, int L, int cur, int cn
   }
 }
 
+// Bottom-up step of the same level (direction-optimising BFS): every
+// unreached own vertex v scans its own row for a residual slot v -> u into
+// the frontier {h == L} and stops at the first one.  On R-MAT's wide middle
+// levels most unreached vertices hit within their first 32 slots, instead of
+// the frontier rows being scanned whole.  The heights are the same BFS
+// distances as the top-down step's; v is written by its own warp only.
+__global__ void part_bfs_bottomup_kernel(PeerTab T, int me, int nl, int L, int cur, int s, int t,
+                                         int forbidden, int rcap) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int gwarps = (gridDim.x * blockDim.x) >> 5;
+  const int n = T.n, lo_g = T.lo[me];
+  int *ctr = T.ctr[me];
+  for (int v0 = gwarp * 32; v0 < nl; v0 += gwarps * 32) {
+    const int vme = v0 + lane;
+    const bool open = vme < nl && vol_ld(T.h[me] + vme) == n && lo_g + vme != forbidden;
+    unsigned todo = __ballot_sync(0xffffffffu, open);
+    while (todo) {  // the warp scans each open vertex's row in turn
+      const int k = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int v = v0 + k;
+      const int lo = T.off[me][v], hi = T.off[me][v + 1];
+      bool found = false;
+      for (int i0 = lo; i0 < hi && !found; i0 += 32) {
+        const int i = i0 + lane;
+        bool hit = false;
+        if (i < hi && vol_ld(T.cf[me] + i) > 0) {
+          const int u = T.adj[me][i];
+          const int p = owner_of(T, u);
+          hit = vol_ld(T.h[p] + (u - T.lo[p])) == L;
+        }
+        found = __any_sync(0xffffffffu, hit);
+      }
+      if (found && lane == 0) {
+        T.h[me][v] = L + 1;
+        const int b = (hi - lo) > kPartHeavy ? 1 : 0;
+        T.F[me][cur ^ 1][b][atomicAdd(ctr + PC_FN0 + b, 1)] = v;
+        atomicAdd(ctr + PC_REACHED, 1);
+        const int g = lo_g + v;
+        if (g != s && g != t && vol_ld(T.ex[me] + v) > 0) {
+          atomicAdd(ctr + PC_ACTIVE, 1);
+          const int q = atomicAdd(ctr + PC_RT0 + b, 1);
+          if (q < rcap) T.R[me][b][q] = v;
+          else atomicExch(ctr + PC_OVF, 1);
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // push wave (kernels.py:19-67): cooperative per row (warp or CTA), pushing
 // along every admissible slot at the minimum residual height in slot order
@@ -1346,9 +1396,13 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
       count_launch();
       break;
     }
-    case MFX_PH_BFS_EXPAND: {  // args: L, cur, cnt0, cnt1, dyn
+    case MFX_PH_BFS_EXPAND: {  // args: L, cur, cnt0, cnt1, dyn, bottom-up
       int forbidden = args[4] ? o.s : -1;
-      if (args[2] + args[3] > 0) {
+      if (args[5]) {  // the level's frontier is {h == L} on every part
+        part_bfs_bottomup_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.nl, (int)args[0], (int)args[1],
+                                                           o.s, o.t, forbidden, o.rcap);
+        count_launch();
+      } else if (args[2] + args[3] > 0) {
         part_bfs_expand_kernel<<<G, kPartBlock, 0, st>>>(T, me, (int)args[0], (int)args[1],
                                                          (int)args[2], (int)args[3], o.s, o.t,
                                                          forbidden, o.rcap, o.huge, o.nhuge);

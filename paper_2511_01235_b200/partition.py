@@ -17,6 +17,7 @@ the reference (tests/test_gpu_partition.py).
 """
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -237,6 +238,9 @@ class PartitionedGraph:
         self.m_original = int(sum(self.info[r][3] for r in range(P)))
         self.stamp = 0
         self.terminated = False
+        # global relabel: levels whose frontier exceeds 1/div of the unreached
+        # vertices run bottom-up (0 = always top-down)
+        self.bottom_up_div = int(os.environ.get("MFX_PART_BOTTOM_UP", "16"))
 
     # -- plumbing ------------------------------------------------------------
     def _connect(self):
@@ -283,12 +287,17 @@ class PartitionedGraph:
         self.group.barrier()
         outs = self._phase_all(PH_SWAP)
         tot = int(self._sum(outs, (0, 1)).sum())
+        reached = int(self._sum(outs, (5,))[0])
         cur, L_ = 0, 0
         while tot > 0:
-            self._phase_all(PH_BFS_EXPAND, {r: (L_, cur, o[0], o[1], dyn) for r, o in outs.items()})
+            # direction-optimising: a level whose frontier holds more than
+            # 1/bottom_up_div of the unreached vertices runs bottom-up
+            up = int(self.bottom_up_div > 0 and tot * self.bottom_up_div > self.n - reached)
+            self._phase_all(PH_BFS_EXPAND, {r: (L_, cur, o[0], o[1], dyn, up) for r, o in outs.items()})
             self.group.barrier()
             outs = self._phase_all(PH_SWAP)
             tot = int(self._sum(outs, (0, 1)).sum())
+            reached = int(self._sum(outs, (5,))[0])
             cur ^= 1
             L_ += 1
         return outs, L_
