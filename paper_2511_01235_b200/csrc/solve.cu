@@ -54,10 +54,10 @@ struct SolveArgs {
   int async;         // asynchronous push phase (data mode only)
   int async_budget;  // items per initially active vertex before the next global relabel
   int *rdirty;       // NBIN used extents of the R lists (device, shared by states)
-  int bfs_local;     // CTA-local BFS sub-levels per grid barrier (0 = level-synchronous)
+  int bfs_local;     // labels a CTA's BFS ring may run ahead per grid barrier (0 = level-synchronous)
   int flags;         // bit 0: BFS relaxes with the atomic alone (no pre-load of h[v])
-  int bfs_local_max; // CTA-local sub-levels only when the frontier <= this many items per CTA
-  int lq_cap;        // CTA-local queue capacity per sub-level (<= kLQ; the rest spills)
+  int bfs_local_max; // the ring only when the frontier <= this many items per CTA
+  int lq_cap;        // CTA ring capacity is 2 x lq_cap (<= 2 kLQ; the rest spills)
   int tail_items;    // push: after the wave budget, continue while a wave holds <= this many
   int tail_cap;      //   ... up to this many waves in the round
   int coop_kc;       // push/relabel steps per visit of a cooperative (long) row
@@ -393,12 +393,13 @@ struct Kern {
   // =========================================================================
   // Frontier BFS over reverse residual slots with label-correcting relaxation
   // (atomicMin on h): between two grid barriers ("epoch") a CTA may expand
-  // its own discoveries for up to `local_levels` further BFS sub-levels,
-  // staged in a shared-memory queue and separated by __syncthreads only.
-  // Queue overflow and the last sub-level's discoveries go to the global next
-  // frontier (deduplicated per epoch by an epoch stamp).  Every lowering of
-  // h[v] schedules an expansion of v that re-reads h[v], so the fixpoint is
-  // the exact BFS distance (bit-exact with the reference's FIFO BFS, tested);
+  // its own discoveries, up to `local_levels` labels past the epoch's start
+  // depth, from a shared-memory work ring drained asynchronously by its warps
+  // (ring_drain: no barrier between BFS levels).  Ring overflow and the
+  // discoveries past the label cap go to the global next frontier
+  // (deduplicated per epoch by an epoch stamp).  Every lowering of h[v]
+  // schedules an expansion of v that re-reads h[v], so the fixpoint is the
+  // exact BFS distance (bit-exact with the reference's FIFO BFS, tested);
   // local_levels = 0 is the strict level-synchronous BFS.
   //
   // A discovery costs one atomic: the item carries a "first visit" flag
@@ -609,7 +610,7 @@ struct Kern {
     const bool heavy = valid && d > kBin0Max;
     if (__any_sync(FULL, heavy)) {
       // (only items of the grid-wide pass: those are spread evenly over the
-      // CTAs; a CTA's own sub-levels hand long rows to the whole grid)
+      // CTAs; a CTA's own ring hands long rows to the whole grid)
       bool mid = hq_ok && heavy && d <= kBin1Max, to_cta = false;
       unsigned m = __ballot_sync(FULL, mid);
       if (m) {  // warp-per-row rows: this CTA's warps, after this pass
@@ -880,10 +881,9 @@ struct Kern {
       rb_ = rb;
       bst = ++bstamp;
       xc = 0;
-      // CTA-local sub-levels only while the frontier is thin (latency-bound
-      // levels); wide levels stay grid-wide so no CTA serialises a share of
-      // them (R-MAT hubs)
-      // them (R-MAT hubs)
+      // the CTA ring only while the frontier is thin (latency-bound levels);
+      // wide levels stay grid-wide so no CTA serialises a share of them
+      // (R-MAT hubs)
       loc_ok = local_levels > 0 && tot <= a.bfs_local_max * (int)gridDim.x;
       lcap = sy.s_snap[C_DEPTH] + local_levels;  // (labels so far <= C_DEPTH)
       // flags bit 1: thin (latency-bound) epochs relax by atomic alone
