@@ -1814,6 +1814,17 @@ struct Kern {
         else a.heavy[atomicAdd(a.ctrl->live + C_HEAVY, 1)] = u;
         continue;
       }
+      if (hi - lo <= kBin0Max) {  // short rows: every load in flight together
+        int vv[kBin0Max], hv[kBin0Max];
+#pragma unroll
+        for (int k = 0; k < kBin0Max; ++k) vv[k] = lo + k < hi ? __ldg(a.adj + lo + k) : -1;
+#pragma unroll
+        for (int k = 0; k < kBin0Max; ++k) hv[k] = vv[k] >= 0 ? ldcg(a.h + vv[k]) : n;
+#pragma unroll
+        for (int k = 0; k < kBin0Max; ++k)
+          if (hv[k] != n) c += (long long)__ldg(a.cap0 + lo + k);
+        continue;
+      }
       for (int i = lo; i < hi; ++i)
         if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
     }
