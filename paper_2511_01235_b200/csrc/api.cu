@@ -662,6 +662,7 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   if (const char *mc = getenv("MFX_MAX_CTAS")) cfg.max_ctas = atoi(mc);
   if (const char *tl = getenv("MFX_TAIL_LOCAL")) cfg.tail_local = atoi(tl);
   if (const char *wt = getenv("MFX_WAVE_TIME")) cfg.wave_time = atoi(wt);
+  if (const char *rs = getenv("MFX_RING_SLEEP")) cfg.ring_sleep = atoi(rs);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;

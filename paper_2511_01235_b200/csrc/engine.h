@@ -99,6 +99,7 @@ struct SolveConfig {
   int walk_depth = 0;     // ... and the BFS is at least walk_depth levels deep
   int max_ctas = 0;       // cap on the persistent grid (0: every SM at full occupancy)
   int tail_local = 256;   // push waves of <= tail_local short-row items run in CTA 0 alone
+  int ring_sleep = 64;    // ns an idle warp sleeps between polls of its CTA's BFS ring
   int wave_time = -1;     // > 0: a push phase ends once it has run wave_time/8 x the last BFS's
                           //   time; 0 off; < 0 auto (10 on short-row graphs, off on long-row)
   int bfs_local = -1;     // CTA-local BFS levels per grid barrier (0 = level-synchronous);

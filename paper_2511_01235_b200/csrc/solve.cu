@@ -65,6 +65,7 @@ struct SolveArgs {
   int walk_depth;    // ... at least this many BFS levels deep
   int tail_local;    // push waves of <= this many items run in CTA 0 alone (0: off)
   int wave_time;     // push phase time budget, eighths of the last BFS's time (0: off)
+  int ring_sleep;    // ns an idle warp sleeps between polls of the BFS ring
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -479,7 +480,7 @@ struct Kern {
       c = __shfl_sync(FULL, c, 0);
       if (c == 0) {
         if (__shfl_sync(FULL, (int)fin, 0)) break;
-        __nanosleep(64);
+        if (a.ring_sleep > 0) __nanosleep(a.ring_sleep);
         continue;
       }
       h = __shfl_sync(FULL, h, 0);
@@ -2058,6 +2059,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.walk_depth = cfg.walk_depth;
   a.tail_local = cfg.tail_local;
   a.wave_time = cfg.wave_time;
+  a.ring_sleep = cfg.ring_sleep;
   a.coop_kc = cfg.coop_kc > 0 ? (cfg.coop_kc < cfg.kc ? cfg.coop_kc : cfg.kc) : cfg.kc;
   a.tail_cap = cfg.tail_cap;
   a.bmark = W.bmark;
