@@ -932,7 +932,12 @@ int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int
   cfg.what = WHAT_SOLVE;
   cfg.gate = T.ws.d_err;
   cfg.pushpull = true;
+  // the region-restricted relabels start from wide base sets (every overflowing
+  // A-side vertex); the CTA rings still pay there (C2: 126 -> 10 epochs/batch)
+  const int blm = cfg.bfs_local_max;
+  if (!(p && p->bfs_local_max > 0) && !getenv("MFX_BFS_LOCAL_MAX")) cfg.bfs_local_max = 1 << 20;
   CK(launch_solve(g->g, st->s, cfg, &launches));
+  cfg.bfs_local_max = blm;
   cfg.pushpull = false;  // final pass: overflow on the B side meets deficits on the A side
   cfg.reset_counters = false;
   cfg.dyn_bases = 1;
