@@ -79,11 +79,15 @@ def test_parts_are_slices_of_the_reference_layout(mf, part, name, P):
     pg.close()
 
 
+@pytest.mark.parametrize("bottom_up", ["0", "16", "1000000000"], ids=["topdown", "auto", "bottomup"])
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("name", ["rand3", "rand7", "grid64", "rmat12"])
-def test_global_relabel_heights_bit_exact(mf, part, name, P):
+def test_global_relabel_heights_bit_exact(mf, part, name, P, bottom_up, monkeypatch):
     """Saturated state -> backward BFS (bases {t}): heights equal the
-    reference's bfs_heights (golden sha over the whole height array)."""
+    reference's bfs_heights (golden sha over the whole height array), with
+    top-down levels only, the automatic direction switch, and bottom-up
+    levels throughout."""
+    monkeypatch.setenv("MFX_PART_BOTTOM_UP", bottom_up)
     n, us, vs, caps, s, t = instance(name)
     pg = part.PartitionedGraph(n, us, vs, caps, s, t, part.LocalGroup(P))
     pg.init_residuals()
