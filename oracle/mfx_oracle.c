@@ -17,9 +17,25 @@
  * which is the reference's `deterministic=True` schedule (solver.py:56-58,
  * 70-73).  Flow values are schedule independent (unique max-flow value).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
+
+/* Wall-clock cap for bounded CPU-baseline samples (bench.py cpu_baseline):
+ * push_rounds stops at a round boundary once it is past, and the solve
+ * reports status 5 ("capped") with the rounds it completed.  0 = no cap. */
+static double g_deadline = 0.0;
+
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+void orc_set_time_cap(double seconds) { g_deadline = seconds > 0 ? now_s() + seconds : 0.0; }
 
 /* ------------------------------------------------------------------ */
 /* radix sort of (uint64 key, int64 payload) pairs, LSD, 16-bit digits  */
@@ -367,7 +383,7 @@ int64_t orc_cut_capacity(int64_t n, const int64_t *offsets, const int64_t *adj,
 /* ------------------------------------------------------------------ */
 typedef struct {
     int64_t flow, cut, rounds, pushes, relabels, repairs;
-    int64_t status; /* 0 ok, 2 batch error kind in bad, 3 solver error */
+    int64_t status; /* 0 ok, 2 batch error kind in bad, 3 solver error, 5 time cap hit */
     int64_t bad;    /* batch error: kind*2^32 + index */
 } orc_result;
 
@@ -409,6 +425,7 @@ static void push_rounds(int64_t n, const int64_t *offsets, const int64_t *adj,
         orc_push_relabel(work, nw, offsets, adj, rev, cf, excess, height, n, kc, counts);
         r->repairs += orc_remove_invalid(work, nw, offsets, adj, rev, cf, excess, height);
         r->rounds++;
+        if (g_deadline > 0 && now_s() > g_deadline) { r->status = 5; break; }
     }
     r->pushes += counts[0];
     r->relabels += counts[1];
@@ -428,6 +445,7 @@ void orc_solve_static(int64_t n, const int64_t *offsets, const int64_t *adj,
     memset(height, 0, sizeof(int64_t) * (size_t)n);
     orc_saturate_source(s, offsets, adj, rev, cf, excess);
     push_rounds(n, offsets, adj, rev, cf, excess, height, s, t, kc, 0, topology, r);
+    if (r->status == 5) return;
     r->flow = excess[t];
     r->cut = orc_cut_capacity(n, offsets, adj, cap0, is_original, excess, height, s, t);
     if (r->cut != r->flow) r->status = 3;
@@ -452,9 +470,78 @@ void orc_solve_dynamic(int64_t n, const int64_t *offsets, const int64_t *adj,
     orc_recompute_excess(n, offsets, rev, cf, cap0, excess);
     orc_saturate_source(s, offsets, adj, rev, cf, excess);
     push_rounds(n, offsets, adj, rev, cf, excess, height, s, t, kc, 1, topology, r);
+    if (r->status == 5) return;
     int64_t flow = 0;
     for (int64_t v = 0; v < n; v++) if (height[v] == 0) flow += excess[v];
     r->flow = flow;
     r->cut = orc_cut_capacity(n, offsets, adj, cap0, is_original, excess, height, s, t);
     if (r->cut != r->flow) r->status = 3;
+}
+
+/* dinic_maxflow, oracle.py:20-55 + _augment_in_level_graph oracle.py:58-84,
+ * restated on the Bi-CSR residual layout: the reference builds its own
+ * per-vertex [head, residual, reverse] lists from the edge list, and a
+ * Bi-CSR slot pair (i, rev i) with cf = cap0 is exactly that residual
+ * graph with parallel edges merged.  Level graph by BFS from s over cf > 0;
+ * blocking flow by iterative current-arc DFS, dead ends get level -1.
+ * Leaves the final residuals in cf (cf = cap0 on entry is the caller's job)
+ * and returns the flow value.  Test infrastructure: it produces terminated
+ * states for the capped CPU baselines and checks flow values. */
+int64_t orc_dinic(int64_t n, const int64_t *offsets, const int64_t *adj, const int64_t *rev,
+                  int64_t *cf, int64_t s, int64_t t)
+{
+    if (s == t) return -1;
+    int64_t *level = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *it = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *path = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1)); /* slots */
+    int64_t total = 0;
+    for (;;) {
+        for (int64_t v = 0; v < n; v++) level[v] = -1;
+        level[s] = 0;
+        int64_t head = 0, tail = 0;
+        queue[tail++] = s;
+        while (head < tail) {
+            int64_t u = queue[head++];
+            for (int64_t i = offsets[u]; i < offsets[u + 1]; i++) {
+                int64_t v = adj[i];
+                if (cf[i] > 0 && level[v] < 0) { level[v] = level[u] + 1; queue[tail++] = v; }
+            }
+        }
+        if (level[t] < 0) break;
+        for (int64_t v = 0; v < n; v++) it[v] = offsets[v];
+        for (;;) { /* augmenting paths inside the level graph */
+            int64_t depth = 0, u = s, pushed = 0;
+            for (;;) {
+                if (u == t) {
+                    int64_t amt = INT64_MAX;
+                    for (int64_t d = 0; d < depth; d++) if (cf[path[d]] < amt) amt = cf[path[d]];
+                    for (int64_t d = 0; d < depth; d++) { cf[path[d]] -= amt; cf[rev[path[d]]] += amt; }
+                    pushed = amt;
+                    break;
+                }
+                int advanced = 0;
+                while (it[u] < offsets[u + 1]) {
+                    int64_t i = it[u];
+                    if (cf[i] > 0 && level[adj[i]] == level[u] + 1) {
+                        path[depth++] = i;
+                        u = adj[i];
+                        advanced = 1;
+                        break;
+                    }
+                    it[u]++;
+                }
+                if (!advanced) {
+                    level[u] = -1;
+                    if (depth == 0) break;
+                    u = (depth >= 2) ? adj[path[depth - 2]] : s;
+                    depth--;
+                }
+            }
+            if (pushed == 0) break;
+            total += pushed;
+        }
+    }
+    free(level); free(queue); free(it); free(path);
+    return total;
 }
