@@ -1,25 +1,54 @@
-"""Benchmark: dynamic max-flow ms per update batch (vs a GPU static re-solve)
-and static max-flow edges/s on config C2 of BASELINE.json (2048x2048
-4-neighbour grid with terminal edges, batches of 10,000 mixed updates).
+"""Benchmark for BASELINE.json's metric: dynamic max-flow ms per update batch
+(against a GPU static re-solve) and static max-flow edges/s.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config auto|C1|C2|C3|C4|C5]
 
-A step = one chained dynamic batch through solve_dynamic.  ``value`` times K
-steps with the batches already resident in HBM (CUDA events on the engine's
-stream, max over ranks); ``e2e`` times K further chained steps through the
-public Python API from pinned host arrays (H2D of the batch and D2H of the
-result inside the timed region).  ``--impl reference`` runs the unmodified
-reference package (baseline/_ref, numba) on the host cores instead, or the C
-oracle port when the reference is not installed.
+Headline (N = 1, ``--config auto``): C4, the largest single-GPU config of
+BASELINE.json -- a road-shaped lattice of 24,010,000 vertices / 58,104,530
+directed edges, corner to corner, chained batches of 10,000 mixed updates.
+C1-C3 are the same measurement on the other single-GPU configs.
 
-N > 1: one process per GPU (torchrun); the grid config does not partition,
-so every rank runs an independent replica ("replicas only").
+A step = one chained batch through solve_dynamic:
+
+* ``value``: K steps with the batches resident in HBM, CUDA events on the
+  engine's stream, max over ranks.
+* ``e2e``: the SAME K batches replayed from a device snapshot of the state
+  and capacities taken before the timed region, through the public API
+  ``solve_dynamic(st, g, UpdateBatch(...))`` from pinned host arrays (H2D of
+  the batch and D2H of the result inside the timed region).  Its flows must
+  equal the ``value`` leg's.
+* ``roofline``: the persistent solve kernel (one launch per batch):
+  algorithmic bytes counted on the device / its event-timed duration,
+  against MEASURED_PEAKS.json; ``traffic`` = ncu DRAM bytes of the same
+  kernel on the same config and batch index, read from
+  profiles/ncu_<config>_solve_kernel.json only when that capture was taken
+  from the current kernel sources (hash), else null.
+* ``cpu_baseline``: the C oracle port (1 thread) on one batch of the same
+  workload continuing from the GPU's terminated state, wall-clock capped
+  (a capped sample is a lower bound and says so).
+
+N > 1 (torchrun, or ``--gpus N`` which re-launches itself under torchrun):
+the one multi-GPU path of the north star, C5 -- R-MAT vertex-range
+partitioned, one part per rank (``--scale``, default 26).  ``--config C5`` at
+N = 1 runs the same partition code with ``--parts`` parts on one GPU.
+
+``--impl reference`` runs the unmodified reference package
+(baseline/_ref, numba, all host threads) on the same config: for C4 its
+static solve is infeasible (thousands of O(n) rounds), so its start state is
+a maximum flow from the oracle's Dinic restatement (not timed) and each
+batch is capped through the reference's own ``instrument`` hook; a capped
+batch reports its elapsed time as a lower bound.  A scaled road anchor
+(512^2, ``threads=nproc`` and ``threads=1``) runs to completion beside it.
 """
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -30,9 +59,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "dynamic maxflow ms per update batch vs static recompute; static maxflow edges/s"
-CONFIG_NAME = "C2"
-GRID_W = GRID_H = 2048
-BATCH = 10_000
+
+# config -> (generator, args, batch size, description)
+CONFIGS = {
+    "C1": ("random", (10000, 100000), 1000,
+           "C1: random graph 10K vertices / 100K edges (reference random_graph, seed 0)"),
+    "C2": ("grid", (2048,), 10000,
+           "C2: 2048x2048 4-neighbour grid + terminal edge per pixel (caps U[1,100], seed 0)"),
+    "C3": ("rmat", (20,), 10000,
+           "C3: R-MAT scale 20 ef 16 (0.57,0.19,0.19), caps U[1,100], seed 0"),
+    "C4": ("road", (4900,), 10000,
+           "C4: road-shaped lattice 4900x4900 (every row link, vertical links p=0.21, "
+           "column 0 kept), both directions, caps U[1,100], corner to corner"),
+}
 
 
 def parse():
@@ -41,66 +80,94 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--grid", type=int, default=GRID_W, help="grid side (C2: 2048)")
-    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--config", default="auto", choices=["auto", "C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--batch", type=int, default=0, help="updates per batch (0: the config's)")
+    ap.add_argument("--side", type=int, default=0, help="grid/road side override (scaled runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=150.0)
-    ap.add_argument("--max-waves", type=int, default=0)
+    ap.add_argument("--cpu-cap-s", type=float, default=30.0, help="cap of the cpu_baseline sample")
+    ap.add_argument("--ref-cap-s", type=float, default=120.0,
+                    help="reference arm: wall-clock cap per batch")
+    ap.add_argument("--ref-budget-s", type=float, default=240.0,
+                    help="reference arm: wall-clock budget for the chained batches")
     ap.add_argument("--profile", action="store_true",
-                    help="short run for ncu: no e2e / cpu baseline / re-solve legs")
-    ap.add_argument("--config", default="C2", choices=["C2", "C5"],
-                    help="C2: single-GPU headline; C5: R-MAT 26 vertex-range partitioned "
-                         "(one part per rank under torchrun, --parts parts on one GPU otherwise)")
+                    help="ncu mode: static solve, W warm-up batches, then K batches inside the "
+                         "NVTX range 'timed' (no e2e / re-solve / cpu legs)")
     ap.add_argument("--scale", type=int, default=26, help="C5 R-MAT scale")
     ap.add_argument("--parts", type=int, default=4, help="C5 parts when run as one process")
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------------------
-def dist_setup(args):
+# launch / ranks
+# ---------------------------------------------------------------------------
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_relaunch(args):
+    """``--gpus N`` outside torchrun: re-run this script as N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def dist_setup():
+    """One process per GPU.  NCCL when every rank has its own GPU; gloo
+    when ranks share devices (one-GPU boxes) or there is no GPU."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    pg = None
+    pg, device, backend = None, 0, None
+    import torch
+    ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if ngpu:
+        device = local % ngpu
     if world > 1:
-        import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
-            torch.cuda.set_device(local)
+        backend = "nccl" if ngpu >= world else "gloo"
+        if ngpu:
+            torch.cuda.set_device(device)
         dist.init_process_group(backend=backend)
         pg = dist
-    return rank, world, local, pg
+    return rank, world, device, pg, backend
 
 
-def barrier(pg, local):
-    if pg is not None:
-        import torch
-        if torch.cuda.is_available():
-            pg.barrier(device_ids=[local])
-        else:
-            pg.barrier()
+def barrier(pg, backend, device):
+    if pg is None:
+        return
+    if backend == "nccl":
+        pg.barrier(device_ids=[device])
+    else:
+        pg.barrier()
 
 
-def max_over_ranks(pg, x: float, local: int) -> float:
+def max_over_ranks(pg, backend, x: float, device: int) -> float:
     if pg is None:
         return x
     import torch
-    dev = f"cuda:{local}" if torch.cuda.is_available() else "cpu"
+    dev = f"cuda:{device}" if backend == "nccl" else "cpu"
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     pg.all_reduce(t, op=pg.ReduceOp.MAX)
     return float(t.item())
 
 
 class ClockSampler:
-    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the
-    timed region."""
+    """NVML SM clock and throttle-reason sampling during the timed region
+    (the profiling recipe's clocks line)."""
+
+    NAMES = {"applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+             "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+             "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
-        self.reasons = set()
+        self.samples, self.reasons = [], set()
         self._stop = threading.Event()
         self._t = None
         self.max_mhz = None
@@ -111,24 +178,16 @@ class ClockSampler:
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            names = {
-                "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
-                "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
-                "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
-                "display_clock_setting": 0x100,
-            }
 
             def run():
                 while not self._stop.is_set():
                     try:
                         self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
                         r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        for k, bit in names.items():
-                            if r & bit and k != "gpu_idle":
-                                self.reasons.add(k)
+                        self.reasons.update(k for k, b in self.NAMES.items() if r & b)
                     except Exception:
                         pass
-                    self._stop.wait(0.05)
+                    self._stop.wait(0.02)
 
             self._t = threading.Thread(target=run, daemon=True)
             self._t.start()
@@ -142,153 +201,190 @@ class ClockSampler:
             self._t.join()
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
         busy = [s for s in self.samples if s > 0]
         return {"sm_mhz": float(statistics.median(busy)) if busy else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
 
 
+# ---------------------------------------------------------------------------
+# evidence helpers
+# ---------------------------------------------------------------------------
 def load_peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def kernel_source_hash() -> str:
+    """Hash of everything that determines the solve kernel's code."""
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2511_01235_b200", "csrc")
+    for name in sorted(os.listdir(csrc)):
+        if name.endswith((".cu", ".cuh", ".h", ".cpp")) or name == "Makefile":
+            with open(os.path.join(csrc, name), "rb") as fh:
+                h.update(name.encode() + b"\0" + fh.read())
+    with open(os.path.join(ROOT, "include", "mfx.h"), "rb") as fh:
+        h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def load_traffic(config: str):
+    """ncu DRAM bytes per solve-kernel launch for this config, valid only
+    if captured from the current kernel sources."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{config}_solve_kernel.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
     except Exception:
-        return 6650.0, "fallback"
-
-
-def load_traffic():
-    """dram bytes per solve-kernel launch from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_solve_kernel.json")
-    try:
-        with open(path) as fh:
-            d = json.load(fh)
-        return d
-    except Exception:
-        return None
+        return None, "no ncu capture for this config"
+    if d.get("src_hash") != kernel_source_hash():
+        return None, f"stale ncu capture ({os.path.basename(path)} src_hash {d.get('src_hash')})"
+    return d, os.path.relpath(path, ROOT)
 
 
 # ---------------------------------------------------------------------------
-def make_instance(side):
+# workloads
+# ---------------------------------------------------------------------------
+def make_instance(cfg: str, side: int = 0):
     from paper_2511_01235_b200 import gen
-    us, vs, caps, s, t = gen.grid_graph(side, side, seed=0)
-    return side * side + 2, us, vs, caps, s, t
+    kind, a, _, _ = CONFIGS[cfg]
+    if kind == "random":
+        us, vs, caps, s, t = gen.random_edges(*a, seed=0)
+        return a[0], us, vs, caps, s, t
+    if kind == "grid":
+        w = side or a[0]
+        us, vs, caps, s, t = gen.grid_graph(w, w, seed=0)
+        return w * w + 2, us, vs, caps, s, t
+    if kind == "rmat":
+        us, vs, caps, s, t = gen.rmat_graph(a[0], 16, seed=0)
+        return 1 << a[0], us, vs, caps, s, t
+    w = side or a[0]
+    us, vs, caps, s, t = gen.road_graph(w, w, seed=0, p_vert=0.21)
+    return w * w, us, vs, caps, s, t
 
 
 def make_chain(n, el_us, el_vs, el_caps, s, t, count, k, seed0):
-    """`count` chained batches: each drawn from the capacities left by the
-    previous one (fast_batch: reference generate_batch semantics)."""
+    """``count`` chained mixed batches, each drawn from the capacities the
+    previous one left (gen.sparse_batch: reference generate_batch law)."""
     from paper_2511_01235_b200 import gen
-    caps = el_caps.copy()
+    caps = np.array(el_caps, np.int64, copy=True)
     out = []
     for i in range(count):
-        bu, bv, bc, pick = gen.fast_batch(n, el_us, el_vs, caps, s, t, k, "mixed", seed0 + i)
+        bu, bv, bc, pick = gen.sparse_batch(n, el_us, el_vs, caps, s, t, k, "mixed", seed0 + i)
         caps[pick] = bc
         out.append((bu, bv, bc))
     return out
 
 
-def bench_ours(args, rank, world, local, pg):
+def workload_block(args, cfg, k, world):
+    desc = CONFIGS[cfg][3]
+    if args.side:
+        desc += f" [scaled: side {args.side}]"
+    return {"workload": f"{desc}; chained batches of {k} mixed updates (bias 10, "
+                        f"gen.sparse_batch = reference generate_batch law)",
+            "config": cfg, "batch_updates": k,
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (Bi-CSR + state > 126 MB)" if cfg != "C1"
+            else "graph fits in L2 (C1: ~3 MB); no flush"}
+
+
+# ---------------------------------------------------------------------------
+# our arm, single GPU configs
+# ---------------------------------------------------------------------------
+def bench_ours(args, cfg, rank, world, dev, pg, backend):
+    import ctypes
+
     import torch
 
     import paper_2511_01235_b200 as mfx
     from paper_2511_01235_b200 import _lib
 
-    dev = local
-    torch.cuda.set_device(dev)
-    n, us, vs, caps, s, t = make_instance(args.grid)
-    # graph build (not part of the metric, reported)
+    L = _lib.load()
+    k = args.batch or CONFIGS[cfg][2]
+    n, us, vs, caps, s, t = make_instance(cfg, args.side)
     t0 = time.perf_counter()
     g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps), device=dev)
     build_s = time.perf_counter() - t0
-    params = mfx.SolverParams(max_waves=args.max_waves)
-    # static solve: warm once, then time
-    res = mfx.solve_static(g, s, t, params)
-    static_runs = []
-    for _ in range(1 if args.profile else 2):
-        res = mfx.solve_static(g, s, t, params)
-        static_runs.append(res.device["ms_total"])
-    static_ms = min(static_runs)
-    static_flow = res.flow_value
-    m_orig = g.m_original
+    del us, vs, caps
+    params = mfx.SolverParams()
+    res = mfx.solve_static(g, s, t, params)  # warm
+    static_ms = [res.device["ms_total"]]
+    if not args.profile:
+        for _ in range(2):
+            res = mfx.solve_static(g, s, t, params)
+            static_ms.append(res.device["ms_total"])
     st = res.state
     el = g.to_edge_list()
     W, K = args.warmup, args.steps
-    chain = make_chain(n, el.us, el.vs, el.caps, s, t, W + 2 * K, args.batch, 1000 * rank)
-    # device-resident batches for the `value` leg
-    dbat = []
-    for bu, bv, bc in chain[:W + K]:
-        dbat.append(tuple(torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev}")
-                          for a in (bu, bv, bc)))
+    chain = make_chain(n, el.us, el.vs, el.caps, s, t, W + K, k, 1000 * rank)
+    dbat = [tuple(torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev}") for a in b)
+            for b in chain]
     torch.cuda.synchronize()
-    stream = torch.cuda.ExternalStream(_lib.load().mfx_graph_stream(g.handle), device=dev)
+    stream = torch.cuda.ExternalStream(L.mfx_graph_stream(g.handle), device=dev)
     for i in range(W):
         bu, bv, bc = dbat[i]
-        mfx.solve_dynamic_device(st, g, bu.numel(), bu.data_ptr(), bv.data_ptr(), bc.data_ptr(), params)
+        mfx.solve_dynamic_device(st, g, k, bu.data_ptr(), bv.data_ptr(), bc.data_ptr(), params)
+    # snapshot for the e2e replay of the same batches
+    g_snap, st_snap = (None, None) if args.profile else (g.copy(), st.copy())
+    torch.cuda.synchronize()
 
-    flows, rounds, solve_ms, bytes_alg, pushes, levels, waves = [], [], [], [], [], [], []
+    rows = []
     launches0 = mfx.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
-        barrier(pg, local)
+        barrier(pg, backend, dev)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("timed")
         ev0.record(stream)
         for i in range(W, W + K):
             bu, bv, bc = dbat[i]
-            r = mfx.solve_dynamic_device(st, g, bu.numel(), bu.data_ptr(), bv.data_ptr(),
-                                         bc.data_ptr(), params)
-            flows.append(r.flow_value)
-            rounds.append(r.rounds)
-            solve_ms.append(r.device["ms_solve"])
-            bytes_alg.append(r.device["bytes_alg"])
-            pushes.append(r.pushes)
-            levels.append(r.device["bfs_levels"])
-            waves.append(r.device["waves"])
+            r = mfx.solve_dynamic_device(st, g, k, bu.data_ptr(), bv.data_ptr(), bc.data_ptr(),
+                                         params)
+            d = r.device
+            rows.append((r.flow_value, r.rounds, d["ms_solve"], d["bytes_alg"], d["bfs_epochs"],
+                         d["waves"], d["bfs_levels"], d["ms_total"]))
         ev1.record(stream)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
-        barrier(pg, local)
+        barrier(pg, backend, dev)
     launches = mfx.launch_count() - launches0
-    elapsed_ms = ev0.elapsed_time(ev1)
-    elapsed_ms = max_over_ranks(pg, elapsed_ms, local)
-    ms_per_step = elapsed_ms / K
-
-    out = {"elapsed_ms": elapsed_ms, "ms_per_step": ms_per_step, "flows": flows,
-           "rounds": rounds, "solve_ms": solve_ms, "bytes_alg": bytes_alg, "launches": launches,
-           "clocks": clk.summary(), "static_ms": static_ms, "static_flow": static_flow,
-           "m_orig": m_orig, "n": n, "S": g.m, "build_s": build_s, "pushes": pushes,
-           "levels": levels, "waves": waves, "cap_bytes": g.cap_bytes}
+    elapsed = max_over_ranks(pg, backend, ev0.elapsed_time(ev1), dev)
+    a = np.array(rows, dtype=np.float64)
+    out = {"cfg": cfg, "k": k, "n": n, "S": g.m, "m_orig": g.m_original, "build_s": build_s,
+           "static_ms": min(static_ms), "static_flow": res.flow_value,
+           "static_rounds": res.rounds, "elapsed_ms": elapsed, "flows": [int(x) for x in a[:, 0]],
+           "rounds": a[:, 1], "solve_ms": a[:, 2], "bytes_alg": a[:, 3], "epochs": a[:, 4],
+           "waves": a[:, 5], "levels": a[:, 6], "launches": launches, "clocks": clk.summary(),
+           "cap_bytes": g.cap_bytes}
     if args.profile:
         return out
 
-    # ---- e2e: public API, pinned host batches, H2D + D2H in the timed region
+    # ---- e2e: same batches, public API, pinned host memory, from the snapshot
     pinned = []
-    for bu, bv, bc in chain[W + K:]:
+    for bu, bv, bc in chain[W:]:
         hb = [mfx.HostBuffer(bu.size) for _ in range(3)]
-        for h, a in zip(hb, (bu, bv, bc)):
-            h.array[:] = a
+        for h, x in zip(hb, (bu, bv, bc)):
+            h.array[:] = x
         pinned.append(hb)
-    barrier(pg, local)
+    barrier(pg, backend, dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e2e_flows = []
     for hb in pinned:
-        r = mfx.solve_dynamic(st, g, mfx.UpdateBatch(hb[0].array, hb[1].array, hb[2].array), params)
-        e2e_flows.append(r.flow_value)  # D2H of the result struct happened inside the call
+        r = mfx.solve_dynamic(st_snap, g_snap, mfx.UpdateBatch(hb[0].array, hb[1].array,
+                                                               hb[2].array), params)
+        e2e_flows.append(r.flow_value)
     torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3
-    barrier(pg, local)
-    e2e_ms = max_over_ranks(pg, e2e_ms, local)
-    out["e2e_ms_per_step"] = e2e_ms / K
-    import ctypes
+    e2e_ms = max_over_ranks(pg, backend, (time.perf_counter() - t0) * 1e3, dev)
+    assert e2e_flows == out["flows"], (e2e_flows, out["flows"])
     h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
-    _lib.load().mfx_transfer_bytes(args.batch, ctypes.byref(h2d), ctypes.byref(d2h))
-    out["e2e_h2d"] = int(h2d.value)  # batch (us, vs, new caps) int64
-    out["e2e_d2h"] = int(d2h.value)  # result control block + batch error block
-    out["e2e_flows"] = e2e_flows
+    L.mfx_transfer_bytes(k, ctypes.byref(h2d), ctypes.byref(d2h))
+    out.update(e2e_ms_per_step=e2e_ms / K, e2e_h2d=int(h2d.value), e2e_d2h=int(d2h.value))
+    del g_snap, st_snap
 
     # ---- GPU static re-solve on the updated capacities (the comparison point)
     st2 = mfx.init_residuals(g, s, t)
@@ -296,146 +392,131 @@ def bench_ours(args, rank, world, local, pg):
     for _ in range(2):
         rr = mfx.resolve_static(g, st2, params)
         rs.append(rr.device["ms_total"])
-    out["resolve_ms"] = min(rs)
-    out["resolve_flow"] = rr.flow_value
-    assert rr.flow_value == e2e_flows[-1], (rr.flow_value, e2e_flows[-1])
-    rep = mfx.verify_gpu(st, g, e2e_flows[-1])
+    assert rr.flow_value == out["flows"][-1], (rr.flow_value, out["flows"][-1])
+    out.update(resolve_ms=min(rs), resolve_flow=rr.flow_value)
+    rep = mfx.verify_gpu(st, g, out["flows"][-1])
     assert rep.ok, rep.problems
-    out["verified"] = True
+    del st2
 
-    # ---- CPU baseline sample: the C oracle (1 thread), one batch of the same
-    # workload from the GPU's terminated state (rank 0, N = 1 only)
+    # ---- grid-barrier cost, for the latency floor of the solve kernel
+    ns = ctypes.c_double()
+    _lib.check(L.mfx_bench_barrier(g.handle, st.handle, 2000, 0, ctypes.byref(ns)))
+    out["barrier_ns"] = ns.value
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_sample(g, st, s, t, n, chain, args)
+        out["cpu_baseline"] = cpu_sample(g, st, s, t, n, k, args)
     return out
 
 
-def cpu_sample(g, st, s, t, n, chain, args):
+def cpu_sample(g, st, s, t, n, k, args):
+    """The C oracle (test infrastructure, 1 thread) on one batch of the same
+    workload, from the GPU's terminated state, capped at --cpu-cap-s."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     og = O.OracleGraph(n, g.m, g.offsets.copy(), g.adj.copy(), g.src.copy(), g.rev.copy(),
                        g.cap0.copy(), g.is_original.copy(), (0, 0, 0))
-    ost = O.OracleState(st.cf.copy(), st.excess.copy(), st.height.copy(), s, t)
-    from paper_2511_01235_b200 import gen
-    el_caps = og.cap0[og.is_original]
-    bu, bv, bc, _ = gen.fast_batch(n, og.src[og.is_original], og.adj[og.is_original], el_caps, s,
-                                   t, args.batch, "mixed", 99991)
+    ost = O.OracleState(st.cf.astype(np.int64), st.excess.astype(np.int64),
+                        st.height.astype(np.int64), s, t)
+    keep = og.is_original
+    (bu, bv, bc), = make_chain(n, og.src[keep], og.adj[keep], og.cap0[keep], s, t, 1, k, 99991)
+    O.set_time_cap(args.cpu_cap_s)
     t0 = time.perf_counter()
     r = O.solve_dynamic(og, ost, bu, bv, bc)
     dt = time.perf_counter() - t0
-    return {"value": dt * 1e3, "unit": "ms/batch", "cores": 1, "kind": "port",
-            "sample": f"1 batch of {args.batch} mixed updates on the {args.grid}^2 grid (C oracle, "
-                      f"deterministic schedule) continuing from the GPU's terminated state; "
-                      f"flow {r.flow}, {r.rounds} rounds"}
+    O.set_time_cap(0)
+    capped = r.status == 5
+    return {"value": round(dt * 1e3, 1), "unit": "ms/batch", "cores": 1, "kind": "port",
+            "lower_bound": capped,
+            "sample": (f"1 batch of {k} mixed updates (C oracle: deterministic single-thread "
+                       f"restatement of the reference rounds) from the GPU's terminated state; "
+                       + (f"capped at {args.cpu_cap_s:.0f} s after {r.rounds} rounds "
+                          f"(value is a lower bound)" if capped else
+                          f"flow {r.flow}, {r.rounds} rounds"))}
 
 
-# ---------------------------------------------------------------------------
-def bench_reference(args, rank, world):
-    """Reference arm: the unmodified reference package on the host cores."""
-    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
-    cores = os.cpu_count() or 1
-    try:
-        import dynmaxflow as ref
-        kind = "reference"
-    except Exception:
-        ref = None
-        kind = "port"
-    n, us, vs, caps, s, t = make_instance(args.grid)
+def emit_ours(args, out, world):
     K = args.steps
-    if ref is not None:
-        params = ref.SolverParams(threads=cores)
-        # warm the numba JIT on a tiny instance (reference bench protocol)
-        tg, ts, tt = ref.random_graph(50, 300, seed=0)
-        ref.solve_static(ref.build_bicsr(tg), ts, tt, params)
-        csr = ref.build_bicsr(ref.EdgeListGraph(n, us, vs, caps))
-        t0 = time.perf_counter()
-        prior = ref.solve_static(csr, s, t, params)
-        static_s = time.perf_counter() - t0
-        el = csr.to_edge_list()
-        chain = make_chain(n, el.us, el.vs, el.caps, s, t, K, args.batch, 0)
-        st, g = prior.state, csr
-        times = []
-        tb = time.perf_counter()
-        for bu, bv, bc in chain:
-            t0 = time.perf_counter()
-            r = ref.solve_dynamic(st, g, ref.UpdateBatch(bu, bv, bc), params)
-            times.append(time.perf_counter() - t0)
-            st, g = r.state, r.graph
-            if time.perf_counter() - tb > args.cpu_budget_s:
-                break
-        m_orig = csr.m_original
-    else:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import oracle as O
-        og = O.build_bicsr(n, us, vs, caps)
-        t0 = time.perf_counter()
-        _, ost = O.solve_static(og, s, t)
-        static_s = time.perf_counter() - t0
-        el_us, el_vs = og.src[og.is_original], og.adj[og.is_original]
-        chain = make_chain(n, el_us, el_vs, og.cap0[og.is_original], s, t, K, args.batch, 0)
-        times = []
-        tb = time.perf_counter()
-        for bu, bv, bc in chain:
-            t0 = time.perf_counter()
-            O.solve_dynamic(og, ost, bu, bv, bc)
-            times.append(time.perf_counter() - t0)
-            if time.perf_counter() - tb > args.cpu_budget_s:
-                break
-        m_orig = og.m_original
-        cores = 1
-    ms = 1e3 * sum(times) / len(times)
-    sample = (f"{len(times)} chained batches of {args.batch} mixed updates on the "
-              f"{args.grid}^2 grid after a static solve of {static_s:.1f} s "
-              f"(time budget {args.cpu_budget_s:.0f} s)")
+    peak, peak_src = load_peaks()
+    solve_ms = out["solve_ms"]
+    kernel_ms = float(np.mean(solve_ms))
+    bytes_launch = float(np.mean(out["bytes_alg"]))
+    achieved = bytes_launch / 1e9 / (kernel_ms / 1e3) if kernel_ms > 0 else 0.0
+    traffic, tsrc = load_traffic(out["cfg"])
+    barriers = float(np.mean(out["epochs"] + out["waves"]))
+    bar_us = out.get("barrier_ns", 0.0) / 1e3
+    value = out["elapsed_ms"] / K
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/batch",
-        "n_gpus": world, "steps": len(times), "warmup": 0, "ms_per_step": round(ms, 3),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic",
-        "config": dict(config_block(args, world), parallelism=f"{cores} host threads (numba)"
-                       if kind == "reference" else "1 host thread (C oracle port)"),
-        "static_maxflow_edges_per_s": round(m_orig / static_s, 1), "static_ms": round(1e3 * static_s, 1),
-        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/batch", "cores": cores, "kind": kind,
-                         "sample": sample},
-        "e2e": {"value": round(ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": round(value, 4), "unit": "ms/batch", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(value, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32" if out["cap_bytes"] == 4 else "int64", "data": "synthetic",
+        "config": workload_block(args, out["cfg"], out["k"], world),
+        "graph": {"n": out["n"], "slots": out["S"], "m_original": out["m_orig"],
+                  "build_s": round(out["build_s"], 2)},
+        "static_maxflow_edges_per_s": round(out["m_orig"] / (out["static_ms"] / 1e3), 1),
+        "static_ms": round(out["static_ms"], 3), "static_rounds": out["static_rounds"],
+        "gpu_static_resolve_ms": round(out["resolve_ms"], 3) if "resolve_ms" in out else None,
+        "dynamic_speedup_vs_gpu_static_resolve": (round(out["resolve_ms"] / value, 2)
+                                                  if "resolve_ms" in out else None),
+        "flow_static": out["static_flow"], "flows": out["flows"],
+        "per_batch_ms": [round(x, 3) for x in out["solve_ms"]],
+        "rounds_per_batch": round(float(np.mean(out["rounds"])), 2),
+        "gpu_launches": out["launches"],
+        "roofline": {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 5), "peak_source": peak_src,
+            "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+            "traffic_source": tsrc,
+            "kernel": "solve_kernel (persistent cooperative, one launch per batch)",
+            "bytes_alg_per_launch": int(bytes_launch),
+            "kernel_ms_per_launch": round(kernel_ms, 4),
+            "latency": {"grid_barriers_per_launch": round(barriers, 1),
+                        "barrier_us": round(bar_us, 2),
+                        "barrier_floor_ms": round(barriers * bar_us / 1e3, 4),
+                        "frac": round(barriers * bar_us / 1e3 / kernel_ms, 4) if kernel_ms else None,
+                        "bfs_levels_per_launch": round(float(np.mean(out["levels"])), 1)},
+        },
+        "clocks": out["clocks"],
+        "kernel_src_hash": kernel_source_hash(),
     }
+    if "e2e_ms_per_step" in out:
+        line["e2e"] = {"value": round(out["e2e_ms_per_step"], 4), "unit": "ms/batch",
+                       "h2d_bytes_per_step": out["e2e_h2d"], "d2h_bytes_per_step": out["e2e_d2h"],
+                       "same_batches_as_value": True}
+    if "cpu_baseline" in out:
+        line["cpu_baseline"] = out["cpu_baseline"]
     print(json.dumps(line), flush=True)
 
 
-def bench_c5(args, rank, world, local, pg):
-    """C5: R-MAT (scale 26, ef 16) split by vertex range.  Under
-    torchrun every rank hosts one part on its GPU (NCCL all-reduces, CUDA IPC
-    peer mappings); as one process, --parts parts share cuda:0.  Each step
-    is one chained batch of --batch mixed updates sampled on the device
-    before the timed region and applied from host memory (H2D of the batch
-    and D2H of the per-phase counters inside the timed region, so `value`
-    is end to end)."""
+# ---------------------------------------------------------------------------
+# C5: vertex-range partition (the multi-GPU path)
+# ---------------------------------------------------------------------------
+def bench_c5(args, rank, world, dev, pg, backend):
     import torch
 
     from paper_2511_01235_b200 import partition
-    torch.cuda.set_device(local)
-    group = partition.TorchGroup(device=local) if world > 1 else \
-        partition.LocalGroup(args.parts, [local] * args.parts)
+    group = partition.TorchGroup(device=dev) if world > 1 else \
+        partition.LocalGroup(args.parts, [dev] * args.parts)
     t0 = time.perf_counter()
-    g = partition.PartitionedGraph.rmat(args.scale, 16, 0, group, device=local)
+    g = partition.PartitionedGraph.rmat(args.scale, 16, 0, group, device=dev)
     build_s = time.perf_counter() - t0
     st = g.solve_static()
     W, K = args.warmup, args.steps
-    k = args.batch if args.batch != BATCH else 1_000_000  # C5 batches: 1M updates
+    k = args.batch or 1_000_000
     for i in range(W):
         g.solve_dynamic(g.sample_batch(k, seed=i))
-    timed, flows = [], []
+    timed, flows, phases = [], [], []
     calls0 = g.calls
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for i in range(W, W + K):
             b = g.sample_batch(k, seed=i)  # device sampler, outside the timed solve
-            barrier(pg, local)
+            barrier(pg, backend, dev)
             torch.cuda.synchronize()
             r = g.solve_dynamic(b)  # host batch in, counters out (end to end)
             torch.cuda.synchronize()
             timed.append(r.seconds)  # max over ranks inside solve_dynamic
             flows.append(r.flow_value)
+            phases.append({"rounds": r.rounds, "bfs_levels": r.bfs_levels, "waves": r.waves})
     calls = (g.calls - calls0) / K
     rs = g.solve_static()
     assert rs.flow_value == flows[-1], (rs.flow_value, flows[-1])
@@ -450,83 +531,196 @@ def bench_c5(args, rank, world, local, pg):
         "config": {"workload": f"C5: R-MAT scale {args.scale} ef 16 (device generator, seed 0), "
                                f"{g.m} Bi-CSR slots, chained batches of {k} mixed "
                                f"updates (device sampler, bias 10)",
-                   "parallelism": f"vertex-range partition, {parts} parts on {world} GPU(s)",
-                   "l2": "inputs larger than L2 (~44 GB of Bi-CSR + state)"},
+                   "config": "C5", "parts": parts,
+                   "parallelism": f"vertex-range partition, {parts} parts on {world} rank(s), "
+                                  f"collectives {backend or 'none (one process)'}",
+                   "l2": "inputs larger than L2"},
         "static_maxflow_edges_per_s": round(g.m_original / st.seconds, 1),
         "static_ms": round(1e3 * st.seconds, 3), "build_s": round(build_s, 2),
         "gpu_static_resolve_ms": round(1e3 * rs.seconds, 3),
         "dynamic_speedup_vs_gpu_static_resolve": round(rs.seconds * 1e3 / ms, 2),
-        "flow_static": st.flow_value, "flows": flows[:3], "resolve_agrees": True,
-        "e2e": {"value": round(ms, 3), "unit": "ms/batch",
-                "h2d_bytes_per_step": 32 * k,
+        "flow_static": st.flow_value, "flows": flows, "resolve_agrees": True,
+        "per_batch": {k2: round(float(np.mean([p[k2] for p in phases])), 2)
+                      for k2 in ("rounds", "bfs_levels", "waves")},
+        "e2e": {"value": round(ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": 32 * k,
                 "d2h_bytes_per_step": int(64 * calls)},
+        "host_calls_per_batch": round(calls, 1),
         "roofline": None, "clocks": clk.summary(),
-        "note": "partitioned path is host-driven per phase; the roofline line is the C2 "
-                "single-GPU bench (python bench.py)",
+        "note": "host-driven per phase; the roofline line is the single-GPU bench",
     }
+    print(json.dumps(line), flush=True)
+    g.close()
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+class _Capped(Exception):
+    pass
+
+
+def _ref_dynamic(ref, st, g, batch, params, cap_s):
+    """One reference solve_dynamic, stopped through its instrument hook
+    (called after every global relabel, solver.py:219-241) once past cap."""
+    t0 = time.perf_counter()
+    rounds = [0]
+
+    def hook(_st, _g, rnd, label):
+        rounds[0] = rnd
+        if time.perf_counter() - t0 > cap_s:
+            raise _Capped()
+
+    params.instrument = hook
+    try:
+        r = ref.solve_dynamic(st, g, batch, params)
+        return time.perf_counter() - t0, r, False
+    except _Capped:
+        return time.perf_counter() - t0, rounds[0], True
+    finally:
+        params.instrument = None
+
+
+def bench_reference(args, cfg, world):
+    """The unmodified reference package on the host cores, same config."""
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    cores = os.cpu_count() or 1
+    try:
+        import dynmaxflow as ref
+    except Exception as e:  # pragma: no cover - install missing
+        print(json.dumps({"impl": "reference", "unavailable": f"baseline/_ref import failed: {e}"}))
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    k = args.batch or CONFIGS[cfg][2]
+    params = ref.SolverParams(threads=cores)
+    tg, ts, tt = ref.random_graph(50, 300, seed=0)  # warm the numba JIT (bench.py protocol)
+    g0 = ref.build_bicsr(tg)
+    ref.solve_dynamic(ref.solve_static(g0, ts, tt, params).state, g0,
+                      ref.UpdateBatch.from_updates([]), params)
+    n, us, vs, caps, s, t = make_instance(cfg, args.side)
+    t0 = time.perf_counter()
+    csr = ref.build_bicsr(ref.EdgeListGraph(n, us, vs, caps))
+    build_s = time.perf_counter() - t0
+    del us, vs, caps
+    notes = {}
+    static_s = None
+    if cfg == "C4" and not args.side:
+        # start state: a maximum flow from the oracle's Dinic restatement
+        import oracle as O
+        og = O.OracleGraph(n, csr.m, csr.offsets, csr.adj, csr.src, csr.rev, csr.cap0,
+                           csr.is_original, (0, 0, 0))
+        t0 = time.perf_counter()
+        flow0, ost = O.terminated_state(og, s, t)
+        notes["start_state"] = (f"max flow {flow0} from oracle Dinic (oracle.py:20-84 restated), "
+                                f"{time.perf_counter() - t0:.1f} s, not timed; reference static "
+                                f"solve infeasible (~10^4 rounds of O(n) BFS)")
+        st = ref.SolverState(ost.cf, ost.excess, ost.height, s, t, n)
+        g = csr
+    else:
+        t0 = time.perf_counter()
+        prior = ref.solve_static(csr, s, t, params)
+        static_s = time.perf_counter() - t0
+        st, g = prior.state, csr
+    el = csr.to_edge_list()
+    chain = make_chain(n, el.us, el.vs, el.caps, s, t, max(1, args.steps), k, 0)
+    times, capped_any, done = [], False, 0
+    tb = time.perf_counter()
+    for bu, bv, bc in chain:
+        dt, r, capped = _ref_dynamic(ref, st, g, ref.UpdateBatch(bu, bv, bc), params,
+                                     args.ref_cap_s)
+        times.append(dt)
+        if capped:
+            capped_any = True
+            notes["capped_batch"] = (f"batch {len(times) - 1} unfinished after {dt:.1f} s "
+                                     f"(round {r}); value is a lower bound")
+            break
+        done += 1
+        st, g = r.state, r.graph
+        if time.perf_counter() - tb > args.ref_budget_s:
+            break
+    ms = 1e3 * sum(times) / len(times)
+    anchor = ref_anchor(ref, args, cores) if cfg == "C4" and not args.side else None
+    sample = (f"{done} chained batch(es) of {k} mixed updates completed"
+              + (", then one capped" if capped_any else "") +
+              f" (per-batch cap {args.ref_cap_s:.0f} s, budget {args.ref_budget_s:.0f} s); "
+              f"build_bicsr {build_s:.1f} s not timed")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/batch",
+        "n_gpus": world, "steps": len(times), "warmup": 0, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "lower_bound": capped_any,
+        "config": dict(workload_block(args, cfg, k, 1),
+                       parallelism=f"{cores} host threads (numba, SolverParams(threads={cores}))"),
+        "static_ms": round(1e3 * static_s, 1) if static_s else None,
+        "static_maxflow_edges_per_s": round(csr.m_original / static_s, 1) if static_s else None,
+        "per_batch_ms": [round(1e3 * x, 1) for x in times],
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/batch", "cores": cores,
+                         "kind": "reference", "sample": sample, "lower_bound": capped_any},
+        "e2e": {"value": round(ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "notes": notes,
+    }
+    if anchor:
+        line["scaled_anchor"] = anchor
     print(json.dumps(line), flush=True)
 
 
-def config_block(args, world):
-    return {"workload": f"C2: {args.grid}x{args.grid} 4-neighbour grid + terminal edge per pixel "
-                        f"(caps U[1,100], seed 0), chained batches of {args.batch} mixed updates "
-                        f"(bias 10)",
-            "graph": f"grid{args.grid}", "batch_updates": args.batch,
-            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-            "l2": "inputs larger than L2 (Bi-CSR + state ~0.8 GB > 126 MB L2)"}
+def ref_anchor(ref, args, cores):
+    """C4's generator at 512^2 run to completion by the reference:
+    static solve and chained batches, threads=nproc and threads=1."""
+    from paper_2511_01235_b200 import gen
+    side = 512
+    us, vs, caps, s, t = gen.road_graph(side, side, seed=0, p_vert=0.21)
+    n = side * side
+    out = {"graph": f"road {side}x{side} (C4 generator), n={n}, m={us.size}"}
+    csr0 = ref.build_bicsr(ref.EdgeListGraph(n, us, vs, caps))
+    k = max(1, round(10000 * csr0.m_original / 58104530))
+    el = csr0.to_edge_list()
+    chain = make_chain(n, el.us, el.vs, el.caps, s, t, 2, k, 0)
+    out["batch_updates"] = k
+    for thr in (cores, 1):
+        p = ref.SolverParams(threads=thr)
+        csr = csr0.copy()
+        t0 = time.perf_counter()
+        prior = ref.solve_static(csr, s, t, p)
+        st_s = time.perf_counter() - t0
+        st, g, dts, flows = prior.state, csr, [], []
+        for bu, bv, bc in chain:
+            t0 = time.perf_counter()
+            r = ref.solve_dynamic(st, g, ref.UpdateBatch(bu, bv, bc), p)
+            dts.append(time.perf_counter() - t0)
+            st, g = r.state, r.graph
+            flows.append(r.flow_value)
+        out[f"threads_{thr}"] = {"static_ms": round(1e3 * st_s, 1), "static_rounds": prior.rounds,
+                                 "static_flow": prior.flow_value,
+                                 "dynamic_ms_per_batch": round(1e3 * float(np.mean(dts)), 1),
+                                 "flows": flows}
+    return out
 
 
+# ---------------------------------------------------------------------------
 def main():
     args = parse()
-    rank, world, local, pg = dist_setup(args)
+    maybe_relaunch(args)
+    rank, world, dev, pg, backend = dist_setup()
+    cfg = args.config
+    if cfg == "auto":
+        cfg = "C5" if world > 1 else "C4"
     if args.impl == "reference":
         if rank == 0:
-            if args.config == "C5":
+            if cfg == "C5":
                 print(json.dumps({"impl": "reference", "unavailable":
-                                  "the reference CPU build_bicsr cannot hold the 2.1 B-slot C5 "
-                                  "graph (SURVEY 6.2); C5 parity = dynamic vs GPU static re-solve"}))
+                                  "the reference's numpy build_bicsr cannot hold the 2.1 B-slot "
+                                  "C5 graph (SURVEY 6.2); C5 parity = dynamic vs GPU static "
+                                  "re-solve"}))
             else:
-                bench_reference(args, rank, world)
+                bench_reference(args, cfg, world)
         return
-    if args.config == "C5":
-        bench_c5(args, rank, world, local, pg)
+    if cfg == "C5":
+        bench_c5(args, rank, world, dev, pg, backend)
         return
-    out = bench_ours(args, rank, world, local, pg)
-    if rank != 0:
-        return
-    K = args.steps
-    peak, peak_kind = load_peaks()
-    solve_ms_tot = sum(out["solve_ms"])
-    achieved = (sum(out["bytes_alg"]) / 1e9) / (solve_ms_tot / 1e3) if solve_ms_tot > 0 else 0.0
-    traffic = load_traffic()
-    value = out["elapsed_ms"] / (K * world)
-    line = {
-        "metric": METRIC, "value": round(value, 4), "unit": "ms/batch", "n_gpus": world,
-        "steps": K, "warmup": args.warmup, "ms_per_step": round(out["ms_per_step"], 4),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic", "config": config_block(args, world),
-        "static_maxflow_edges_per_s": round(out["m_orig"] / (out["static_ms"] / 1e3), 1),
-        "static_ms": round(out["static_ms"], 3),
-        "gpu_static_resolve_ms": round(out.get("resolve_ms", float("nan")), 3),
-        "dynamic_speedup_vs_gpu_static_resolve": (round(out["resolve_ms"] / out["ms_per_step"], 2)
-                                                  if "resolve_ms" in out else None),
-        "flow_static": out["static_flow"], "flows": out["flows"][:3] + ["..."],
-        "rounds_per_batch": round(float(np.mean(out["rounds"])), 2),
-        "gpu_launches": out["launches"],
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "peak_source": peak_kind,
-                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                     "kernel": "mfx::solve_kernel (persistent, one launch per batch)",
-                     "bytes_alg_per_launch": int(np.mean(out["bytes_alg"])),
-                     "kernel_ms_per_launch": round(solve_ms_tot / K, 4)},
-        "clocks": out["clocks"],
-    }
-    if "e2e_ms_per_step" in out:
-        line["e2e"] = {"value": round(out["e2e_ms_per_step"] / world, 4), "unit": "ms/batch",
-                       "h2d_bytes_per_step": out["e2e_h2d"], "d2h_bytes_per_step": out["e2e_d2h"]}
-    if "cpu_baseline" in out:
-        line["cpu_baseline"] = out["cpu_baseline"]
-    print(json.dumps(line), flush=True)
+    out = bench_ours(args, cfg, rank, world, dev, pg, backend)
+    if rank == 0:
+        emit_ours(args, out, world)
 
 
 if __name__ == "__main__":

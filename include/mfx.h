@@ -169,6 +169,12 @@ int mfx_solve_dynamic_device(mfx_graph *g, mfx_state *st, int64_t k, const int64
 int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
                                const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
                                mfx_result *r);
+/* solve_dynamic_pushpull up to (not including) its final ordinary pass: the
+ * host then steps the final rounds with mfx_step so SolverParams.instrument
+ * sees them (dynamic.py:366-369).  The state is left non-terminated. */
+int mfx_pushpull_regions(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                         const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
+                         mfx_result *r);
 /* apply_updates (dynamic.py:91-111) alone. */
 int mfx_apply_updates(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
                       const int64_t *vs, const int64_t *new_caps);

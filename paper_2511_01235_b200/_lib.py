@@ -101,6 +101,8 @@ SIGNATURES = {
                                                 ctypes.POINTER(Params), ctypes.POINTER(Result)]),
     "mfx_solve_dynamic_pushpull": (ctypes.c_int, [vp, vp, i64, p_i64, p_i64, p_i64,
                                                   ctypes.POINTER(Params), ctypes.POINTER(Result)]),
+    "mfx_pushpull_regions": (ctypes.c_int, [vp, vp, i64, p_i64, p_i64, p_i64,
+                                            ctypes.POINTER(Params), ctypes.POINTER(Result)]),
     "mfx_apply_updates": (ctypes.c_int, [vp, vp, i64, p_i64, p_i64, p_i64]),
     "mfx_dynamic_prephase": (ctypes.c_int, [vp, vp, i64, p_i64, p_i64, p_i64]),
     "mfx_recompute_excess": (ctypes.c_int, [vp, vp]),

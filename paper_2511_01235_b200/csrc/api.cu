@@ -53,6 +53,15 @@ static int fail(int code, const char *fmt, ...) {
   } while (0)
 
 template <typename T>
+static void dfree(T *&p);
+
+static std::atomic<unsigned long long> g_cap_ids{1};
+static uint64_t next_cap_id() { return g_cap_ids++; }
+
+// every entry point that touches a topology's workspace / stream holds its lock
+#define LOCK_TOPO(T) std::lock_guard<std::recursive_mutex> _topo_lock((T).mu)
+
+template <typename T>
 static void dfree(T *&p) {
   if (p) cudaFree((void *)p);
   p = nullptr;
@@ -211,6 +220,34 @@ cudaError_t ensure_batch_capacity(Topology &t, int64_t k) {
 
 using namespace mfx;
 
+// A state whose residuals were last consistent with other capacity contents
+// (set_cap0, or a batch applied through another state / graph copy): the
+// reference recomputes excess from max(0, cap0 - cf) on every solve_dynamic
+// (dynamic.py:114-116) and reads cf[rev] directly.  Here the BFS reads the
+// reverse residual as pc - cf, so the pair sums must still hold: if they do,
+// the excess is rebuilt in full before the next use; if not, the state no
+// longer describes a flow on this graph and the call is rejected.
+static int sync_caps(const GraphObj &g, StateObj &st) {
+  if (st.cap_id == g.cap_id) return MFX_OK;
+  Topology &T = *g.topo;
+  CK(ensure_workspace(T));
+  unsigned long long out[2];
+  CK(launch_pair_check(g, st, T.ws.d_red));
+  CK(cudaMemcpyAsync(out, T.ws.d_red, sizeof(out), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  if (out[0])
+    return fail(MFX_SOLVER_ERROR,
+                "state residuals do not match the graph's capacities (%llu slot pair(s) "
+                "violate residual-sum conservation, first slot %llu); the capacities changed "
+                "after this state was solved -- start from init_residuals",
+                out[0], out[1]);
+  st.excess_consistent = false;
+  st.terminated_known = false;
+  st.cap_id = g.cap_id;
+  return MFX_OK;
+}
+
+
 // ---------------------------------------------------------------------------
 static int make_topology(int device, std::shared_ptr<Topology> &topo) {
   int count = 0;
@@ -241,6 +278,7 @@ static int finish_graph(mfx_graph *G, int64_t *d_cap0_64, int force_wide) {
   CK(cudaMalloc(&G->g.pc, S * T.cap_bytes));
   CK(launch_convert_cap(d_cap0_64, G->g.cap0, T.cap_bytes, T.S, T.stream));
   CK(launch_refresh_pc(G->g));
+  G->g.cap_id = next_cap_id();
   CK(cudaStreamSynchronize(T.stream));
   CK(ensure_workspace(T));
   CK(cudaStreamSynchronize(T.stream));
@@ -402,7 +440,8 @@ static int download_cap(const void *d, int cap_bytes, int64_t *h, size_t cnt, cu
 
 int mfx_graph_download(const mfx_graph *g, int64_t *offsets, int64_t *adj, int64_t *src,
                        int64_t *rev, int64_t *cap0, uint8_t *is_original) {
-  const Topology &T = *g->g.topo;
+  Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   int rc;
   if ((rc = widen_download_i32(T.off, offsets, (size_t)T.n + 1, T.stream))) return rc;
@@ -424,10 +463,12 @@ int mfx_graph_download(const mfx_graph *g, int64_t *offsets, int64_t *adj, int64
 }
 
 int mfx_graph_copy(const mfx_graph *g, mfx_graph **out) {
-  const Topology &T = *g->g.topo;
+  Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   mfx_graph *G = new mfx_graph();
   G->g.topo = g->g.topo;
+  G->g.cap_id = g->g.cap_id;  // same contents
   size_t bytes = (size_t)(T.S > 0 ? T.S : 1) * T.cap_bytes;
   cudaError_t e = cudaMalloc(&G->g.cap0, bytes);
   if (!e) e = cudaMalloc(&G->g.pc, bytes);
@@ -444,25 +485,37 @@ int mfx_graph_copy(const mfx_graph *g, mfx_graph **out) {
 
 int mfx_graph_set_cap0(mfx_graph *g, const int64_t *cap0) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   if (T.S == 0) return MFX_OK;
-  if (T.cap_bytes == 4)
-    for (int64_t i = 0; i < T.S; ++i)
-      if (cap0[i] < 0 || cap0[i] >= (1ll << 30))
-        return fail(MFX_VALUE_ERROR, "capacity %lld does not fit the int32 residual storage",
-                    (long long)cap0[i]);
+  CK(ensure_workspace(T));
   Staged b;
   CK(cudaMalloc(&b.p, sizeof(int64_t) * (size_t)T.S));
   CK(cudaMemcpy(b.p, cap0, sizeof(int64_t) * (size_t)T.S, cudaMemcpyHostToDevice));
+  // negative capacities, and (int32 storage) pair sums that reach 2^31
+  unsigned long long bad[2];
+  CK(launch_cap_check(T, (const int64_t *)b.p, T.ws.d_red));
+  CK(cudaMemcpyAsync(bad, T.ws.d_red, sizeof(bad), cudaMemcpyDeviceToHost, T.stream));
+  CK(cudaStreamSynchronize(T.stream));
+  if (bad[0] != ~0ull)
+    return fail(MFX_GRAPH_ERROR, "edge %llu has negative capacity %lld", bad[0],
+                (long long)cap0[bad[0]]);
+  if (bad[1] != ~0ull)
+    return fail(MFX_VALUE_ERROR,
+                "capacity %lld on slot %llu: pair sum overflows the int32 residual storage; "
+                "rebuild the graph with wide capacities",
+                (long long)cap0[bad[1]], bad[1]);
   CK(launch_convert_cap((const int64_t *)b.p, g->g.cap0, T.cap_bytes, T.S, T.stream));
   CK(launch_refresh_pc(g->g));
   CK(cudaStreamSynchronize(T.stream));
+  g->g.cap_id = next_cap_id();  // states solved against the old capacities are now stale
   return MFX_OK;
 }
 
 int mfx_edge_indices(const mfx_graph *g, int64_t k, const int64_t *us, const int64_t *vs,
                      int64_t *out) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   if (k <= 0) return MFX_OK;
   CK(ensure_batch_capacity(T, k));
@@ -491,6 +544,7 @@ int mfx_state_create(const mfx_graph *g, int64_t source, int64_t sink, mfx_state
   st.topo = g->g.topo;
   st.s = (int)source;
   st.t = (int)sink;
+  st.cap_id = g->g.cap_id;
   size_t SS = (size_t)(T.S > 0 ? T.S : 1);
   cudaError_t e = cudaMalloc(&st.cf, SS * T.cap_bytes);
   if (!e) e = cudaMalloc(&st.ex, sizeof(long long) * (size_t)T.n);
@@ -510,7 +564,8 @@ int mfx_state_create(const mfx_graph *g, int64_t source, int64_t sink, mfx_state
 }
 
 int mfx_state_copy(const mfx_state *st, mfx_state **out) {
-  const Topology &T = *st->s.topo;
+  Topology &T = *st->s.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   mfx_state *S = new mfx_state();
   StateObj &d = S->s;
@@ -519,6 +574,7 @@ int mfx_state_copy(const mfx_state *st, mfx_state **out) {
   d.t = st->s.t;
   d.excess_consistent = st->s.excess_consistent;
   d.terminated_known = st->s.terminated_known;
+  d.cap_id = st->s.cap_id;
   size_t cfb = (size_t)(T.S > 0 ? T.S : 1) * T.cap_bytes;
   cudaError_t e = cudaMalloc(&d.cf, cfb);
   if (!e) e = cudaMalloc(&d.ex, sizeof(long long) * (size_t)T.n);
@@ -542,7 +598,8 @@ int mfx_state_copy(const mfx_state *st, mfx_state **out) {
 int mfx_state_assign(mfx_state *dst, const mfx_state *src) {
   if (dst->s.topo != src->s.topo)
     return fail(MFX_VALUE_ERROR, "states belong to different graph topologies");
-  const Topology &T = *src->s.topo;
+  Topology &T = *src->s.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   size_t cfb = (size_t)(T.S > 0 ? T.S : 1) * T.cap_bytes;
   CK(cudaMemcpyAsync(dst->s.cf, src->s.cf, cfb, cudaMemcpyDeviceToDevice, T.stream));
@@ -553,12 +610,14 @@ int mfx_state_assign(mfx_state *dst, const mfx_state *src) {
   dst->s.t = src->s.t;
   dst->s.excess_consistent = src->s.excess_consistent;
   dst->s.terminated_known = src->s.terminated_known;
+  dst->s.cap_id = src->s.cap_id;
   return MFX_OK;
 }
 
 int mfx_state_upload(mfx_state *st, const int64_t *cf, const int64_t *excess,
                      const int64_t *height) {
-  const Topology &T = *st->s.topo;
+  Topology &T = *st->s.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   if (cf && T.S > 0) {
     if (T.cap_bytes == 8) {
@@ -582,11 +641,13 @@ int mfx_state_upload(mfx_state *st, const int64_t *cf, const int64_t *excess,
   }
   st->s.excess_consistent = false;
   st->s.terminated_known = false;
+  st->s.cap_id = 0;  // arbitrary residuals: pair sums are checked at the next use
   return MFX_OK;
 }
 
 int mfx_state_download(const mfx_state *st, int64_t *cf, int64_t *excess, int64_t *height) {
-  const Topology &T = *st->s.topo;
+  Topology &T = *st->s.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   int rc;
   if ((rc = download_cap(st->s.cf, T.cap_bytes, cf, (size_t)T.S, T.stream))) return rc;
@@ -601,7 +662,8 @@ int mfx_state_download(const mfx_state *st, int64_t *cf, int64_t *excess, int64_
 void mfx_state_free(mfx_state *st) { delete st; }
 
 int mfx_saturate_source(mfx_state *st, const mfx_graph *g) {
-  const Topology &T = *g->g.topo;
+  Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   CK(launch_saturate(g->g, st->s));
   CK(cudaStreamSynchronize(T.stream));
@@ -610,7 +672,8 @@ int mfx_saturate_source(mfx_state *st, const mfx_graph *g) {
 }
 
 int mfx_mask(const mfx_state *st, int which, uint8_t *out) {
-  const Topology &T = *st->s.topo;
+  Topology &T = *st->s.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   Staged b;
   CK(cudaMalloc(&b.p, (size_t)T.n));
@@ -672,6 +735,7 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.timeout_s = p->timeout_s > 0 ? p->timeout_s : tmo;
   cfg.blocks_per_sm = p->blocks_per_sm;
   cfg.ceiling = operation_ceiling(T.n, T.m_original);
+  if (const char *ce = getenv("MFX_CEILING")) cfg.ceiling = strtoull(ce, nullptr, 10);  // tests
   return MFX_OK;
 }
 
@@ -717,7 +781,10 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 
 int mfx_global_relabel(mfx_state *st, const mfx_graph *g, int dynamic_bases, int64_t *reached) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
+  int rc0 = sync_caps(g->g, st->s);
+  if (rc0) return rc0;
   SolveConfig cfg;
   cfg.what = WHAT_BFS;
   if (const char *fl = getenv("MFX_FLAGS")) cfg.flags = atoi(fl);  // (tests: forced retry)
@@ -733,6 +800,7 @@ int mfx_global_relabel(mfx_state *st, const mfx_graph *g, int dynamic_bases, int
 
 int mfx_solve_static(const mfx_graph *g, mfx_state *st, const mfx_params *p, mfx_result *r) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   memset(r, 0, sizeof(*r));
   if (st->s.s == st->s.t) return fail(MFX_VALUE_ERROR, "source and sink must differ");
   if (st->s.topo != g->g.topo) return fail(MFX_VALUE_ERROR, "state belongs to another graph");
@@ -747,6 +815,8 @@ int mfx_solve_static(const mfx_graph *g, mfx_state *st, const mfx_params *p, mfx
   CK(cudaEventRecord(T.ev[0], T.stream));
   CK(launch_init_state(g->g, st->s));
   CK(launch_saturate(g->g, st->s));
+  st->s.cap_id = g->g.cap_id;
+  st->s.excess_consistent = true;
   launches += 1;
   CK(cudaEventRecord(T.ev[1], T.stream));
   CK(launch_solve(g->g, st->s, cfg, &launches));
@@ -817,12 +887,14 @@ static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const in
                                 const int64_t *d_vs, const int64_t *d_caps, const mfx_params *p,
                                 mfx_result *r) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   memset(r, 0, sizeof(*r));
   if (st->s.topo != g->g.topo) return fail(MFX_VALUE_ERROR, "state belongs to another graph");
   SolveConfig cfg;
   int rc = resolve_config(T, p, cfg);
   if (rc) return rc;
   CK(cudaSetDevice(T.device));
+  if ((rc = sync_caps(g->g, st->s))) return rc;
   if ((rc = require_terminated(st, "solve_dynamic"))) return rc;
   CK(ensure_batch_capacity(T, k));
   int launches = 0;
@@ -861,6 +933,8 @@ static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const in
   CK(cudaEventSynchronize(T.ev[3]));
   CK(cudaGetLastError());
   if ((rc = batch_error(st->host_err, k, h_us, h_vs, h_caps, d_us, d_vs, d_caps))) return rc;
+  if (k > 0) g->g.cap_id = next_cap_id();
+  st->s.cap_id = g->g.cap_id;
   fill_result(st, r);
   r->updates = k;
   r->ms_update = ev_ms(T.ev[0], T.ev[1]);
@@ -886,16 +960,21 @@ int mfx_solve_dynamic_device(mfx_graph *g, mfx_state *st, int64_t k, const int64
 // solve_dynamic_pushpull (dynamic.py:292-377): regions from the prior cut,
 // batch pre-phase, A->B saturation, the two region-restricted pipelines as
 // one device round loop, then ordinary dynamic rounds for what crosses.
-int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
-                               const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
-                               mfx_result *r) {
+static int pushpull_common(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                           const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
+                           mfx_result *r, bool final_pass) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   memset(r, 0, sizeof(*r));
   if (st->s.topo != g->g.topo) return fail(MFX_VALUE_ERROR, "state belongs to another graph");
   SolveConfig cfg;
   int rc = resolve_config(T, p, cfg);
   if (rc) return rc;
+  // every pipeline and the final pass check against 2x the ceiling
+  // (dynamic.py:322); the device counters accumulate over all of them
+  cfg.ceiling = cfg.ceiling > (~0ull >> 1) ? ~0ull : 2 * cfg.ceiling;
   CK(cudaSetDevice(T.device));
+  if ((rc = sync_caps(g->g, st->s))) return rc;
   if ((rc = require_terminated(st, "solve_dynamic_pushpull"))) return rc;
   {  // the prior heights must carry a cut certificate: s in A, t in B
     int hs = 0, ht = 0;
@@ -938,11 +1017,13 @@ int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int
   if (!(p && p->bfs_local_max > 0) && !getenv("MFX_BFS_LOCAL_MAX")) cfg.bfs_local_max = 1 << 20;
   CK(launch_solve(g->g, st->s, cfg, &launches));
   cfg.bfs_local_max = blm;
-  cfg.pushpull = false;  // final pass: overflow on the B side meets deficits on the A side
-  cfg.reset_counters = false;
-  cfg.dyn_bases = 1;
-  cfg.forbidden = st->s.s;
-  CK(launch_solve(g->g, st->s, cfg, &launches));
+  if (final_pass) {
+    cfg.pushpull = false;  // final pass: overflow on the B side meets deficits on the A side
+    cfg.reset_counters = false;
+    cfg.dyn_bases = 1;
+    cfg.forbidden = st->s.s;
+    CK(launch_solve(g->g, st->s, cfg, &launches));
+  }
   CK(cudaEventRecord(T.ev[2], T.stream));
   CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
   CK(cudaMemcpyAsync(st->host_err, T.ws.d_err, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
@@ -951,6 +1032,8 @@ int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int
   CK(cudaEventSynchronize(T.ev[3]));
   CK(cudaGetLastError());
   if ((rc = batch_error(st->host_err, k, us, vs, new_caps, d_us, d_vs, d_caps))) return rc;
+  if (k > 0) g->g.cap_id = next_cap_id();
+  st->s.cap_id = g->g.cap_id;
   fill_result(st, r);
   r->updates = k;
   r->ms_update = ev_ms(T.ev[0], T.ev[1]);
@@ -958,14 +1041,39 @@ int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int
   r->ms_total = ev_ms(T.ev[0], T.ev[3]);
   r->launches = launches;
   st->s.excess_consistent = true;
+  if (!final_pass) {  // the host steps the final rounds (mfx_step)
+    st->s.terminated_known = false;
+    if (st->host_ctrl->status == 6) return fail(MFX_TIMEOUT, "device watchdog expired");
+    if (st->host_ctrl->status == 3)
+      return fail(MFX_SOLVER_ERROR, "push/relabel count %llu exceeded the termination ceiling %llu",
+                  st->host_ctrl->pushes + st->host_ctrl->relabels, st->host_ctrl->ceiling);
+    return MFX_OK;
+  }
   st->s.terminated_known = r->status == 0;
   return solve_status(st, r);
+}
+
+int mfx_solve_dynamic_pushpull(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                               const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
+                               mfx_result *r) {
+  return pushpull_common(g, st, k, us, vs, new_caps, p, r, true);
+}
+
+int mfx_pushpull_regions(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
+                         const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
+                         mfx_result *r) {
+  return pushpull_common(g, st, k, us, vs, new_caps, p, r, false);
 }
 
 int mfx_apply_updates(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
                       const int64_t *vs, const int64_t *new_caps) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
+  if (st) {
+    int rc0 = sync_caps(g->g, st->s);
+    if (rc0) return rc0;
+  }
   CK(ensure_batch_capacity(T, k));
   int64_t *d = T.ws.d_batch;
   if (k > 0) {
@@ -979,6 +1087,8 @@ int mfx_apply_updates(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
   CK(cudaStreamSynchronize(T.stream));
   int rc = batch_error(err, k, us, vs, new_caps, nullptr, nullptr, nullptr);
   if (rc) return rc;
+  if (k > 0) g->g.cap_id = next_cap_id();
+  if (st) st->s.cap_id = g->g.cap_id;
   if (st && k > 0) {
     // apply_updates alone leaves excess stale until recompute_excess (dynamic.py:114-116)
     st->s.excess_consistent = false;
@@ -990,8 +1100,10 @@ int mfx_apply_updates(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
 int mfx_dynamic_prephase(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
                          const int64_t *vs, const int64_t *new_caps) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   int rc;
+  if ((rc = sync_caps(g->g, st->s))) return rc;
   if ((rc = require_terminated(st, "solve_dynamic"))) return rc;
   CK(ensure_batch_capacity(T, k));
   int64_t *d = T.ws.d_batch;
@@ -1007,28 +1119,38 @@ int mfx_dynamic_prephase(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *
   CK(cudaMemcpyAsync(err, T.ws.d_err, sizeof(err), cudaMemcpyDeviceToHost, T.stream));
   CK(cudaStreamSynchronize(T.stream));
   if ((rc = batch_error(err, k, us, vs, new_caps, nullptr, nullptr, nullptr))) return rc;
+  if (k > 0) g->g.cap_id = next_cap_id();
+  st->s.cap_id = g->g.cap_id;
   st->s.excess_consistent = true;
   st->s.terminated_known = false;
   return MFX_OK;
 }
 
 int mfx_recompute_excess(mfx_state *st, const mfx_graph *g) {
-  const Topology &T = *g->g.topo;
+  Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
+  int rc0 = sync_caps(g->g, st->s);
+  if (rc0) return rc0;
   CK(launch_recompute_excess(g->g, st->s));
   CK(cudaStreamSynchronize(T.stream));
+  st->s.excess_consistent = true;
   return MFX_OK;
 }
 
 int mfx_step(const mfx_graph *g, mfx_state *st, const mfx_params *p, int step, int dynamic_bases,
              int64_t *active, mfx_result *r) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   SolveConfig cfg;
   int rc = resolve_config(T, p, cfg);
   if (rc) return rc;
   CK(cudaSetDevice(T.device));
+  if ((rc = sync_caps(g->g, st->s))) return rc;
+  // static rounds: bases {t}, nothing forbidden (solver.py:155-164); dynamic:
+  // bases {t} U deficient, s forbidden (dynamic.py:119-133)
   cfg.dyn_bases = dynamic_bases ? 1 : 0;
-  cfg.forbidden = st->s.s;
+  cfg.forbidden = dynamic_bases ? st->s.s : -1;
   cfg.reset_counters = (step & 0x10) != 0;  // first step of an instrumented solve
   step &= 0xF;
   if (step == 0) cfg.what = WHAT_BFS;
@@ -1068,6 +1190,7 @@ int mfx_certificate(const mfx_state *st, const mfx_graph *g, int64_t *cut, uint8
 
 int mfx_verify(const mfx_state *st, const mfx_graph *g, mfx_verify_report *rep) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   Staged b;
   CK(cudaMalloc(&b.p, sizeof(long long) * 16));
@@ -1093,6 +1216,7 @@ int mfx_verify(const mfx_state *st, const mfx_graph *g, mfx_verify_report *rep) 
 int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_per_sm,
                       double *ns_per_barrier) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   SolveConfig cfg;
   cfg.what = WHAT_BARRIER;
@@ -1110,6 +1234,7 @@ int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_p
 int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int64_t cap,
                     int64_t *count) {
   Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
   CK(cudaSetDevice(T.device));
   *count = 0;
   if (!T.ws.trace) return MFX_OK;

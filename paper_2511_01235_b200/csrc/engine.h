@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include "mfx_internal.cuh"
@@ -54,6 +55,9 @@ struct Topology {
   int num_sms = 0;
   int variant = -1;  // solve-kernel build: 0 = v256, 1 = v512 (-1: not chosen yet)
   Workspace ws;
+  // every C-ABI call on this topology (graph copies and their states share the
+  // workspace, the stream and the events) holds this lock
+  std::recursive_mutex mu;
   ~Topology();
 };
 
@@ -61,6 +65,9 @@ struct GraphObj {
   std::shared_ptr<Topology> topo;
   void *cap0 = nullptr;  // CapT[S]
   void *pc = nullptr;    // CapT[S]
+  // identity of the current capacity contents: a fresh id on every cap0
+  // write (builds, set_cap0, applied batches); copies inherit it
+  uint64_t cap_id = 0;
   ~GraphObj();
 };
 
@@ -73,6 +80,7 @@ struct StateObj {
   Ctrl *ctrl = nullptr;      // control block
   bool excess_consistent = true;  // excess == sum_row(cf - cap0) known to hold
   bool terminated_known = false;  // last op was a completed solve
+  uint64_t cap_id = 0;            // capacities cf / excess were last consistent with
   ~StateObj();
 };
 
@@ -140,6 +148,8 @@ cudaError_t launch_refresh_pc(const GraphObj &g);
 cudaError_t launch_mask(const StateObj &st, int which, uint8_t *d_out);
 cudaError_t launch_recompute_excess(const GraphObj &g, StateObj &st);
 cudaError_t launch_count_active(const StateObj &st, unsigned long long *d_out);
+cudaError_t launch_pair_check(const GraphObj &g, const StateObj &st, unsigned long long *d_out);
+cudaError_t launch_cap_check(const Topology &T, const int64_t *d_cap, unsigned long long *d_out);
 // Batch: validate into ws.d_err (no mutation), then apply only if no error.
 // update_excess: move excess at repaired endpoints (fused solve_dynamic path);
 // false mirrors apply_updates alone, which leaves excess to recompute_excess.

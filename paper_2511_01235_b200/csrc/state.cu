@@ -245,12 +245,24 @@ __global__ void batch_resolve_kernel(const int *__restrict__ off, const int *__r
     slot[j] = i;
     uv[2 * j] = uu;
     uv[2 * j + 1] = vv;
-    if (i < 0 || !orig[i]) {
-      atomicMin(err + E_UNKNOWN, j);
-    } else if (sizeof(CapT) == 4 && c >= 0) {
-      // int32 residual storage needs every pair sum < 2^31
-      if (c >= (1ll << 30) || c + (long long)cap0[rev[i]] >= (1ll << 31)) atomicMin(err + E_OVER, j);
-    }
+    if (i < 0 || !orig[i]) atomicMin(err + E_UNKNOWN, j);
+  }
+}
+
+// int32 residual storage needs every post-batch pair sum below 2^31: the new
+// capacity plus the partner slot's capacity after the batch (its own update
+// if it is in the batch, found through slot_first, else its cap0).
+template <typename CapT>
+__global__ void batch_over_kernel(long long k, const int *slot, const int *first,
+                                  const int *__restrict__ rev, const CapT *cap0,
+                                  const long long *caps, long long *err) {
+  if (err[E_NEG] != LLONG_MAX || err[E_UNKNOWN] != LLONG_MAX) return;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
+       j += (long long)gridDim.x * blockDim.x) {
+    int r = rev[slot[j]];
+    int jr = first[r];
+    long long partner = jr != kFirstNone ? caps[jr] : (long long)cap0[r];
+    if (caps[j] + partner >= (1ll << 31)) atomicMin(err + E_OVER, j);
   }
 }
 
@@ -349,6 +361,12 @@ static cudaError_t batch_t(GraphObj &g, StateObj *st, int64_t k, const int64_t *
                                                             (const CapT *)g.cap0, T.n, k, us, vs,
                                                             cs, W.d_slot, W.d_uv, W.d_err);
   batch_first_kernel<<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, W.d_err);
+  if (sizeof(CapT) == 4) {
+    batch_over_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, T.rev,
+                                                           (const CapT *)g.cap0, cs, W.d_err);
+    count_launch();
+    if (launches) *launches += 1;
+  }
   batch_dup_kernel<<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, W.d_err);
   batch_dupidx_kernel<<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, W.d_err);
   batch_apply_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(
@@ -540,6 +558,57 @@ cudaError_t launch_verify(const GraphObj &g, const StateObj &st, long long *d_re
     verify_kernel<int><<<grid, kBlock, 0, T.stream>>>(T.off, T.adj, T.rev, T.orig,
                                                       (const int *)g.cap0, (const int *)st.cf,
                                                       st.ex, st.h, T.n, st.s, st.t, d_rep);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// capacity consistency checks
+// ---------------------------------------------------------------------------
+// cf[i] + cf[rev i] == pc[i] on every slot (residual-sum conservation,
+// oracle.py:118): out[0] = violations, out[1] = first violating slot.
+template <typename CapT>
+__global__ void pair_check_kernel(const CapT *cf, const CapT *pc, const int *__restrict__ rev,
+                                  int S, unsigned long long *out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
+    if ((long long)cf[i] + (long long)cf[rev[i]] != (long long)pc[i]) {
+      atomicAdd(out, 1ull);
+      atomicMin(out + 1, (unsigned long long)i);
+    }
+}
+
+cudaError_t launch_pair_check(const GraphObj &g, const StateObj &st, unsigned long long *d_out) {
+  const Topology &T = *g.topo;
+  unsigned long long init[2] = {0ull, ~0ull};
+  cudaError_t e = cudaMemcpyAsync(d_out, init, sizeof(init), cudaMemcpyHostToDevice, T.stream);
+  if (e || T.S == 0) return e;
+  if (T.cap_bytes == 8)
+    pair_check_kernel<long long><<<grid_for(T.S, T.num_sms), kBlock, 0, T.stream>>>(
+        (const long long *)st.cf, (const long long *)g.pc, T.rev, T.S, d_out);
+  else
+    pair_check_kernel<int><<<grid_for(T.S, T.num_sms), kBlock, 0, T.stream>>>(
+        (const int *)st.cf, (const int *)g.pc, T.rev, T.S, d_out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// capacities staged as int64 for set_cap0: out[0] = first negative slot,
+// out[1] = first slot whose pair sum reaches 2^31 (int32 storage only).
+__global__ void cap_check_kernel(const long long *cap, const int *__restrict__ rev, int S,
+                                 int narrow, unsigned long long *out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    long long c = cap[i];
+    if (c < 0) atomicMin(out, (unsigned long long)i);
+    else if (narrow && c + cap[rev[i]] >= (1ll << 31)) atomicMin(out + 1, (unsigned long long)i);
+  }
+}
+
+cudaError_t launch_cap_check(const Topology &T, const int64_t *d_cap, unsigned long long *d_out) {
+  unsigned long long init[2] = {~0ull, ~0ull};
+  cudaError_t e = cudaMemcpyAsync(d_out, init, sizeof(init), cudaMemcpyHostToDevice, T.stream);
+  if (e || T.S == 0) return e;
+  cap_check_kernel<<<grid_for(T.S, T.num_sms), kBlock, 0, T.stream>>>(
+      (const long long *)d_cap, T.rev, T.S, T.cap_bytes == 4, d_out);
   count_launch();
   return cudaGetLastError();
 }

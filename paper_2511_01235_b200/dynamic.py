@@ -122,6 +122,16 @@ def solve_dynamic_pushpull(st: SolverState, g: BiCsrGraph, batch: UpdateBatch,
     p = params.to_c()
     us, vs, cs = batch.arrays()
     r = L.Result()
+    if params.instrument is not None:
+        # the reference hands instrument to the final ordinary pass only
+        # (dynamic.py:366-369): device pipelines, then host-stepped rounds
+        L.check(L.load().mfx_pushpull_regions(g.handle, st.handle, us.size, L.ptr64(us),
+                                              L.ptr64(vs), L.ptr64(cs), ctypes.byref(p),
+                                              ctypes.byref(r)))
+        st._invalidate()
+        g._invalidate()
+        return _instrumented_rounds(st, g, p, params.instrument, dynamic=True,
+                                    round_base=int(r.rounds), reset=False)
     L.check(L.load().mfx_solve_dynamic_pushpull(g.handle, st.handle, us.size, L.ptr64(us),
                                                 L.ptr64(vs), L.ptr64(cs), ctypes.byref(p),
                                                 ctypes.byref(r)))

@@ -59,9 +59,10 @@ def pct_for_count(k: int, m: int) -> float:
 # graphs
 # ----------------------------------------------------------------------------
 
-def random_graph(n: int, m: int, seed: int, cap_lo: int = 1, cap_hi: int = 100):
+def random_edges(n: int, m: int, seed: int, cap_lo: int = 1, cap_hi: int = 100):
     """C1 generator; identical draws to reference bench.py:124-147.
-    Returns ``(us, vs, caps, s, t)`` as int64 arrays."""
+    Returns ``(us, vs, caps, s, t)`` as int64 arrays (the array form of
+    :func:`random_graph`)."""
     if n < 2:
         raise ValueError("need at least two vertices")
     rng = np.random.default_rng(seed)
@@ -140,7 +141,7 @@ def road_graph(w: int, h: int, seed: int = 0, p_vert: float = 0.2):
 def config_graph(name: str):
     """(n, us, vs, caps, s, t) for the named benchmark configuration."""
     if name == "C1":
-        us, vs, caps, s, t = random_graph(10000, 100000, seed=0)
+        us, vs, caps, s, t = random_edges(10000, 100000, seed=0)
         return 10000, us, vs, caps, s, t
     if name == "C2":
         us, vs, caps, s, t = grid_graph(2048, 2048, seed=0)
@@ -180,10 +181,12 @@ def _choice(rng, pool, weights, k):
     return rng.choice(pool, size=k, replace=False, p=w / w.sum()).astype(np.int64)
 
 
-def generate_batch(n, us, vs, caps, s, t, spec: BatchSpec):
+def batch_arrays(n, us, vs, caps, s, t, spec: BatchSpec):
     """Draw-for-draw reproduction of the reference sampler
-    (reference bench.py:66-121).  Returns (us, vs, new_caps, pick) sorted
-    by (u, v); ``pick`` indexes the input edge list."""
+    (reference bench.py:66-121) on edge arrays.  Returns (us, vs, new_caps,
+    pick) sorted by (u, v); ``pick`` indexes the input edge list.  Raises
+    ValueError on a non-normalized list (:func:`generate_batch` raises the
+    reference's GraphError)."""
     spec.validate()
     kind = spec.canonical_kind()
     us, vs, caps = (np.asarray(a, np.int64) for a in (us, vs, caps))
@@ -264,3 +267,96 @@ def fast_batch(n, us, vs, caps, s, t, k: int, kind: str = "mixed", seed: int = 0
     order = np.lexsort((vs[pick], us[pick]))
     pick = pick[order]
     return us[pick], vs[pick], new[order], pick
+
+
+
+def _race_smallest(rng, m, excluded, heavy, bias, cnt):
+    """The ``cnt`` smallest exponential-race keys E_i / w_i over the edges
+    [0, m) minus ``excluded`` (sorted; weight 1) plus ``heavy`` (weight
+    ``bias``), without a key per light edge: the positions of the j smallest
+    of M iid Exp(1) keys form a uniform random subset, and their values are
+    the order statistics sum_{i<=j} E_i / (M - i + 1)."""
+    M = m - excluded.size
+    c = min(cnt, M)
+    if c:
+        ranks = rng.choice(M, size=c, replace=False).astype(np.int64)
+        # rank among the non-excluded edges -> edge index
+        shift = excluded - np.arange(excluded.size, dtype=np.int64)
+        light = ranks + np.searchsorted(shift, ranks, side="right")
+        vals = np.cumsum(rng.exponential(size=c) / (M - np.arange(c, dtype=np.float64)))
+    else:
+        light, vals = np.empty(0, np.int64), np.empty(0)
+    idx = np.concatenate([light, heavy])
+    key = np.concatenate([vals, rng.exponential(size=heavy.size) / bias])
+    take = min(cnt, idx.size)
+    return idx[np.argsort(key, kind="stable")[:take]]
+
+
+def sparse_batch(n, us, vs, caps, s, t, k: int, kind: str = "mixed", seed: int = 0,
+                 bias: float = 10.0):
+    """:func:`fast_batch`'s law (the reference generate_batch semantics,
+    bench.py:66-121: k distinct edges drawn with weight ``bias`` on s-out /
+    t-in edges, half decrements on positive edges and half increments on
+    the rest) from O(k + |heavy|) random draws plus a few O(m) masks, for
+    the 58 M-edge C4 chains.  A different random stream from fast_batch."""
+    kind = KINDS[kind]
+    us, vs, caps = (np.asarray(a, np.int64) for a in (us, vs, caps))
+    m = us.size
+    k = min(k, m)
+    rng = np.random.default_rng(seed)
+    heavy = np.flatnonzero((us == s) | (vs == t))
+    dec_pick = np.empty(0, np.int64)
+    if kind in ("dec", "mixed"):
+        zero = np.flatnonzero(caps <= 0)
+        excl = np.union1d(heavy, zero)
+        hpos = heavy[caps[heavy] > 0]
+        dec_pick = _race_smallest(rng, m, excl, hpos, bias, k if kind == "dec" else k // 2)
+    if kind == "dec":
+        pick = dec_pick
+        new = _dec(rng, caps[pick])
+    else:
+        excl = np.union1d(heavy, dec_pick)
+        hrest = np.setdiff1d(heavy, dec_pick, assume_unique=True)
+        inc_pick = _race_smallest(rng, m, excl, hrest, bias, k - dec_pick.size)
+        pick = np.concatenate([dec_pick, inc_pick])
+        new = np.concatenate([_dec(rng, caps[dec_pick]), _inc(rng, caps[inc_pick])])
+    order = np.lexsort((vs[pick], us[pick]))
+    pick = pick[order]
+    return us[pick], vs[pick], new[order], pick
+
+
+# ----------------------------------------------------------------------------
+# reference-signature entry points (reference bench.py:66-147)
+# ----------------------------------------------------------------------------
+
+def random_graph(n: int, m: int, seed: int, cap_lo: int = 1, cap_hi: int = 100):
+    """Reference ``random_graph`` (bench.py:124-147): returns
+    ``(EdgeListGraph, s, t)`` with identical draws."""
+    from .graph import EdgeListGraph
+    us, vs, caps, s, t = random_edges(n, m, seed, cap_lo, cap_hi)
+    return EdgeListGraph(n, us, vs, caps), s, t
+
+
+def generate_batch(g, s: int, t: int, spec: BatchSpec):
+    """Reference ``generate_batch`` (bench.py:66-121): ``g`` is a normalized
+    EdgeListGraph (e.g. ``BiCsrGraph.to_edge_list()``); returns an
+    UpdateBatch, draw for draw the reference's; GraphError on a
+    non-normalized list."""
+    from .dynamic import UpdateBatch
+    from .graph import GraphError
+    try:
+        bu, bv, bc, _ = batch_arrays(g.n, g.us, g.vs, g.caps, s, t, spec)
+    except ValueError as e:
+        if "normalized" in str(e):
+            raise GraphError("generate_batch expects a normalized edge list "
+                             "(unique directed pairs)") from None
+        raise
+    return UpdateBatch(bu, bv, bc)
+
+
+def source_edges(name: str, args):
+    """Edge arrays of a named generator as recorded in the golden fixtures
+    (``random_graph`` there means the reference generator's draws)."""
+    if name == "random_graph":
+        return random_edges(*args)
+    return globals()[name](*args)

@@ -129,6 +129,8 @@ class BiCsrGraph:
                                                 L.ptr64(src), L.ptr64(rev), None, L.ptr8(orig)))
             self._topo_cache = {"offsets": off, "adj": adj, "src": src, "rev": rev,
                                 "is_original": orig.astype(bool)}
+            for arr in self._topo_cache.values():
+                arr.setflags(write=False)
         return self._topo_cache
 
     @property
@@ -153,12 +155,13 @@ class BiCsrGraph:
 
     @property
     def cap0(self):
-        """Current capacities (a downloaded snapshot; use :meth:`set_cap0` to
-        write)."""
+        """Current capacities: a read-only downloaded snapshot (the device
+        copy is the truth; write through :meth:`set_cap0`)."""
         if self._cap0_cache is None:
             c = np.empty(self.m, np.int64)
             L.check(L.load().mfx_graph_download(self.handle, None, None, None, None,
                                                 L.ptr64(c), None))
+            c.setflags(write=False)  # a snapshot: in-place writes would be lost, so they raise
             self._cap0_cache = c
         return self._cap0_cache
 

@@ -16,7 +16,7 @@ import statistics
 import time
 
 from .dynamic import UpdateBatch, solve_dynamic, solve_dynamic_pushpull, updated_edge_list
-from .gen import BatchSpec, generate_batch
+from .gen import BatchSpec, batch_arrays
 from .graph import EdgeListGraph, build_bicsr
 from .io import ResultRecord
 from .solver import SolverParams, solve_static
@@ -58,7 +58,7 @@ def run_benchmark(g: EdgeListGraph, s: int, t: int, specs: list[BatchSpec],
     prior = solve_static(csr, s, t, params)
     out = []
     for spec in specs:
-        batch = UpdateBatch(*generate_batch(el.n, el.us, el.vs, el.caps, s, t, spec)[:3])
+        batch = UpdateBatch(*batch_arrays(el.n, el.us, el.vs, el.caps, s, t, spec)[:3])
         runs = {m: _time_mode(m, csr, prior, batch, s, t, params, reps) for m in BENCH_MODES}
         agree = len({r[2] for r in runs.values()}) == 1
         for m in BENCH_MODES:

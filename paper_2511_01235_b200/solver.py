@@ -192,26 +192,31 @@ def _validate_endpoints(g: BiCsrGraph, source: int, sink: int) -> None:
 
 
 def _instrumented_rounds(st: SolverState, g: BiCsrGraph, p: L.Params, instrument,
-                         dynamic: bool) -> FlowResult:
-    """Host-stepped variant of the device round loop (solver.py:204-241)."""
+                         dynamic: bool, round_base: int = 0, reset: bool = True) -> FlowResult:
+    """Host-stepped variant of the device round loop (solver.py:204-241):
+    static rounds relabel from {t} with nothing forbidden, dynamic ones from
+    {t} U deficient with s forbidden.  ``round_base``/``reset``: continue the
+    counters of an earlier device phase (push-pull's final pass)."""
     lib = L.load()
     active = ctypes.c_int64()
     r = L.Result()
-    rnd = 0
-    first = 0x10
+    rnd = round_base
+    first = 0x10 if reset else 0
+    dyn = 1 if dynamic else 0
     while True:
-        L.check(lib.mfx_step(g.handle, st.handle, ctypes.byref(p), 0 | first, 1,
+        L.check(lib.mfx_step(g.handle, st.handle, ctypes.byref(p), 0 | first, dyn,
                              ctypes.byref(active), ctypes.byref(r)))
         first = 0
         st._invalidate()
         instrument(st, g, rnd, "bfs")
         if active.value == 0:
             break
-        L.check(lib.mfx_step(g.handle, st.handle, ctypes.byref(p), 1, 1, None, ctypes.byref(r)))
+        L.check(lib.mfx_step(g.handle, st.handle, ctypes.byref(p), 1, dyn, None,
+                             ctypes.byref(r)))
         st._invalidate()
         instrument(st, g, rnd, "repair")
         rnd += 1
-    L.check(lib.mfx_step(g.handle, st.handle, ctypes.byref(p), 2, 1, None, ctypes.byref(r)))
+    L.check(lib.mfx_step(g.handle, st.handle, ctypes.byref(p), 2, dyn, None, ctypes.byref(r)))
     res = _result(r, st, g)
     if res.flow_value != res.certificate.cut_capacity:
         raise SolverError(f"flow {res.flow_value} does not match cut capacity "

@@ -51,6 +51,8 @@ class SolverState:
             ex = np.empty(g.n, np.int64)
             h = np.empty(g.n, np.int64)
             L.check(L.load().mfx_state_download(self.handle, L.ptr64(cf), L.ptr64(ex), L.ptr64(h)))
+            for arr in (cf, ex, h):  # snapshots of device memory: write through upload()
+                arr.setflags(write=False)
             self._cache = (cf, ex, h)
         return self._cache
 

@@ -11,8 +11,9 @@
 #   bench[:ARGS]     python bench.py ARGS (default: the C4 headline)
 #   ref[:ARGS]       python bench.py --impl reference ARGS
 #   sweep:ARGS       python scripts/sweep.py ARGS
-#   ncu_c4 / ncu_c2  ncu --set full of one solve_kernel launch (bench --profile batch) -> .ncu-rep
-#   launches_c4      ncu launch list (gpu__time_duration.sum) of bench.py --profile
+#   ncu_<cfg>        ncu --set full of the first timed solve_kernel launch of bench.py --profile
+#                    (NVTX range "timed") -> .ncu-rep (summarise here: scripts/ncu_summary.py)
+#   launches_<cfg>   ncu launch list (gpu__time_duration.sum) of bench.py --profile
 #   sanitize         compute-sanitizer memcheck + synccheck over the parity tests
 #   cmd:SHELL        any shell command
 set -x
@@ -32,12 +33,13 @@ for task in "$@"; do
     bench)    eval "timeout 1200 python bench.py $args" > "$log" 2>&1 ;;
     ref)      eval "timeout 1500 python bench.py --impl reference $args" > "$log" 2>&1 ;;
     sweep)    eval "MFX_TIMEOUT_S=300 timeout 1500 python scripts/sweep.py $args" > "$log" 2>&1 ;;
-    ncu_c4)   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:solve_kernel \
-                -s 1 -c 1 -o gpurun_out/prof_C4_dyn python bench.py --profile --steps 1 --warmup 3 $args > "$log" 2>&1 ;;
-    ncu_c2)   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:solve_kernel \
-                -s 1 -c 1 -o gpurun_out/prof_C2_dyn python bench.py --config C2 --profile --steps 1 --warmup 3 $args > "$log" 2>&1 ;;
-    launches_c4) timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-                --log-file gpurun_out/launches_C4.csv python bench.py --profile --steps 3 --warmup 3 $args > "$log" 2>&1 ;;
+    ncu_*)    cfg=$(echo "${name#ncu_}" | tr a-z A-Z)
+              timeout 1500 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" \
+                -k regex:^solve_kernel -c 1 -f -o gpurun_out/prof_${cfg}_dyn \
+                python bench.py --config $cfg --profile --steps 1 --warmup 3 $args > "$log" 2>&1 ;;
+    launches_*) cfg=$(echo "${name#launches_}" | tr a-z A-Z)
+              timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+                --log-file gpurun_out/launches_${cfg}.csv python bench.py --config $cfg --profile --steps 3 --warmup 3 $args > "$log" 2>&1 ;;
     sanitize) timeout 2400 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest -x -q -m gpu \
                 tests/test_gpu_parity.py -k "bit_exact or random" > "$log" 2>&1
               timeout 2400 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest -x -q -m gpu \

@@ -34,7 +34,7 @@ def instance(kind, side, scale):
         us, vs, caps, s, t = gen.road_graph(side, side, 0, 0.21)
         return side * side, us, vs, caps, s, t
     if kind == "random":
-        us, vs, caps, s, t = gen.random_graph(10000, 100000, 0)
+        us, vs, caps, s, t = gen.random_edges(10000, 100000, 0)
         return 10000, us, vs, caps, s, t
     raise ValueError(kind)
 

@@ -22,7 +22,7 @@ def main():
     dist.init_process_group("gloo", rank=rank, world_size=2)
     G = load()
     rec = G.rec["grid64"]
-    us, vs, caps, s, t = getattr(gen, rec["source"]["gen"])(*rec["source"]["args"])
+    us, vs, caps, s, t = gen.source_edges(rec["source"]["gen"], rec["source"]["args"])
     n = rec["n"]
     pg = partition.PartitionedGraph(n, us, vs, caps, s, t, partition.TorchGroup(device=0))
     flows = [pg.solve_static().flow_value]
@@ -31,7 +31,7 @@ def main():
     keep = g.is_original.astype(bool)
     for e in rec["chain"]:
         spec = gen.BatchSpec(e["pct"], e["kind"], e["seed"])
-        bu, bv, bc, _ = gen.generate_batch(n, g.src[keep], g.adj[keep], cap0[keep], s, t, spec)
+        bu, bv, bc, _ = gen.batch_arrays(n, g.src[keep], g.adj[keep], cap0[keep], s, t, spec)
         flows.append(pg.solve_dynamic(mf.UpdateBatch(bu, bv, bc)).flow_value)
         cap0[g.edge_indices(bu, bv)] = bc
     with open(out, "w") as fh:

@@ -31,16 +31,20 @@ def mf():
 
 
 def instance(rec):
-    us, vs, caps, s, t = getattr(gen, rec["gen"])(*rec["args"])
+    us, vs, caps, s, t = gen.source_edges(rec["gen"], rec["args"])
     assert (s, t) == (rec["s"], rec["t"])
     return rec["n"], us, vs, caps, s, t
 
 
 @pytest.mark.parametrize("name", NAMES)
-def test_reference_flows_full_size(mf, name):
+@pytest.mark.parametrize("wide", [False, True])
+def test_reference_flows_full_size(mf, name, wide):
+    """``wide``: the same chains on int64 residual storage (both solve-kernel
+    builds: v256 on the grids / roads, v512 on R-MAT)."""
     rec = LARGE[name]
     n, us, vs, caps, s, t = instance(rec)
-    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps), wide=wide)
+    assert g.cap_bytes == (8 if wide else 4)
     assert (g.m, g.m_original) == (rec["S"], rec["m_original"])
     res = mf.solve_static(g, s, t)
     assert res.flow_value == rec["static_flow"] == res.certificate.cut_capacity
@@ -58,13 +62,13 @@ def test_reference_flows_full_size(mf, name):
         st = r.state
 
 
-@pytest.mark.parametrize("side,batches", [(4900, 2)])
-def test_c4_road_dynamic_equals_static_resolve(mf, side, batches):
+@pytest.mark.parametrize("side,batches,wide", [(4900, 3, False), (4900, 2, True)])
+def test_c4_road_dynamic_equals_static_resolve(mf, side, batches, wide):
     """C4 (road, 24 M vertices, BFS depth ~10^4): no CPU ground truth, so
     dynamic == GPU static re-solve after every batch, both certified."""
     us, vs, caps, s, t = gen.road_graph(side, side, 0, 0.21)
     n = side * side
-    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps), wide=wide)
     res = mf.solve_static(g, s, t)
     assert res.flow_value == res.certificate.cut_capacity
     el = g.to_edge_list()

@@ -31,14 +31,14 @@ def instance(name):
         return (rec["n"], G.arr[f"{name}/in_us"], G.arr[f"{name}/in_vs"],
                 G.arr[f"{name}/in_caps"], rec["s"], rec["t"])
     src = rec["source"]
-    us, vs, caps, s, t = getattr(gen, src["gen"])(*src["args"])
+    us, vs, caps, s, t = gen.source_edges(src["gen"], src["args"])
     return rec["n"], us, vs, caps, s, t
 
 
 def chain_batch(g_src, g_adj, g_orig, cap0, n, s, t, entry):
     keep = g_orig.astype(bool)
     spec = gen.BatchSpec(entry["pct"], entry["kind"], entry["seed"])
-    bu, bv, bc, _ = gen.generate_batch(n, g_src[keep], g_adj[keep], cap0[keep], s, t, spec)
+    bu, bv, bc, _ = gen.batch_arrays(n, g_src[keep], g_adj[keep], cap0[keep], s, t, spec)
     return bu, bv, bc
 
 
@@ -58,9 +58,10 @@ def test_build_bit_exact(mf, name, wide):
 
 
 @pytest.mark.parametrize("name", SMALL)
-def test_saturate_and_global_relabel_bit_exact(mf, name):
+@pytest.mark.parametrize("wide", [False, True])
+def test_saturate_and_global_relabel_bit_exact(mf, name, wide):
     n, us, vs, caps, s, t = instance(name)
-    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps), wide=wide)
     st = mf.init_residuals(g, s, t)
     mf.saturate_source(st, g)
     assert np.array_equal(st.cf, G.arr[f"{name}/sat_cf"])
@@ -70,7 +71,8 @@ def test_saturate_and_global_relabel_bit_exact(mf, name):
 
 
 @pytest.mark.parametrize("name", SMALL)
-def test_dynamic_prephase_and_bfs_bit_exact(mf, name):
+@pytest.mark.parametrize("wide", [False, True])
+def test_dynamic_prephase_and_bfs_bit_exact(mf, name, wide):
     """Given the reference's terminated state, the fused device pre-phase
     equals apply_updates + recompute_excess + saturate_source byte for byte,
     and the dynamic global relabel equals backward_bfs_dynamic."""
@@ -79,7 +81,9 @@ def test_dynamic_prephase_and_bfs_bit_exact(mf, name):
     for bi, entry in enumerate(rec["chain"]):
         a = lambda k: G.arr[f"{name}/b{bi}/{k}"]  # noqa: E731
         g = mf.upload_bicsr(n, G.arr[f"{name}/offsets"], G.arr[f"{name}/adj"],
-                            G.arr[f"{name}/rev"], a("prior_cap0"), G.arr[f"{name}/is_original"])
+                            G.arr[f"{name}/rev"], a("prior_cap0"), G.arr[f"{name}/is_original"],
+                            wide=wide)
+        assert g.cap_bytes == (8 if wide else 4)
         st = mf.init_residuals(g, s, t)
         st.upload(a("prior_cf"), a("prior_excess"), a("prior_height"))
         mf.dynamic_prephase(st, g, mf.UpdateBatch(a("us"), a("vs"), a("caps")))
@@ -114,12 +118,15 @@ def test_prephase_bit_exact_from_oracle_state(mf, name):
 
 
 @pytest.mark.parametrize("name", CASES)
-def test_static_and_chained_dynamic_flows(mf, name):
+@pytest.mark.parametrize("wide", [False, True])
+def test_static_and_chained_dynamic_flows(mf, name, wide):
     """Flow and cut after the static solve and after every chained batch
-    equal the reference's; the device verifier passes each time."""
+    equal the reference's; the device verifier passes each time.  ``wide``
+    runs the int64-residual builds of the solve kernel and pre-phase."""
     rec = G.rec[name]
     n, us, vs, caps, s, t = instance(name)
-    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps), wide=wide)
+    assert g.cap_bytes == (8 if wide else 4)
     res = mf.solve_static(g, s, t)
     assert res.flow_value == rec["static_flow"]
     assert res.certificate.cut_capacity == res.flow_value
@@ -135,7 +142,7 @@ def test_static_and_chained_dynamic_flows(mf, name):
         rep = mf.verify_gpu(r.state, g, r.flow_value)
         assert rep.ok, rep.problems
         # GPU static re-solve on the updated capacities agrees
-        g2 = mf.build_bicsr(g.to_edge_list())
+        g2 = mf.build_bicsr(g.to_edge_list(), wide=wide)
         assert mf.solve_static(g2, s, t).flow_value == entry["flow"]
         st = r.state
 
@@ -255,7 +262,7 @@ def test_random_vs_oracle(mf, seed):
     rng = np.random.default_rng(1000 + seed)
     n = int(rng.integers(2, 400))
     m = int(rng.integers(1, 4000))
-    us, vs, caps, s, t = gen.random_graph(n, m, seed)
+    us, vs, caps, s, t = gen.random_edges(n, m, seed)
     knobs = [dict(), dict(kernel_cycles=1), dict(kernel_cycles=64), dict(mode="topology"),
              dict(max_waves=1), dict(max_waves=3, kernel_cycles=2),
              dict(schedule="async"), dict(schedule="async", async_budget=1),
@@ -270,7 +277,7 @@ def test_random_vs_oracle(mf, seed):
     st = res.state
     for j, (kind, pct) in enumerate([("inc", 5.0), ("dec", 10.0), ("mixed", 25.0), ("mixed", 1.0)]):
         el_us, el_vs, el_caps = og.src[og.is_original], og.adj[og.is_original], og.cap0[og.is_original]
-        bu, bv, bc, _ = gen.generate_batch(n, el_us, el_vs, el_caps, s, t,
+        bu, bv, bc, _ = gen.batch_arrays(n, el_us, el_vs, el_caps, s, t,
                                            gen.BatchSpec(pct, kind, seed * 10 + j))
         r = mf.solve_dynamic(st, g, mf.UpdateBatch(bu, bv, bc), params)
         orr = O.solve_dynamic(og, ost, bu, bv, bc)
@@ -283,7 +290,7 @@ def test_random_vs_oracle(mf, seed):
 def test_instrument_invariants(mf):
     """SPEC acceptance 4 on the device path: at every round boundary cf >= 0,
     residual-sum conservation, sum(excess) == 0."""
-    us, vs, caps, s, t = gen.random_graph(80, 600, 5)
+    us, vs, caps, s, t = gen.random_edges(80, 600, 5)
     g = mf.build_bicsr(mf.EdgeListGraph(80, us, vs, caps))
     seen = []
 
@@ -299,20 +306,20 @@ def test_instrument_invariants(mf):
     assert res.flow_value == O.solve_static(og, s, t)[0].flow
     assert seen and seen[0] == (0, "bfs")
     el = g.to_edge_list()
-    bu, bv, bc, _ = gen.generate_batch(80, el.us, el.vs, el.caps, s, t, gen.BatchSpec(20.0, "mixed", 1))
+    bu, bv, bc, _ = gen.batch_arrays(80, el.us, el.vs, el.caps, s, t, gen.BatchSpec(20.0, "mixed", 1))
     r = mf.solve_dynamic(res.state, g, mf.UpdateBatch(bu, bv, bc), mf.SolverParams(instrument=hook))
     g2 = mf.build_bicsr(g.to_edge_list())
     assert r.flow_value == mf.solve_static(g2, s, t).flow_value
 
 
 def test_state_copy_and_graph_copy_semantics(mf):
-    us, vs, caps, s, t = gen.random_graph(300, 3000, 9)
+    us, vs, caps, s, t = gen.random_edges(300, 3000, 9)
     g = mf.build_bicsr(mf.EdgeListGraph(300, us, vs, caps))
     res = mf.solve_static(g, s, t)
     snap_st, snap_g = res.state.copy(), g.copy()
     cap_before = g.cap0.copy()
     el = g.to_edge_list()
-    bu, bv, bc, _ = gen.generate_batch(300, el.us, el.vs, el.caps, s, t, gen.BatchSpec(10.0, "dec", 2))
+    bu, bv, bc, _ = gen.batch_arrays(300, el.us, el.vs, el.caps, s, t, gen.BatchSpec(10.0, "dec", 2))
     r1 = mf.solve_dynamic(res.state, g, mf.UpdateBatch(bu, bv, bc))
     # the snapshot is untouched and can replay the same batch
     assert np.array_equal(snap_g.cap0, cap_before)
@@ -327,7 +334,7 @@ def test_state_copy_and_graph_copy_semantics(mf):
 
 
 def test_edge_indices_and_reverse(mf):
-    us, vs, caps, s, t = gen.random_graph(50, 300, 4)
+    us, vs, caps, s, t = gen.random_edges(50, 300, 4)
     g = mf.build_bicsr(mf.EdgeListGraph(50, us, vs, caps))
     idx = g.edge_indices(g.src, g.adj)
     assert np.array_equal(idx, np.arange(g.m))

@@ -43,14 +43,14 @@ def instance(name):
         return (rec["n"], G.arr[f"{name}/in_us"], G.arr[f"{name}/in_vs"],
                 G.arr[f"{name}/in_caps"], rec["s"], rec["t"])
     src = rec["source"]
-    us, vs, caps, s, t = getattr(gen, src["gen"])(*src["args"])
+    us, vs, caps, s, t = gen.source_edges(src["gen"], src["args"])
     return rec["n"], us, vs, caps, s, t
 
 
 def chain_batch(g_src, g_adj, g_orig, cap0, n, s, t, entry):
     keep = g_orig.astype(bool)
     spec = gen.BatchSpec(entry["pct"], entry["kind"], entry["seed"])
-    bu, bv, bc, _ = gen.generate_batch(n, g_src[keep], g_adj[keep], cap0[keep], s, t, spec)
+    bu, bv, bc, _ = gen.batch_arrays(n, g_src[keep], g_adj[keep], cap0[keep], s, t, spec)
     return bu, bv, bc
 
 

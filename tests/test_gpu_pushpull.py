@@ -28,7 +28,7 @@ def instance(name):
         return (rec["n"], G.arr[f"{name}/in_us"], G.arr[f"{name}/in_vs"],
                 G.arr[f"{name}/in_caps"], rec["s"], rec["t"])
     src = rec["source"]
-    us, vs, caps, s, t = getattr(gen, src["gen"])(*src["args"])
+    us, vs, caps, s, t = gen.source_edges(src["gen"], src["args"])
     return rec["n"], us, vs, caps, s, t
 
 
@@ -43,7 +43,7 @@ def test_pushpull_chain_matches_reference(mf, name, interleave):
     keep = g.is_original.astype(bool)
     for j, entry in enumerate(rec["chain"]):
         spec = gen.BatchSpec(entry["pct"], entry["kind"], entry["seed"])
-        bu, bv, bc, _ = gen.generate_batch(n, g.src[keep], g.adj[keep], g.cap0[keep], s, t, spec)
+        bu, bv, bc, _ = gen.batch_arrays(n, g.src[keep], g.adj[keep], g.cap0[keep], s, t, spec)
         fn = mf.solve_dynamic if (interleave and j % 2) else mf.solve_dynamic_pushpull
         r = fn(st, g, mf.UpdateBatch(bu, bv, bc))
         assert r.flow_value == entry["flow"] == r.certificate.cut_capacity, (name, j)

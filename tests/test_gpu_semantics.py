@@ -1,0 +1,244 @@
+"""Drop-in semantics on the device path that round 1 left untested or got
+wrong (ADVICE.md / VERDICT.md round 1):
+
+* int32 residual storage admits every batch whose post-batch pair sums fit
+  (the reference accepts any non-negative int64 capacity);
+* states solved against other capacities are detected, not silently reused;
+* downloaded arrays are read-only snapshots (writes would be lost);
+* the device operation ceiling and the watchdog fire with the reference's
+  exception classes;
+* O2 push-pull hands ``instrument`` to its final ordinary pass;
+* two host threads on one graph topology are serialised;
+* the BFS ring's polled work queue gives bit-exact heights under repeated,
+  randomly re-parameterised runs.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2511_01235_b200 import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mf():
+    import paper_2511_01235_b200 as m
+    return m
+
+
+def small(mf, n=300, m=3000, seed=9, wide=False):
+    us, vs, caps, s, t = gen.random_edges(n, m, seed)
+    return mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps), wide=wide), s, t
+
+
+# ---------------------------------------------------------------------------
+def test_int32_storage_accepts_pair_sums_below_2_31(mf):
+    """A 1.5e9 edge with a zero-capacity reverse stub keeps int32 storage;
+    re-applying that capacity (or anything whose pair sum stays < 2^31) is
+    accepted as the reference accepts it; a pair sum >= 2^31 is refused
+    with a ValueError naming the update, and nothing is applied."""
+    big = 1_500_000_000
+    el = mf.EdgeListGraph.from_edges(4, [(0, 1, big), (1, 3, 7), (0, 2, 5), (2, 3, 9), (2, 1, 4)])
+    g = mf.build_bicsr(el)
+    assert g.cap_bytes == 4
+    r = mf.solve_static(g, 0, 3)
+    assert r.flow_value == 16
+    r = mf.solve_dynamic(r.state, g, mf.UpdateBatch.from_updates([(0, 1, big), (1, 3, 2**31 - 8)]))
+    assert r.flow_value == O.solve_static(O.build_bicsr(4, [0, 1, 0, 2, 2], [1, 3, 2, 3, 1],
+                                                        [big, 2**31 - 8, 5, 9, 4]), 0, 3)[0].flow
+    cap_before = g.cap0.copy()
+    with pytest.raises(ValueError, match="update 1 .*overflows the int32"):
+        mf.solve_dynamic(r.state, g, mf.UpdateBatch.from_updates([(0, 2, 3), (2, 3, 2**31)]))
+    assert np.array_equal(g.cap0, cap_before)
+    # both directions of a pair in one batch: the partner's NEW capacity counts
+    el2 = mf.EdgeListGraph.from_edges(3, [(0, 1, 10), (1, 0, 10), (1, 2, 10)])
+    g2 = mf.build_bicsr(el2)
+    r2 = mf.solve_static(g2, 0, 2)
+    ok = mf.solve_dynamic(r2.state, g2, mf.UpdateBatch.from_updates(
+        [(0, 1, 2**30), (1, 0, 2**30 - 1)]))
+    assert ok.flow_value == 10
+    with pytest.raises(ValueError, match="overflows the int32"):
+        mf.solve_dynamic(ok.state, g2, mf.UpdateBatch.from_updates([(0, 1, 2**30), (1, 0, 2**30)]))
+
+
+def test_set_cap0_pair_sum_check(mf):
+    g, s, t = small(mf, 50, 300, 4)
+    c = np.array(g.cap0)
+    c[0] = 2**31 - 1 - c[int(g.rev[0])] + 1  # pair sum exactly 2^31
+    with pytest.raises(ValueError, match="overflows the int32"):
+        g.set_cap0(c)
+    c = np.array(g.cap0)
+    c[3] = -1
+    with pytest.raises(mf.GraphError, match="negative capacity"):
+        g.set_cap0(c)
+
+
+def test_state_solved_against_other_capacities_is_detected(mf):
+    """set_cap0 (or a batch applied through another state on the same graph)
+    leaves older states inconsistent with the capacities: the next use
+    rejects them with SolverError instead of reusing stale excess."""
+    g, s, t = small(mf)
+    r = mf.solve_static(g, s, t)
+    st = r.state
+    c = np.array(g.cap0)
+    orig = np.flatnonzero(g.is_original)
+    c[orig[:40]] += 5
+    g.set_cap0(c)
+    el = g.to_edge_list()
+    bu, bv, bc, _ = gen.batch_arrays(g.n, el.us, el.vs, el.caps, s, t,
+                                     gen.BatchSpec(5.0, "mixed", 3))
+    with pytest.raises(mf.SolverError, match="do not match the graph's capacities"):
+        mf.solve_dynamic(st, g, mf.UpdateBatch(bu, bv, bc))
+    # a state re-solved on the new capacities chains normally
+    r2 = mf.solve_static(g, s, t)
+    r3 = mf.solve_dynamic(r2.state, g, mf.UpdateBatch(bu, bv, bc))
+    g_ref = mf.build_bicsr(g.to_edge_list())
+    assert r3.flow_value == mf.solve_static(g_ref, s, t).flow_value
+    # two states on one graph: a batch through one makes the other stale
+    ra, rb = mf.solve_static(g, s, t), mf.solve_static(g, s, t)
+    el = g.to_edge_list()
+    b6 = gen.batch_arrays(g.n, el.us, el.vs, el.caps, s, t, gen.BatchSpec(5.0, "mixed", 6))[:3]
+    mf.solve_dynamic(ra.state, g, mf.UpdateBatch(*b6))
+    el = g.to_edge_list()
+    bu2, bv2, bc2, _ = gen.batch_arrays(g.n, el.us, el.vs, el.caps, s, t,
+                                        gen.BatchSpec(5.0, "dec", 4))
+    with pytest.raises(mf.SolverError):
+        mf.solve_dynamic(rb.state, g, mf.UpdateBatch(bu2, bv2, bc2))
+    # ...while a graph copy (same capacity contents) keeps a snapshot usable
+    g3, s3, t3 = small(mf, 200, 2000, 11)
+    r = mf.solve_static(g3, s3, t3)
+    snap_g, snap_st = g3.copy(), r.state.copy()
+    el = g3.to_edge_list()
+    b = gen.batch_arrays(g3.n, el.us, el.vs, el.caps, s3, t3, gen.BatchSpec(5.0, "mixed", 1))[:3]
+    f1 = mf.solve_dynamic(r.state, g3, mf.UpdateBatch(*b)).flow_value
+    assert mf.solve_dynamic(snap_st, snap_g, mf.UpdateBatch(*b)).flow_value == f1
+
+
+def test_downloaded_arrays_are_read_only(mf):
+    g, s, t = small(mf, 60, 400, 2)
+    r = mf.solve_static(g, s, t)
+    for a in (r.state.cf, r.state.excess, r.state.height, g.cap0, g.rev, g.offsets):
+        with pytest.raises(ValueError):
+            a[0] = 1
+    # writes go through the explicit upload / set_cap0 paths
+    c = np.array(g.cap0)
+    c[np.flatnonzero(g.is_original)[0]] += 1
+    g.set_cap0(c)
+    assert np.array_equal(g.cap0, c)
+
+
+def test_operation_ceiling_and_watchdog(mf, monkeypatch):
+    """SolverError with the reference's text once pushes + relabels pass the
+    ceiling (solver.py:196-201); the watchdog raises DeviceTimeout."""
+    g, s, t = small(mf, 400, 4000, 5)
+    monkeypatch.setenv("MFX_CEILING", "10")
+    with pytest.raises(mf.SolverError, match="exceeded the termination ceiling 10"):
+        mf.solve_static(g, s, t)
+    monkeypatch.delenv("MFX_CEILING")
+    assert mf.solve_static(g, s, t).flow_value > 0
+    us, vs, caps, s2, t2 = gen.road_graph(256, 256, 0, 0.21)
+    g2 = mf.build_bicsr(mf.EdgeListGraph(256 * 256, us, vs, caps))
+    with pytest.raises(mf.DeviceTimeout):
+        mf.solve_static(g2, s2, t2, mf.SolverParams(timeout_s=1e-5))
+    # the library stays usable afterwards
+    assert mf.solve_static(g2, s2, t2).flow_value == mf.solve_static(g2, s2, t2).flow_value
+
+
+def test_pushpull_instrument_final_pass(mf):
+    g, s, t = small(mf, 300, 3000, 21)
+    r = mf.solve_static(g, s, t)
+    el = g.to_edge_list()
+    b = mf.generate_batch(el, s, t, mf.BatchSpec(10.0, "mixed", 5))
+    seen = []
+
+    def hook(st, gg, rnd, label):
+        cf = st.cf
+        assert (cf >= 0).all() and st.excess.sum() == 0
+        seen.append((rnd, label))
+
+    snap_g, snap_st = g.copy(), r.state.copy()
+    rp = mf.solve_dynamic_pushpull(r.state, g, b, mf.SolverParams(instrument=hook))
+    assert seen and seen[-1][1] == "bfs"
+    ref = mf.solve_dynamic(snap_st, snap_g, b)
+    assert rp.flow_value == ref.flow_value == rp.certificate.cut_capacity
+    assert mf.verify_gpu(rp.state, g, rp.flow_value).ok
+
+
+def test_threads_on_one_topology_are_serialised(mf):
+    """Graph copies share the topology's workspace and stream: concurrent
+    host threads (ctypes releases the GIL) must still get exact results."""
+    g, s, t = small(mf, 2000, 20000, 3)
+    want = mf.solve_static(g, s, t).flow_value
+    el = g.to_edge_list()
+    batches = [gen.batch_arrays(g.n, el.us, el.vs, el.caps, s, t,
+                                gen.BatchSpec(2.0, "mixed", i))[:3] for i in range(4)]
+    resolve = []
+    for b in batches:
+        gg = g.copy()
+        rr = mf.solve_static(gg, s, t)
+        resolve.append(mf.solve_dynamic(rr.state, gg, mf.UpdateBatch(*b)).flow_value)
+    out, errs = {}, []
+
+    def work(i):
+        try:
+            gg = g.copy()
+            for _ in range(3):
+                r = mf.solve_static(gg, s, t)
+                assert r.flow_value == want
+            out[i] = mf.solve_dynamic(r.state, gg, mf.UpdateBatch(*batches[i])).flow_value
+        except BaseException as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    assert [out[i] for i in range(4)] == resolve
+
+
+@pytest.mark.parametrize("kind,arg", [("grid", 64), ("rmat", 12), ("road", 48)])
+def test_bfs_ring_stress_bit_exact(mf, kind, arg, monkeypatch):
+    """The CTA-local BFS ring is a polled work queue (racecheck cannot prove
+    it): 50 device global relabels per case, each under a random ring sleep,
+    ring capacity and local depth, on a static state right after saturation
+    and on a terminated dynamic state; every height array equals the
+    oracle's FIFO BFS (kernels.py:168-215) byte for byte."""
+    if kind == "grid":
+        us, vs, caps, s, t = gen.grid_graph(arg, arg, 0)
+        n = arg * arg + 2
+    elif kind == "rmat":
+        us, vs, caps, s, t = gen.rmat_graph(arg, 16, 0)
+        n = 1 << arg
+    else:
+        us, vs, caps, s, t = gen.road_graph(arg, arg, 0, 0.21)
+        n = arg * arg
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    og = O.build_bicsr(n, us, vs, caps)
+    rng = np.random.default_rng(7)
+    # static: saturated fresh state, bases {t}
+    st0 = mf.init_residuals(g, s, t)
+    mf.saturate_source(st0, g)
+    want0, _ = O.bfs_heights(og, np.asarray(st0.cf, np.int64), [t], -1)
+    # dynamic: terminated state after one batch, bases {t} U deficient, s forbidden
+    r = mf.solve_static(g, s, t)
+    el = g.to_edge_list()
+    b = gen.batch_arrays(n, el.us, el.vs, el.caps, s, t, gen.BatchSpec(5.0, "mixed", 2))[:3]
+    st1 = mf.solve_dynamic(r.state, g, mf.UpdateBatch(*b)).state
+    ex = np.asarray(st1.excess)
+    bases = [v for v in range(n) if v == t or (v != s and ex[v] < 0)]
+    og.cap0[:] = np.asarray(g.cap0)
+    want1, _ = O.bfs_heights(og, np.asarray(st1.cf, np.int64), bases, s)
+    for i in range(50):
+        monkeypatch.setenv("MFX_RING_SLEEP", str(int(rng.integers(0, 1001))))
+        monkeypatch.setenv("MFX_LQ_CAP", str(int(rng.choice([64, 256, 1024, 2048]))))
+        monkeypatch.setenv("MFX_BFS_LOCAL", str(int(rng.choice([-1, 1, 8, 32, 128, 512]))))
+        monkeypatch.setenv("MFX_BFS_LOCAL_MAX", str(int(rng.choice([4, 64, 1 << 20]))))
+        mf.backward_bfs(st0, g)
+        assert np.array_equal(st0.height, want0), (i, kind)
+        mf.backward_bfs_dynamic(st1, g)
+        assert np.array_equal(st1.height, want1), (i, kind)

@@ -60,7 +60,7 @@ def test_parse_error_attributes_and_missing_file(tmp_path):
 
 def test_write_then_parse_round_trip(tmp_path):
     from paper_2511_01235_b200 import EdgeListGraph, UpdateBatch, gen
-    us, vs, caps, s, t = gen.random_graph(300, 3000, seed=5)
+    us, vs, caps, s, t = gen.random_edges(300, 3000, seed=5)
     p = tmp_path / "g.max"
     mio.write_graph(p, EdgeListGraph(300, us, vs, caps), s, t)
     g, s2, t2 = mio.parse_graph(p)
@@ -104,8 +104,7 @@ def test_run_benchmark_schema_and_plot_data(tmp_path):
     """Reference bench.py run_benchmark schema on the GPU engine: three modes
     per spec, identical verified flows, gnuplot tables per kind."""
     import paper_2511_01235_b200 as mf
-    us, vs, caps, s, t = mf.random_graph(400, 4000, seed=3)
-    g = mf.EdgeListGraph(400, us, vs, caps)
+    g, s, t = mf.random_graph(400, 4000, seed=3)  # reference signature
     specs = [mf.BatchSpec(5.0, "mixed", 0), mf.BatchSpec(10.0, "inc", 1), mf.BatchSpec(5.0, "dec", 2)]
     recs = mf.run_benchmark(g, s, t, specs, reps=2, instance="r400")
     assert [r.mode for r in recs] == list(mf.BENCH_MODES) * 3

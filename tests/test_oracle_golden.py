@@ -21,8 +21,7 @@ def instance(name):
         return (rec["n"], G.arr[f"{name}/in_us"], G.arr[f"{name}/in_vs"],
                 G.arr[f"{name}/in_caps"], rec["s"], rec["t"])
     src = rec["source"]
-    fn = getattr(gen, src["gen"])
-    us, vs, caps, s, t = fn(*src["args"])
+    us, vs, caps, s, t = gen.source_edges(src["gen"], src["args"])
     return rec["n"], us, vs, caps, s, t
 
 
@@ -30,7 +29,7 @@ def batch_for(name, cur_g, entry, s, t):
     el_us, el_vs = cur_g.src[cur_g.is_original], cur_g.adj[cur_g.is_original]
     el_caps = cur_g.cap0[cur_g.is_original]
     spec = gen.BatchSpec(entry["pct"], entry["kind"], entry["seed"])
-    bu, bv, bc, _ = gen.generate_batch(cur_g.n, el_us, el_vs, el_caps, s, t, spec)
+    bu, bv, bc, _ = gen.batch_arrays(cur_g.n, el_us, el_vs, el_caps, s, t, spec)
     return bu, bv, bc
 
 
