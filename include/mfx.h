@@ -69,6 +69,10 @@ typedef struct {
                            /*   < 0 -> strict level-synchronous BFS                */
     int32_t bfs_local_max; /* ... used while the frontier <= this many items per   */
                            /*   CTA; 0 -> 64                                        */
+    int32_t deterministic; /* SolverParams.deterministic (solver.py:56-58): rounds  */
+                           /*   with a serial push / repair phase in worklist order */
+                           /*   -> byte-identical states to the reference's         */
+    int32_t reserved;      /* 0                                                     */
 } mfx_params;
 
 /* FlowResult (solver.py:108-118) plus device counters. */

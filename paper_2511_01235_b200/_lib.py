@@ -40,7 +40,8 @@ class Params(ctypes.Structure):
     _fields_ = [("kernel_cycles", i64), ("mode", i32), ("max_waves", i32),
                 ("timeout_s", ctypes.c_double), ("blocks_per_sm", i32), ("flags", i32),
                 ("wave_mult", i32), ("wave_add", i32), ("schedule", i32),
-                ("async_budget", i32), ("bfs_local", i32), ("bfs_local_max", i32)]
+                ("async_budget", i32), ("bfs_local", i32), ("bfs_local_max", i32),
+                ("deterministic", i32), ("reserved", i32)]
 
 
 class Result(ctypes.Structure):

@@ -220,6 +220,50 @@ cudaError_t ensure_batch_capacity(Topology &t, int64_t k) {
 
 using namespace mfx;
 
+// SolverParams(deterministic=True): each round = the device global relabel
+// (static: bases {t}, nothing forbidden; dynamic: {t} U deficient, s
+// forbidden) followed by the serial round kernel of det.cu; then the usual
+// finalize for flow and cut.  Host-stepped: one sync per round.
+static int det_rounds(const GraphObj &g, mfx_state *st, SolveConfig cfg, bool dynamic,
+                      int *launches) {
+  Topology &T = *g.topo;
+  StateObj &s = st->s;
+  cfg.dyn_bases = dynamic ? 1 : 0;
+  cfg.forbidden = dynamic ? s.s : -1;
+  cfg.what = WHAT_BFS;
+  const double tmo = cfg.timeout_s;
+  cudaEvent_t start = T.ev[1];
+  for (int round = 0;; ++round) {
+    cfg.reset_counters = round == 0;
+    CK(launch_solve(g, s, cfg, launches));
+    CK(launch_det_round(g, s, cfg.kc, cfg.topology));
+    if (launches) *launches += 1;
+    CK(cudaMemcpyAsync(st->host_ctrl, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
+    CK(cudaStreamSynchronize(T.stream));
+    const Ctrl &c = *st->host_ctrl;
+    if (c.status == 3 || c.status == 6 || c.active == 0) break;
+    float ms = 0;
+    CK(cudaEventRecord(T.ev[2], T.stream));
+    CK(cudaEventSynchronize(T.ev[2]));
+    cudaEventElapsedTime(&ms, start, T.ev[2]);
+    if (ms > tmo * 1e3) {
+      st->host_ctrl->status = 6;
+      CK(cudaMemcpyAsync(&s.ctrl->status, &st->host_ctrl->status, sizeof(int),
+                         cudaMemcpyHostToDevice, T.stream));
+      break;
+    }
+  }
+  if (st->host_ctrl->status == 3 || st->host_ctrl->status == 6) {
+    int status = st->host_ctrl->status;  // (the finalize launch would clear it)
+    CK(cudaMemcpyAsync(&s.ctrl->status, &status, sizeof(int), cudaMemcpyHostToDevice, T.stream));
+    return MFX_OK;
+  }
+  cfg.what = WHAT_FINAL;
+  cfg.reset_counters = false;
+  CK(launch_solve(g, s, cfg, launches));
+  return MFX_OK;
+}
+
 // A state whose residuals were last consistent with other capacity contents
 // (set_cap0, or a batch applied through another state / graph copy): the
 // reference recomputes excess from max(0, cap0 - cf) on every solve_dynamic
@@ -734,6 +778,7 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   if (const char *env = getenv("MFX_TIMEOUT_S")) tmo = atof(env) > 0 ? atof(env) : tmo;
   cfg.timeout_s = p->timeout_s > 0 ? p->timeout_s : tmo;
   cfg.blocks_per_sm = p->blocks_per_sm;
+  cfg.deterministic = p->deterministic != 0;
   cfg.ceiling = operation_ceiling(T.n, T.m_original);
   if (const char *ce = getenv("MFX_CEILING")) cfg.ceiling = strtoull(ce, nullptr, 10);  // tests
   return MFX_OK;
@@ -819,7 +864,11 @@ int mfx_solve_static(const mfx_graph *g, mfx_state *st, const mfx_params *p, mfx
   st->s.excess_consistent = true;
   launches += 1;
   CK(cudaEventRecord(T.ev[1], T.stream));
-  CK(launch_solve(g->g, st->s, cfg, &launches));
+  if (cfg.deterministic) {
+    if ((rc = det_rounds(g->g, st, cfg, false, &launches))) return rc;
+  } else {
+    CK(launch_solve(g->g, st->s, cfg, &launches));
+  }
   CK(cudaEventRecord(T.ev[2], T.stream));
   CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
   CK(cudaEventRecord(T.ev[3], T.stream));
@@ -924,7 +973,16 @@ static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const in
   // graphs carry the excess: walk it to the bases (road 1024^2: 57 -> 35 ms)
   if (cfg.walk_max == 0) cfg.walk_max = 4096;
   if (cfg.walk_depth == 0) cfg.walk_depth = 1024;
-  CK(launch_solve(g->g, st->s, cfg, &launches));
+  if (cfg.deterministic) {
+    // (a failed batch leaves the state untouched: skip the rounds)
+    CK(cudaMemcpyAsync(st->host_err, T.ws.d_err, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
+                       T.stream));
+    CK(cudaStreamSynchronize(T.stream));
+    if ((rc = batch_error(st->host_err, k, h_us, h_vs, h_caps, d_us, d_vs, d_caps))) return rc;
+    if ((rc = det_rounds(g->g, st, cfg, true, &launches))) return rc;
+  } else {
+    CK(launch_solve(g->g, st->s, cfg, &launches));
+  }
   CK(cudaEventRecord(T.ev[2], T.stream));
   CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
   CK(cudaMemcpyAsync(st->host_err, T.ws.d_err, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
@@ -1157,7 +1215,12 @@ int mfx_step(const mfx_graph *g, mfx_state *st, const mfx_params *p, int step, i
   else if (step == 1) cfg.what = WHAT_ROUND;
   else cfg.what = WHAT_FINAL;
   int launches = 0;
-  CK(launch_solve(g->g, st->s, cfg, &launches));
+  if (cfg.deterministic && cfg.what == WHAT_ROUND) {
+    CK(launch_det_round(g->g, st->s, cfg.kc, cfg.topology));
+    ++launches;
+  } else {
+    CK(launch_solve(g->g, st->s, cfg, &launches));
+  }
   CK(cudaMemcpyAsync(st->host_ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, T.stream));
   CK(cudaStreamSynchronize(T.stream));
   if (r) {

@@ -119,6 +119,7 @@ struct SolveConfig {
   bool reset_counters = true;
   const long long *gate = nullptr;  // batch error block: skip the solve if the batch failed
   bool pushpull = false;  // O2 pipelines (region-restricted push / pull rounds)
+  bool deterministic = false;  // serial round kernel (det.cu), reference deterministic mode
 };
 
 // Dispatch to the solve-kernel build chosen for the graph (Topology::variant).
@@ -148,6 +149,8 @@ cudaError_t launch_refresh_pc(const GraphObj &g);
 cudaError_t launch_mask(const StateObj &st, int which, uint8_t *d_out);
 cudaError_t launch_recompute_excess(const GraphObj &g, StateObj &st);
 cudaError_t launch_count_active(const StateObj &st, unsigned long long *d_out);
+// one deterministic round after a global relabel: worklist, serial push, serial repair (det.cu)
+cudaError_t launch_det_round(const GraphObj &g, StateObj &st, int kc, int topology);
 cudaError_t launch_pair_check(const GraphObj &g, const StateObj &st, unsigned long long *d_out);
 cudaError_t launch_cap_check(const Topology &T, const int64_t *d_cap, unsigned long long *d_out);
 // Batch: validate into ws.d_err (no mutation), then apply only if no error.

@@ -39,10 +39,13 @@ def operation_ceiling(n: int, m_original: int) -> int:
 class SolverParams:
     """Solver knobs (solver.py:47-84).
 
-    kernel_cycles / mode / instrument have the reference meaning.
-    ``deterministic`` and ``threads`` are accepted for API compatibility and
-    ignored: the device schedule is always massively parallel and the flow
-    value does not depend on it.  Device knobs: ``max_waves`` (push waves per
+    kernel_cycles / mode / instrument / deterministic have the reference
+    meaning: ``deterministic=True`` runs each round's push and repair phases
+    serially in worklist order on the device (the global relabel stays
+    parallel; its heights are unique), so the final cf / excess / height are
+    byte-identical to the reference's deterministic runs -- a parity and
+    tracing mode, not a fast one.  ``threads`` sizes the reference's host
+    thread pool and has no device meaning (accepted, unused).  Device knobs: ``max_waves`` (push waves per
     round before the next global relabel, 0 = until the active list drains),
     ``timeout_s`` (device watchdog; 0 = $MFX_TIMEOUT_S or 600 s), ``blocks_per_sm`` (persistent grid),
     ``bfs_local`` (BFS levels a CTA may run ahead on its own between two grid
@@ -90,7 +93,8 @@ class SolverParams:
                         float(self.timeout_s), int(self.blocks_per_sm), int(self.device_flags),
                         int(self.wave_mult), int(self.wave_add),
                         SCHEDULES.index(self.schedule), int(self.async_budget),
-                        int(self.bfs_local), int(self.bfs_local_max))
+                        int(self.bfs_local), int(self.bfs_local_max), int(bool(self.deterministic)),
+                        0)
 
 
 @dataclass

@@ -85,12 +85,13 @@ def test_solve_kernel_state_stays_in_registers():
 
 
 def test_integration_stub_structs_match_the_abi():
-    """The reference-side ctypes stub in INTEGRATION.md declares the same
-    mfx_params / mfx_result layouts as the package binding."""
+    """The reference-side ctypes binding (integration/dynmaxflow/_mfx.py,
+    shown in INTEGRATION.md) declares the same mfx_params / mfx_result
+    layouts as the package binding."""
     import ctypes
     from paper_2511_01235_b200 import _lib
-    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
-    code = text[text.index("class _Params"):text.index("_ERR = {")]
+    text = open(os.path.join(ROOT, "integration", "dynmaxflow", "_mfx.py")).read()
+    code = text[text.index("class _Params"):text.index("_lib = None")]
     ns = {"ctypes": ctypes}
     exec(code, ns)
     for stub, ours in ((ns["_Params"], _lib.Params), (ns["_Result"], _lib.Result)):

@@ -395,3 +395,28 @@ def test_schedule_knobs_keep_reference_results(mf, name, env, monkeypatch):
         r = mf.solve_dynamic(st, g, mf.UpdateBatch(bu, bv, bc))
         assert r.flow_value == entry["flow"] == r.certificate.cut_capacity, (name, entry["seed"])
         st = r.state
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if c not in ("grid256",)])
+def test_deterministic_mode_states_bit_exact(mf, name):
+    """SolverParams(deterministic=True): the device runs each round's push
+    and repair serially in worklist order, so the whole final state -- cf,
+    excess, height -- after the static solve and after every chained batch
+    is byte-identical to the reference's deterministic runs (state_sha from
+    the live reference), rounds included."""
+    rec = G.rec[name]
+    n, us, vs, caps, s, t = instance(name)
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    det = mf.SolverParams(deterministic=True)
+    res = mf.solve_static(g, s, t, det)
+    assert res.flow_value == rec["static_flow"]
+    assert res.rounds == rec["static_rounds_det"]
+    st = res.state
+    assert {k: sha(getattr(st, k)) for k in ("cf", "excess", "height")} == rec["static_state_sha"]
+    for entry in rec["chain"]:
+        bu, bv, bc = chain_batch(g.src, g.adj, g.is_original, g.cap0, n, s, t, entry)
+        r = mf.solve_dynamic(st, g, mf.UpdateBatch(bu, bv, bc), det)
+        assert r.flow_value == entry["flow"]
+        assert r.rounds == entry["rounds_det"]
+        st = r.state
+        assert {k: sha(getattr(st, k)) for k in ("cf", "excess", "height")} == entry["state_sha"]
