@@ -94,6 +94,9 @@ def parse():
                          "NVTX range 'timed' (no e2e / re-solve / cpu legs)")
     ap.add_argument("--scale", type=int, default=26, help="C5 R-MAT scale")
     ap.add_argument("--parts", type=int, default=4, help="C5 parts when run as one process")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only (ranks, collectives, max-over-ranks, JSON line); "
+                         "no engine calls -- runs without a GPU")
     return ap.parse_args()
 
 
@@ -705,6 +708,13 @@ def main():
     cfg = args.config
     if cfg == "auto":
         cfg = "C5" if world > 1 else "C4"
+    if args.dry_run:
+        barrier(pg, backend, dev)
+        t = max_over_ranks(pg, backend, float(rank + 1), dev)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "config": cfg,
+                              "backend": backend, "max_over_ranks_check": t}), flush=True)
+        return
     if args.impl == "reference":
         if rank == 0:
             if cfg == "C5":

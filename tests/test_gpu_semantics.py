@@ -224,14 +224,16 @@ def test_bfs_ring_stress_bit_exact(mf, kind, arg, monkeypatch):
     st0 = mf.init_residuals(g, s, t)
     mf.saturate_source(st0, g)
     want0, _ = O.bfs_heights(og, np.asarray(st0.cf, np.int64), [t], -1)
-    # dynamic: terminated state after one batch, bases {t} U deficient, s forbidden
-    r = mf.solve_static(g, s, t)
-    el = g.to_edge_list()
+    # dynamic: terminated state after one batch, bases {t} U deficient, s
+    # forbidden (on a graph copy: st0 stays consistent with g's capacities)
+    gd = g.copy()
+    r = mf.solve_static(gd, s, t)
+    el = gd.to_edge_list()
     b = gen.batch_arrays(n, el.us, el.vs, el.caps, s, t, gen.BatchSpec(5.0, "mixed", 2))[:3]
-    st1 = mf.solve_dynamic(r.state, g, mf.UpdateBatch(*b)).state
+    st1 = mf.solve_dynamic(r.state, gd, mf.UpdateBatch(*b)).state
     ex = np.asarray(st1.excess)
     bases = [v for v in range(n) if v == t or (v != s and ex[v] < 0)]
-    og.cap0[:] = np.asarray(g.cap0)
+    og.cap0[:] = np.asarray(gd.cap0)
     want1, _ = O.bfs_heights(og, np.asarray(st1.cf, np.int64), bases, s)
     for i in range(50):
         monkeypatch.setenv("MFX_RING_SLEEP", str(int(rng.integers(0, 1001))))
@@ -240,5 +242,5 @@ def test_bfs_ring_stress_bit_exact(mf, kind, arg, monkeypatch):
         monkeypatch.setenv("MFX_BFS_LOCAL_MAX", str(int(rng.choice([4, 64, 1 << 20]))))
         mf.backward_bfs(st0, g)
         assert np.array_equal(st0.height, want0), (i, kind)
-        mf.backward_bfs_dynamic(st1, g)
+        mf.backward_bfs_dynamic(st1, gd)
         assert np.array_equal(st1.height, want1), (i, kind)
