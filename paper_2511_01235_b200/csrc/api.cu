@@ -226,6 +226,7 @@ using namespace mfx;
 // finalize for flow and cut.  Host-stepped: one sync per round.
 static int det_rounds(const GraphObj &g, mfx_state *st, SolveConfig cfg, bool dynamic,
                       int *launches) {
+  cfg.strand = 0;
   Topology &T = *g.topo;
   StateObj &s = st->s;
   cfg.dyn_bases = dynamic ? 1 : 0;
@@ -770,6 +771,9 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   if (const char *tl = getenv("MFX_TAIL_LOCAL")) cfg.tail_local = atoi(tl);
   if (const char *wt = getenv("MFX_WAVE_TIME")) cfg.wave_time = atoi(wt);
   if (const char *rs = getenv("MFX_RING_SLEEP")) cfg.ring_sleep = atoi(rs);
+  cfg.strand = -1;  // auto: on in dynamic solves
+  if (const char *sr = getenv("MFX_STRAND")) cfg.strand = atoi(sr);
+  if (const char *ee = getenv("MFX_EARLY")) cfg.early = atoi(ee);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;
@@ -969,10 +973,11 @@ static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const in
   cfg.dyn_bases = 1;
   cfg.forbidden = st->s.s;
   cfg.gate = T.ws.d_err;
-  // after an update batch a handful of vertices far down long-diameter
-  // graphs carry the excess: walk it to the bases (road 1024^2: 57 -> 35 ms)
-  if (cfg.walk_max == 0) cfg.walk_max = 4096;
-  if (cfg.walk_depth == 0) cfg.walk_depth = 1024;
+  // the excess walk ($MFX_WALK_MAX / $MFX_WALK_DEPTH) is off by default since
+  // the early-exit relabel and the stranded-excess rule: C4 16.5 (off) vs
+  // 19.3 ms/batch (4096 / 1024)
+  if (cfg.walk_max > 0 && cfg.walk_depth == 0) cfg.walk_depth = 1024;
+  if (cfg.strand < 0) cfg.strand = 1;
   if (cfg.deterministic) {
     // (a failed batch leaves the state untouched: skip the rounds)
     CK(cudaMemcpyAsync(st->host_err, T.ws.d_err, sizeof(long long) * 8, cudaMemcpyDeviceToHost,

@@ -120,6 +120,8 @@ struct SolveConfig {
   const long long *gate = nullptr;  // batch error block: skip the solve if the batch failed
   bool pushpull = false;  // O2 pipelines (region-restricted push / pull rounds)
   bool deterministic = false;  // serial round kernel (det.cu), reference deterministic mode
+  int strand = 0;  // push phase ends once the sink is cut off and every deficit is filled
+  int early = 1;   // solve relabels stop once every excess holder is labelled (0 off)
 };
 
 // Dispatch to the solve-kernel build chosen for the graph (Topology::variant).

@@ -55,7 +55,9 @@ enum CtrIdx {
   C_DEPTH = 13,  // largest BFS label set (max-combined, not summed)
   C_EHOLD = 14,  // vertices holding excess when the global relabel started
   C_STOP = 15,   // set by the barrier leader: this round's push-phase time budget is spent
-  C_NCTR = 16
+  C_TALIVE = 16, // residual slots into the sink at the last global relabel (0: sink cut off)
+  C_DBASES = 17, // deficient bases (all bases but the sink) of the last global relabel
+  C_NCTR = 18
 };
 
 enum Phase { PH_BFS = 0, PH_PUSH = 1, PH_REPAIR = 2, PH_FINAL = 3, PH_N = 4 };
@@ -86,6 +88,10 @@ struct Ctrl {
   int aq_stop;
   int aq_pad;
   unsigned long long async_items;  // items processed by asynchronous push phases
+  // deficits filled since the last global relabel (a push took a head's
+  // excess from < 0 to >= 0); with the sink cut off and every deficient
+  // base filled, no base is left to absorb excess: the push phase ends
+  unsigned long long fills;
   unsigned long long epochs;       // grid barriers spent in global relabels
   // push waves run by CTA 0 alone (thin waves): state for the other CTAs
   int tail_base[NBIN];

@@ -25,6 +25,7 @@
 // operation ceiling, so every loop decision is taken on identical values.
 #include <limits.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "engine.h"
 
@@ -65,6 +66,8 @@ struct SolveArgs {
   int walk_depth;    // ... at least this many BFS levels deep
   int tail_local;    // push waves of <= this many items run in CTA 0 alone (0: off)
   int wave_time;     // push phase time budget, eighths of the last BFS's time (0: off)
+  int strand;        // end a push phase once the sink is cut off and every deficit is filled
+  int early;         // solve relabels stop once every excess holder is labelled
   int ring_sleep;    // ns an idle warp sleeps between polls of the BFS ring
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
@@ -127,6 +130,7 @@ struct Sync {
   int *s_snap;  // smem copy of ctrl->snap after the last barrier
   int *s_abort;
   unsigned long long deadline, ceiling;  // read once at kernel start
+  int strand;                            // SolveArgs::strand
   unsigned long long t_last;             // block 0: phase timing
   unsigned long long t_tail;             // block 0: last tail-wave timestamp (trace)
   unsigned long long ph[PH_N];
@@ -160,6 +164,12 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
       }
       unsigned long long p = vc->pushes, r = vc->relabels;
       int ab = vc->abort;
+      // stranded-excess rule inputs, loaded with the rest (off the chain
+      // when the rule is off: the leader's loads are the barrier's latency)
+      const bool st_on = sy.strand && phase == PH_PUSH;
+      const unsigned long long fills = st_on ? vc->fills : 0ull;
+      const int talive = st_on ? vc->snap[C_TALIVE] : 1;
+      const int dbases = st_on ? vc->snap[C_DBASES] : 0;
 #pragma unroll
       for (int i = 0; i < C_NCTR; ++i) {
         if (rd >> i & 1) {
@@ -171,7 +181,8 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
       }
       const unsigned long long now = globaltimer();
       const unsigned long long wdl = vc->wave_deadline;
-      vc->snap[C_STOP] = phase == PH_PUSH && wdl != 0 && now > wdl;
+      vc->snap[C_STOP] = phase == PH_PUSH && ((wdl != 0 && now > wdl) ||
+                                              (talive == 0 && fills >= (unsigned)dbases));
       if (!ab) {
         if (now > sy.deadline) {
           vc->abort = 1;
@@ -733,6 +744,7 @@ struct Kern {
   __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels, bool early) {
     const int n = a.n;
     int holders = 0;  // vertices (not s, t) with positive excess
+    int dbases = 0;   // deficient bases (bases other than the sink)
     __shared__ int zero[NBIN];
     __shared__ int rb[NBIN];
     __shared__ int s_ring[kRing];
@@ -750,6 +762,7 @@ struct Kern {
     disc_cnt = 0;
     max_lab = 0;
     holders = 0;
+    dbases = 0;
     loc_ok = false;
     nocheck = (a.flags & 1) != 0;
     ring = s_ring;
@@ -819,6 +832,7 @@ struct Kern {
         if (v == a.forbidden) base = false;
         hv[r] = base ? 0 : n;
         bm |= (unsigned)base << r;
+        dbases += base && v != a.t;
       }
       if (full) {
         reinterpret_cast<int4 *>(a.h + vb)[0] = make_int4(hv[0], hv[1], hv[2], hv[3]);
@@ -852,9 +866,26 @@ struct Kern {
     level_flush(a.F0, zero);
     holders = warp_sum(holders);
     if (lane == 0 && holders) atomicAdd(a.ctrl->live + C_EHOLD, holders);
+    // is the sink still reachable at all?  residual slots into t (the
+    // reverse residual of t's row, pc - cf); with none, only deficits can
+    // absorb excess this round (push-phase stop rule, Ctrl::fills)
+    if (!PP) {
+      int talive = 0;
+      const int t0 = __ldg(a.off + a.t), t1 = __ldg(a.off + a.t + 1);
+      for (int i = t0 + gtid; i < t1; i += gthreads)
+        talive += __ldg(a.adj + i) != a.forbidden &&
+                  __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i)) > 0;
+      talive = warp_sum(talive);
+      dbases = warp_sum(dbases);
+      if (lane == 0 && talive) atomicAdd(a.ctrl->live + C_TALIVE, talive);
+      if (lane == 0 && dbases) atomicAdd(a.ctrl->live + C_DBASES, dbases);
+      if (gtid == 0 && !a.strand) atomicAdd(a.ctrl->live + C_DBASES, 1 << 30);  // rule off
+      if (gtid == 0) a.ctrl->fills = 0;
+    }
     lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
     const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
-    const unsigned amask = (1u << C_ACTIVE) | (1u << C_REACHED) | (1u << C_DEPTH) | (1u << C_EHOLD);
+    const unsigned amask = (1u << C_ACTIVE) | (1u << C_REACHED) | (1u << C_DEPTH) |
+                           (1u << C_EHOLD) | (1u << C_TALIVE) | (1u << C_DBASES);
     if (a.trace) {  // trace: CTA 0's seeding pass done (phase-4 entry)
       __syncthreads();
       if (blockIdx.x == 0 && threadIdx.x == 0 && sy.trace_n < sy.trace_cap)
@@ -1003,6 +1034,11 @@ struct Kern {
       eu = ldcg(a.ex + u);
       if (pull) eu = -eu;
       lc.bytes += Bytes<CapT>::kVertex;
+      // a deficient base (height 0, not the sink) that a push listed for
+      // this wave and that holds no deficit any more: filled (a later
+      // refill may count it twice, which only ends the phase earlier)
+      if (!PP && a.strand && !a.topology && hu == 0 && eu >= 0 && u != a.t && u != a.s)
+        atomicAdd(&a.ctrl->fills, 1ull);
     }
     const bool live = eu > 0 && hu < n;
     if (!live) d = 0;
@@ -1104,6 +1140,7 @@ struct Kern {
     // asynchronous phase when it was not holding excess before the push.
 #pragma unroll
     for (int k = 0; k < kBin0Max; ++k) {
+
       if (Async) {
         bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
         activate(p, vv[k], bb[k], stamp, nbase);
@@ -1253,6 +1290,8 @@ struct Kern {
             atomic_add(a.cf + i, (CapT)(-amt));
             atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
             old = add_excess(v, amt);
+            if (!PP && a.strand && old < 0 && old + amt >= 0 && v != a.t)
+              atomicAdd(&a.ctrl->fills, 1ull);
           }
           act = old <= 0 && v != a.s && v != a.t;
           lc.pushes++;
@@ -1430,7 +1469,9 @@ struct Kern {
         if (take <= 0) break;
         atomic_add(a.cf + __ldg(a.rev + pick), (CapT)take);
         atomic_add(a.ex + u, -take);
-        add_excess(v, take);
+        const long long vold = add_excess(v, take);
+        if (!PP && a.strand && vold < 0 && vold + take >= 0 && v != a.t)
+          atomicAdd(&a.ctrl->fills, 1ull);
         lc.pushes++;
         lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kSlot +
                     Bytes<CapT>::kPush;
@@ -1498,7 +1539,9 @@ struct Kern {
         const bool go = tot > 0 && tot <= a.tail_local && s_cnt[1] <= kWarps && s_cnt[2] == 0 &&
                         s_cnt[3] == 0 &&
                         (waves < max_waves || (tot <= a.tail_items && waves < a.tail_cap)) &&
-                        !(a.wave_time > 0 && globaltimer() > a.ctrl->wave_deadline);
+                        !(a.wave_time > 0 && globaltimer() > a.ctrl->wave_deadline) &&
+                        !(!PP && a.strand && sy.s_snap[C_TALIVE] == 0 &&
+                          ((volatile Ctrl *)a.ctrl)->fills >= (unsigned)sy.s_snap[C_DBASES]);
         // consumed here: the next wave appends from zero; else the pending
         // wave's counts go to the live counters the grid barrier snapshots
         for (int b = 0; b < NBIN; ++b) {
@@ -1870,6 +1913,7 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     sy.gen = vc->bar_gen;
     sy.deadline = vc->deadline_ns;
     sy.ceiling = vc->ceiling;
+    sy.strand = a.strand;
     for (int i = 0; i < C_NCTR; ++i) s_snap[i] = vc->snap[i];
     s_abort = vc->abort;
     sy.t_last = globaltimer();
@@ -1898,10 +1942,11 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
     for (; do_bfs || do_push;) {
       if (do_bfs) {
-        // (flags bit 2 enables the early exit -- measured no faster on C1-C4;
-        // the bit-exact global relabel entry point, WHAT_BFS, never takes it)
+        // early exit (stop once every excess holder is labelled; C4
+        // dynamic 25 -> 16.5 ms/batch) in solve rounds only: the bit-exact
+        // global relabel entry point, WHAT_BFS, never takes it
         L = k.bfs(stamp + 1, bstamp, a.bfs_local,
-                  a.what == WHAT_SOLVE && !a.topology && !PP && (a.flags & 4) != 0);
+                  a.what == WHAT_SOLVE && !a.topology && !PP && (a.early || (a.flags & 4) != 0));
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
         // with the walk enabled the BFS stamped the listed active vertices
@@ -2029,6 +2074,43 @@ __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long 
   }
 }
 
+// L2 residency for the heights: every BFS discovery test and every push
+// scan reads h[] of random neighbours, so h (4n bytes; C2 17 MB, C4 96 MB)
+// gets a persisting access-policy window on the engine stream, the rest of
+// the traffic streams past it.  $MFX_L2_WINDOW = 0 turns it off.
+static cudaError_t set_l2_window(const Topology &T, const StateObj &st) {
+  static int enabled = -1;  // device support (probed once)
+  static size_t max_window = 0;
+  if (enabled < 0) {
+    enabled = 1;
+    int mw = 0, mp = 0;
+    if (cudaDeviceGetAttribute(&mw, cudaDevAttrMaxAccessPolicyWindowSize, T.device) ||
+        cudaDeviceGetAttribute(&mp, cudaDevAttrMaxPersistingL2CacheSize, T.device) || mw <= 0 ||
+        mp <= 0) {
+      cudaGetLastError();
+      enabled = 0;
+    } else {
+      max_window = (size_t)mw;
+      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mp)) {
+        cudaGetLastError();
+        enabled = 0;
+      }
+    }
+  }
+  const char *env = getenv("MFX_L2_WINDOW");  // (read per launch: A/B within a process)
+  const bool on = enabled > 0 && (env == nullptr || atoi(env) != 0);
+  cudaStreamAttrValue v = {};
+  if (on) {
+    size_t bytes = sizeof(int) * (size_t)T.n;
+    v.accessPolicyWindow.base_ptr = st.h;
+    v.accessPolicyWindow.num_bytes = bytes < max_window ? bytes : max_window;
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }  // (off: a zero-sized window clears a previous one)
+  return cudaStreamSetAttribute(T.stream, cudaStreamAttributeAccessPolicyWindow, &v);
+}
+
 // ---------------------------------------------------------------------------
 template <typename CapT>
 static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveConfig &cfg,
@@ -2059,6 +2141,8 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.walk_depth = cfg.walk_depth;
   a.tail_local = cfg.tail_local;
   a.wave_time = cfg.wave_time;
+  a.strand = cfg.strand > 0;
+  a.early = cfg.early != 0;
   a.ring_sleep = cfg.ring_sleep;
   a.coop_kc = cfg.coop_kc > 0 ? (cfg.coop_kc < cfg.kc ? cfg.coop_kc : cfg.kc) : cfg.kc;
   a.tail_cap = cfg.tail_cap;
@@ -2118,6 +2202,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   if (cap > 0 && cap < ctas) ctas = cap;
   dim3 grid(ctas), block(kBlock);
   void *args[] = {(void *)&a};
+  if ((e = set_l2_window(T, st)) != cudaSuccess) return e;
   e = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, T.stream);
   if (launches) *launches += 2;
   count_launch(2);

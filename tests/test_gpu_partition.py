@@ -197,3 +197,33 @@ def test_device_rmat_sampler_and_dynamic_equals_resolve(part):
         s = pg.solve_static()
         assert d.flow_value == s.flow_value == d.cut_capacity
     pg.close()
+
+
+def _rmat_chain(part, scale, P, k, batches):
+    pg = part.PartitionedGraph.rmat(scale, 16, 0, part.LocalGroup(P))
+    st = pg.solve_static()
+    assert st.flow_value == st.cut_capacity > 0
+    for b in range(batches):
+        batch = pg.sample_batch(k, seed=b)
+        assert len(batch) == k
+        d = pg.solve_dynamic(batch)
+        assert d.flow_value == d.cut_capacity
+        s = pg.solve_static()  # static re-solve on the updated capacities
+        assert s.flow_value == d.flow_value == s.cut_capacity, (scale, P, b)
+    pg.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_rmat22_partition_million_update_batches(part, P):
+    """C5's generator at scale 22 (131 M slots) over P parts with C5-sized
+    batches of 10^6 mixed updates: dynamic == static re-solve, flow == cut."""
+    _rmat_chain(part, 22, P, 1_000_000, 2)
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.environ.get("MFX_SLOW"), reason="opt-in (minutes): MFX_SLOW=1")
+@pytest.mark.parametrize("scale,P", [(24, 2), (24, 4), (26, 4)])
+def test_rmat_large_partition_million_update_batches(part, scale, P):
+    """R-MAT 24 (521 M slots) and full C5 (R-MAT 26, 2.1 B slots) on one
+    GPU, 10^6-update batches, dynamic == static re-solve."""
+    _rmat_chain(part, scale, P, 1_000_000, 2)
