@@ -57,7 +57,8 @@ enum CtrIdx {
   C_STOP = 15,   // set by the barrier leader: this round's push-phase time budget is spent
   C_TALIVE = 16, // residual slots into the sink at the last global relabel (0: sink cut off)
   C_DBASES = 17, // deficient bases (all bases but the sink) of the last global relabel
-  C_NCTR = 18
+  C_EFILL = 18,  // set by the barrier leader: the labelled excess covers every deficit (BFS may stop)
+  C_NCTR = 19
 };
 
 enum Phase { PH_BFS = 0, PH_PUSH = 1, PH_REPAIR = 2, PH_FINAL = 3, PH_N = 4 };
@@ -92,6 +93,11 @@ struct Ctrl {
   // excess from < 0 to >= 0); with the sink cut off and every deficient
   // base filled, no base is left to absorb excess: the push phase ends
   unsigned long long fills;
+  // demand-covered early exit of a solve's global relabel: [0] = total
+  // deficit of the deficient bases, [1] = excess of the holders labelled so
+  // far; live = appended this epoch, snap = the leader's running totals
+  long long x_live[2], x_snap[2];
+  long long efill_d;  // total deficit at the last early exit it allowed (must shrink)
   unsigned long long epochs;       // grid barriers spent in global relabels
   // push waves run by CTA 0 alone (thin waves): state for the other CTAs
   int tail_base[NBIN];

@@ -179,6 +179,25 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
           vc->snap[i] = 0;
         }
       }
+      // demand-covered rule (BFS barriers that accumulate the relabel's
+      // counters): with the sink cut off, the deficits are the only bases
+      // that can absorb excess; once the labelled holders carry at least
+      // their total, the relabel may stop.  Allowed only while the total
+      // deficit keeps shrinking between such stops, so the rounds progress.
+      if (phase == PH_BFS && ((acc_mask | clear_mask) >> C_EHOLD & 1)) {
+        const bool fresh = (clear_mask >> C_EHOLD & 1) != 0;  // the seeding barrier
+        const long long d = (fresh ? 0 : vc->x_snap[0]) + vc->x_live[0];
+        const long long x = (fresh ? 0 : vc->x_snap[1]) + vc->x_live[1];
+        vc->x_snap[0] = d;
+        vc->x_snap[1] = x;
+        vc->x_live[0] = vc->x_live[1] = 0;
+        const bool fire = sy.strand && vc->snap[C_TALIVE] == 0 && d > 0 && x >= d &&
+                          d < vc->efill_d;
+        if (fire) vc->efill_d = d;
+        vc->snap[C_EFILL] = fire;
+      } else if (phase == PH_BFS) {
+        vc->snap[C_EFILL] = 0;
+      }
       const unsigned long long now = globaltimer();
       const unsigned long long wdl = vc->wave_deadline;
       vc->snap[C_STOP] = phase == PH_PUSH && ((wdl != 0 && now > wdl) ||
@@ -329,6 +348,7 @@ struct Kern {
     rctr = a.ctrl->live + C_RNEXT;
     q = wq + wib;
     act_cnt = 0;
+    hexc = 0;
   }
 
   __device__ __forceinline__ int vbin(int v) const { return __ldg(a.vbin + v); }
@@ -431,6 +451,7 @@ struct Kern {
   int disc_cnt;      // first discoveries (+ bases) by this lane
   int xc;            // trace mode: vertices this lane expanded in the epoch
   int max_lab;       // largest label this lane set
+  long long hexc;    // excess of the active vertices this lane listed (demand-covered exit)
   bool loc_ok;       // discoveries may go to the CTA-local queue
   bool nocheck;      // relax with the atomic alone (no h[v] pre-load)
   int *ring;         // CTA-local work ring (shared memory, kRing slots, kEmpty = free)
@@ -616,6 +637,7 @@ struct Kern {
     const int ru = valid ? region(u) : 0;
     const bool act = first && u != a.s && u != a.t && (ru == 1 ? eu < 0 : eu > 0);
     act_cnt += act;
+    if (!PP && act) hexc += eu;
     // queued for the push phase: owned (async) / listed for wave 0 (walk dedupe)
     if (act && (a.async || a.walk_max > 0)) a.mark[u] = ep_next;
     append_binned(1, act && !a.topology, u, bin_of(d), a.ctrl->live + C_RNEXT, a.R, rb_, a.rcap);
@@ -702,6 +724,11 @@ struct Kern {
     int c = warp_sum(act_cnt);
     if (lane == 0 && c) atomicAdd(a.ctrl->live + C_ACTIVE, c);
     act_cnt = 0;
+    if (!PP) {
+      const long long x = warp_sum(hexc);
+      if (lane == 0 && x) atomicAdd((unsigned long long *)&a.ctrl->x_live[1], (unsigned long long)x);
+      hexc = 0;
+    }
     c = warp_sum(disc_cnt);
     if (lane == 0 && c) atomicAdd(a.ctrl->live + C_REACHED, c);
     disc_cnt = 0;
@@ -745,6 +772,7 @@ struct Kern {
     const int n = a.n;
     int holders = 0;  // vertices (not s, t) with positive excess
     int dbases = 0;   // deficient bases (bases other than the sink)
+    long long dsum = 0;  // their total deficit
     __shared__ int zero[NBIN];
     __shared__ int rb[NBIN];
     __shared__ int s_ring[kRing];
@@ -761,8 +789,10 @@ struct Kern {
     ep_next = ep;
     disc_cnt = 0;
     max_lab = 0;
+    hexc = 0;
     holders = 0;
     dbases = 0;
+    dsum = 0;
     loc_ok = false;
     nocheck = (a.flags & 1) != 0;
     ring = s_ring;
@@ -833,6 +863,7 @@ struct Kern {
         hv[r] = base ? 0 : n;
         bm |= (unsigned)base << r;
         dbases += base && v != a.t;
+        if (!PP && base && v != a.t) dsum -= ev[r];
       }
       if (full) {
         reinterpret_cast<int4 *>(a.h + vb)[0] = make_int4(hv[0], hv[1], hv[2], hv[3]);
@@ -879,6 +910,9 @@ struct Kern {
       dbases = warp_sum(dbases);
       if (lane == 0 && talive) atomicAdd(a.ctrl->live + C_TALIVE, talive);
       if (lane == 0 && dbases) atomicAdd(a.ctrl->live + C_DBASES, dbases);
+      dsum = warp_sum(dsum);
+      if (lane == 0 && dsum)
+        atomicAdd((unsigned long long *)&a.ctrl->x_live[0], (unsigned long long)dsum);
       if (gtid == 0 && !a.strand) atomicAdd(a.ctrl->live + C_DBASES, 1 << 30);  // rule off
       if (gtid == 0) a.ctrl->fills = 0;
     }
@@ -893,6 +927,11 @@ struct Kern {
     }
     grid_sync(a.ctrl, sy, fmask | (1u << C_BASES), rmask | amask, rmask | amask, PH_BFS);
     int E = 0;
+    // With the demand-covered exit in reach (sink cut off, deficits to
+    // fill) the ring epochs start short and double, so the barrier that can
+    // stop the relabel comes a few labels after the holders near the
+    // deficits are found, not after a full 128-label epoch (uniform: snap)
+    int ramp = early && a.strand && sy.s_snap[C_TALIVE] == 0 && sy.s_snap[C_DBASES] > 0 ? 8 : 0;
     for (;;) {
       int cnt[NBIN];
       int tot = 0;
@@ -908,6 +947,13 @@ struct Kern {
       // relabel (no holder left) always runs to the end, so the certificate
       // still comes from exact distances.
       if (early && sy.s_snap[C_EHOLD] > 0 && sy.s_snap[C_ACTIVE] >= sy.s_snap[C_EHOLD]) break;
+      // Demand-covered exit (dynamic solves, sink cut off): the holders
+      // labelled so far carry at least the total deficit, so this round's
+      // pushes can fill every deficit without the far holders (C4: a batch's
+      // new deficit is a few hops from the excess its decrease created,
+      // while excess stranded near the source lies ~10^4 levels away).  The
+      // barrier leader allows it only while the total deficit shrinks.
+      if (early && sy.s_snap[C_EFILL]) break;
       if (threadIdx.x < NBIN) rb[threadIdx.x] = sy.s_snap[C_RNEXT + threadIdx.x];
       __syncthreads();
       rb_ = rb;
@@ -917,7 +963,8 @@ struct Kern {
       // wide levels stay grid-wide so no CTA serialises a share of them
       // (R-MAT hubs)
       loc_ok = local_levels > 0 && tot <= a.bfs_local_max * (int)gridDim.x;
-      lcap = sy.s_snap[C_DEPTH] + local_levels;  // (labels so far <= C_DEPTH)
+      lcap = sy.s_snap[C_DEPTH] + (ramp && ramp < local_levels ? ramp : local_levels);
+      ramp *= 2;  // (labels so far <= C_DEPTH)
       // flags bit 1: thin (latency-bound) epochs relax by atomic alone
       nocheck = (a.flags & 1) != 0 || ((a.flags & 2) != 0 && loc_ok);
       int *const *Fc = (E & 1) ? a.F1 : a.F0;
@@ -1839,6 +1886,11 @@ struct Kern {
   // =========================================================================
   // flow (dynamic.py:141-143) and cut certificate (solver.py:178-184)
   // =========================================================================
+  // slot i of a row on the walked side, head height hv: its share of the cut
+  __device__ __forceinline__ long long cut_slot(bool bside, int hv, int i) const {
+    if (bside) return hv == a.n ? (long long)__ldg(a.cap0 + __ldg(a.rev + i)) : 0ll;
+    return hv != a.n ? (long long)__ldg(a.cap0 + i) : 0ll;
+  }
   __device__ void finalize(long long *scr) {
     const int n = a.n;
     long long f = 0;
@@ -1846,12 +1898,18 @@ struct Kern {
     for (int j = gtid; j < nb; j += gthreads) f += ldcg(a.ex + ldcg(a.bases + j));
     f = block_sum(f, scr);
     if (threadIdx.x == 0 && f) atomicAdd((unsigned long long *)&a.ctrl->flow, (unsigned long long)f);
-    // A-side rows: light ones inline; heavy rows (CTA each) listed from the
-    // front of `heavy`, huge rows (> kBin2Max slots, e.g. the source of the
-    // grid config with ~2.1 M slots; whole grid each) from the back.
+    // cut = sum of cap0 over A -> B slots, A = {h == n}.  Walked from the
+    // smaller side: A-side rows sum their slots into B; B-side rows (when the
+    // last relabel reached fewer than n/2 vertices, e.g. C4 whose sink side
+    // is a corner) sum the reverse slots of their slots out of A.  Light rows
+    // inline; heavy rows (CTA each) listed from the front of `heavy`, huge
+    // rows (> kBin2Max slots, e.g. the source of the grid config with ~2.1 M
+    // slots; whole grid each) from the back.
+    const int reached = sy.s_snap[C_REACHED];
+    const bool bside = reached > 0 && 2ll * reached < (long long)n;
     long long c = 0;
     for (int u = gtid; u < n; u += gthreads) {
-      if (ldcg(a.h + u) != n) continue;
+      if ((ldcg(a.h + u) != n) != bside) continue;
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       if (hi - lo > 64) {
         if (hi - lo > kBin2Max) a.heavy[n - 1 - atomicAdd(a.ctrl->live + C_HUGE, 1)] = u;
@@ -1863,14 +1921,12 @@ struct Kern {
 #pragma unroll
         for (int k = 0; k < kBin0Max; ++k) vv[k] = lo + k < hi ? __ldg(a.adj + lo + k) : -1;
 #pragma unroll
-        for (int k = 0; k < kBin0Max; ++k) hv[k] = vv[k] >= 0 ? ldcg(a.h + vv[k]) : n;
+        for (int k = 0; k < kBin0Max; ++k) hv[k] = vv[k] >= 0 ? ldcg(a.h + vv[k]) : bside ? 0 : n;
 #pragma unroll
-        for (int k = 0; k < kBin0Max; ++k)
-          if (hv[k] != n) c += (long long)__ldg(a.cap0 + lo + k);
+        for (int k = 0; k < kBin0Max; ++k) c += cut_slot(bside, hv[k], lo + k);
         continue;
       }
-      for (int i = lo; i < hi; ++i)
-        if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
+      for (int i = lo; i < hi; ++i) c += cut_slot(bside, ldcg(a.h + __ldg(a.adj + i)), i);
     }
     grid_sync(a.ctrl, sy, (1u << C_HEAVY) | (1u << C_HUGE), 0, 0, PH_FINAL);
     int nh = sy.s_snap[C_HEAVY], ng = sy.s_snap[C_HUGE];
@@ -1878,13 +1934,13 @@ struct Kern {
       int u = ldcg(a.heavy + j);
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
-        if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
+        c += cut_slot(bside, ldcg(a.h + __ldg(a.adj + i)), i);
     }
     for (int j = 0; j < ng; ++j) {
       int u = ldcg(a.heavy + n - 1 - j);
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       for (int i = lo + gtid; i < hi; i += gthreads)
-        if (ldcg(a.h + __ldg(a.adj + i)) != n) c += (long long)__ldg(a.cap0 + i);
+        c += cut_slot(bside, ldcg(a.h + __ldg(a.adj + i)), i);
     }
     c = block_sum(c, scr);
     if (threadIdx.x == 0 && c) atomicAdd((unsigned long long *)&a.ctrl->cut, (unsigned long long)c);
@@ -2066,6 +2122,8 @@ __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long 
   for (int i = 0; i < C_NCTR; ++i) c->live[i] = 0;
   c->flow = 0;
   c->cut = 0;
+  c->x_live[0] = c->x_live[1] = c->x_snap[0] = c->x_snap[1] = 0;
+  c->efill_d = LLONG_MAX;
   if (reset_counters) {
     for (int i = 0; i < PH_N; ++i) c->phase_ns[i] = 0;
     c->pushes = c->relabels = c->repairs = c->rounds = c->levels = c->waves = c->bytes = 0;
