@@ -2135,10 +2135,15 @@ __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long 
 // L2 residency for the heights: every BFS discovery test and every push
 // scan reads h[] of random neighbours, so h (4n bytes; C2 17 MB, C4 96 MB)
 // gets a persisting access-policy window on the engine stream, the rest of
-// the traffic streams past it.  $MFX_L2_WINDOW = 0 turns it off.
+// the traffic streams past it.  Off unless $MFX_L2_WINDOW = 1.
 static cudaError_t set_l2_window(const Topology &T, const StateObj &st) {
   static int enabled = -1;  // device support (probed once)
   static size_t max_window = 0;
+  // Opt-in ($MFX_L2_WINDOW=1): the set-aside carve-out itself cost C2's
+  // static solve 23.6 -> 28.1 ms (15 -> 18 rounds) and gained C4 nothing
+  // (1.09 s either way), so by default no L2 is ever set aside.
+  const char *env = getenv("MFX_L2_WINDOW");  // (read per launch: A/B within a process)
+  if (enabled < 0 && (env == nullptr || atoi(env) == 0)) return cudaSuccess;  // never set aside
   if (enabled < 0) {
     enabled = 1;
     int mw = 0, mp = 0;
@@ -2155,8 +2160,7 @@ static cudaError_t set_l2_window(const Topology &T, const StateObj &st) {
       }
     }
   }
-  const char *env = getenv("MFX_L2_WINDOW");  // (read per launch: A/B within a process)
-  const bool on = enabled > 0 && (env == nullptr || atoi(env) != 0);
+  const bool on = enabled > 0 && env != nullptr && atoi(env) != 0;
   cudaStreamAttrValue v = {};
   if (on) {
     size_t bytes = sizeof(int) * (size_t)T.n;

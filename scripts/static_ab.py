@@ -33,14 +33,18 @@ g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps))
 st = mfx.init_residuals(g, s, t)
 mfx.resolve_static(g, st)
 for spec in a.knobs * 2:  # two passes: interleaved A/B
-    env = dict(kv.split("=") for kv in spec.split(",") if kv)
+    kv_all = dict(kv.split("=") for kv in spec.split(",") if kv)
+    env = {k: v for k, v in kv_all.items() if k.isupper()}  # MFX_* environment knobs
+    params = mfx.SolverParams(**{k: int(v) for k, v in kv_all.items() if not k.isupper()})
     os.environ.update(env)
     ms, rounds = [], []
     for _ in range(a.reps):
-        r = mfx.resolve_static(g, st)
+        r = mfx.resolve_static(g, st, params)
         ms.append(r.device["ms_total"])
         rounds.append(r.rounds)
-    print(f"{spec or 'default':32s} mean {np.mean(ms):8.2f} ms  min {np.min(ms):8.2f}  rounds {rounds}",
-          flush=True)
+    d = r.device
+    print(f"{spec or 'default':32s} mean {np.mean(ms):8.2f} ms  min {np.min(ms):8.2f}  rounds {rounds}"
+          f"  levels {d['bfs_levels']} epochs {d['bfs_epochs']} waves {d['waves']}"
+          f"  bfs {d['ns_bfs'] / 1e6:.1f} push {d['ns_push'] / 1e6:.1f} ms", flush=True)
     for k in env:
         os.environ.pop(k)
