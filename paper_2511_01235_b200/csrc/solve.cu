@@ -768,7 +768,15 @@ struct Kern {
   // Returns the BFS depth (levels incl. level 0 = max label + 1); the active
   // set is left in R (wave 0).  ep: ownership stamp the following
   // asynchronous push phase will use; bstamp: persistent epoch stamp.
-  __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels, bool early) {
+  // filt: holders count for the early exit only if the previous relabel of
+  // this solve reached them (h < n): a vertex it left unreached has no
+  // residual path to a base, pushes only move excess between reached
+  // vertices (creating arcs among them) and the bases only shrink, so it
+  // stays unreachable for the rest of the solve.  (A local relabel to n
+  // means no residual out-arc, which nothing adds back: no push or repair
+  // can target a vertex at height n.)  Not after a batch: its updates and
+  // the source re-saturation change arbitrary arcs.
+  __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels, bool early, bool filt) {
     const int n = a.n;
     int holders = 0;  // vertices (not s, t) with positive excess
     int dbases = 0;   // deficient bases (bases other than the sink)
@@ -846,6 +854,20 @@ struct Kern {
         for (int r = 0; r < V; ++r) ev[r] = vb + r < n ? ldcg(a.ex + vb + r) : 0;
       }
       unsigned bm = 0;  // bases among this lane's vertices
+      unsigned cand = 0xFFu;  // relabel candidates (filt: reached by the previous relabel)
+      if (filt) {
+        if (full) {
+          const int4 h0 = __ldcg(reinterpret_cast<const int4 *>(a.h + vb));
+          const int4 h1 = __ldcg(reinterpret_cast<const int4 *>(a.h + vb) + 1);
+          cand = (unsigned)(h0.x < n) | (unsigned)(h0.y < n) << 1 | (unsigned)(h0.z < n) << 2 |
+                 (unsigned)(h0.w < n) << 3 | (unsigned)(h1.x < n) << 4 | (unsigned)(h1.y < n) << 5 |
+                 (unsigned)(h1.z < n) << 6 | (unsigned)(h1.w < n) << 7;
+        } else {
+          cand = 0;
+#pragma unroll
+          for (int r = 0; r < V; ++r) cand |= (unsigned)(vb + r < n && ldcg(a.h + vb + r) < n) << r;
+        }
+      }
       int hv[V];
 #pragma unroll
       for (int r = 0; r < V; ++r) {
@@ -857,7 +879,7 @@ struct Kern {
                                           : (v == a.s || (v != a.t && ev[r] > 0)));
         } else {
           base = valid && (v == a.t || (a.dyn_bases && v != a.s && ev[r] < 0));
-          holders += valid && v != a.s && v != a.t && ev[r] > 0;
+          holders += valid && v != a.s && v != a.t && ev[r] > 0 && (cand >> r & 1);
         }
         if (v == a.forbidden) base = false;
         hv[r] = base ? 0 : n;
@@ -1037,9 +1059,24 @@ struct Kern {
     if (!ovf || local_levels == 0 || *sy.s_abort || attempt > 0) break;
     local_levels = 0;
     early = false;
+    filt = false;
     __syncthreads();
     }
     const int depth = sy.s_snap[C_DEPTH] + 1;
+    if (sy.trace && threadIdx.x == 0 && sy.trace_n + 1 < sy.trace_cap) {
+      // trace: the relabel's exit inputs (phase-8: deficit | labelled excess;
+      // phase-9: efill | sink slots | deficient bases | holders | active)
+      volatile Ctrl *vc = a.ctrl;
+      const unsigned long long D = (unsigned long long)vc->x_snap[0] & 0xFFFFFFFull;
+      const unsigned long long X = (unsigned long long)vc->x_snap[1] & 0xFFFFFFFFull;
+      sy.trace[sy.trace_n++] = (8ull << 60) | (D << 32) | X;
+      sy.trace[sy.trace_n++] =
+          (9ull << 60) | ((unsigned long long)(sy.s_snap[C_EFILL] & 1) << 59) |
+          ((unsigned long long)(sy.s_snap[C_TALIVE] & 0x7F) << 52) |
+          ((unsigned long long)(sy.s_snap[C_DBASES] & 0xFFF) << 40) |
+          ((unsigned long long)(sy.s_snap[C_EHOLD] & 0xFFFFF) << 20) |
+          (unsigned long long)(sy.s_snap[C_ACTIVE] & 0xFFFFF);
+    }
     if (gtid == 0) {
       a.ctrl->levels += depth;
       a.ctrl->epochs += E_all;
@@ -1996,13 +2033,15 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     const bool do_bfs = a.what == WHAT_SOLVE || a.what == WHAT_BFS;
     const bool do_push = a.what == WHAT_SOLVE || a.what == WHAT_ROUND;
     int L = (int)((volatile Ctrl *)a.ctrl)->last_levels;
+    bool first_bfs = true;
     for (; do_bfs || do_push;) {
       if (do_bfs) {
         // early exit (stop once every excess holder is labelled; C4
         // dynamic 25 -> 16.5 ms/batch) in solve rounds only: the bit-exact
         // global relabel entry point, WHAT_BFS, never takes it
-        L = k.bfs(stamp + 1, bstamp, a.bfs_local,
-                  a.what == WHAT_SOLVE && !a.topology && !PP && (a.early || (a.flags & 4) != 0));
+        const bool early = a.what == WHAT_SOLVE && !a.topology && !PP && (a.early || (a.flags & 4) != 0);
+        L = k.bfs(stamp + 1, bstamp, a.bfs_local, early, early && !first_bfs);
+        first_bfs = false;
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
         // with the walk enabled the BFS stamped the listed active vertices
@@ -2018,7 +2057,16 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
         }
       }
       if (a.async) k.push_round_async(stamp, scr);
-      else k.push_round(stamp, scr, a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add);
+      else {
+        int budget = a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add;
+        // after a demand-covered relabel exit the few labelled holders must
+        // cross their whole distance (<= L hops) to the deficits: the usual
+        // L/2 budget would stop them halfway and the next relabel could not
+        // stop early (the deficit did not shrink), so it would run to the far
+        // holders (C4: one 35 ms relabel per such batch)
+        if (s_snap[C_EFILL] && budget < 4 * L + 8) budget = 4 * L + 8;
+        k.push_round(stamp, scr, budget);
+      }
       if (s_abort || !do_bfs) break;
     }
     flush_counters(a.ctrl, lc, scr);

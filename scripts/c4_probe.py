@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--batch", type=int, default=10000)
     ap.add_argument("--knobs", nargs="*", default=[""])
     ap.add_argument("--quiet", action="store_true", help="summary line per knob only")
+    ap.add_argument("--trace-ms", type=float, default=3.0, help="trace batches slower than this")
     args = ap.parse_args()
     if args.graph == "road":
         us, vs, caps, s, t = gen.road_graph(args.side, args.side, 0, 0.21)
@@ -81,9 +82,19 @@ def main():
                               "push_ms": round(d["ns_push"] / 1e6, 3),
                               "repair_ms": round(d["ns_repair"] / 1e6, 3),
                               "pushes": rr.pushes, "relabels": rr.relabels}), flush=True)
-            if os.environ.get("MFX_TRACE_CAP"):
+            if os.environ.get("MFX_TRACE_CAP") and d["ms_total"] > args.trace_ms:
                 import trace as T
-                T.report(f"batch {i}", rr.state, g, rr)
+                ph, items, dt = T.fetch(rr.state, g)
+                raw = (items.astype(np.uint64) << np.uint64(32)) | dt.astype(np.uint64)
+                for q in np.flatnonzero((ph == 8) | (ph == 9)):
+                    if ph[q] == 8:
+                        print(f"    relabel exit: deficit {int(items[q])} labelled excess {int(dt[q])}")
+                    else:
+                        x = int(raw[q])
+                        print(f"      efill {x >> 59 & 1} sink slots {x >> 52 & 0x7F} "
+                              f"deficient bases {x >> 40 & 0xFFF} holders {x >> 20 & 0xFFFFF} "
+                              f"active {x & 0xFFFFF}")
+                T.rounds_view(f"batch {i}", rr.state, g)
             st = rr.state
         print(f"# {spec or 'default'}: mean {np.mean(rows):.2f} ms/batch over {len(rows)} batches "
               f"(max {np.max(rows):.1f}); flows {'same' if True else ''}", flush=True)

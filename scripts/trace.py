@@ -47,7 +47,7 @@ def report(tag, st, g, res):
             print(f"    state {int(states[i])} done {int(d[i])} tail {int(t[i])}")
         keep = ~raw
         ph, items, dt = ph[keep], items[keep], dt[keep]
-    keep = (ph != 6) & (ph != 5) & (ph != 4)  # epoch stats / tail waves / CTA-0 wave work (rounds_view)
+    keep = (ph != 6) & (ph != 5) & (ph != 4) & (ph < 8)  # epoch stats / tail waves / CTA-0 wave work (rounds_view)
     ph, items, dt = ph[keep], items[keep], dt[keep]
     print(f"== {tag}: {res.device['ms_solve']:.2f} ms, rounds {res.rounds}, "
           f"levels {res.device['bfs_levels']}, waves {res.device['waves']}, barriers {len(ph)}")
@@ -70,7 +70,7 @@ def rounds_view(tag, st, g):
     """Per round: BFS epochs + time (+ vertices expanded: sum / max per CTA,
     from the phase-6 entries), then the push waves' item counts."""
     ph, items, dt = fetch(st, g)
-    keep = ph != 7
+    keep = (ph != 7) & (ph < 8)  # (8, 9: relabel exit inputs)
     ph, items, dt = ph[keep], items[keep], dt[keep]
     # a phase-6 entry follows its epoch's barrier entry
     xs = {}
