@@ -129,14 +129,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--side", type=int, default=2048)
     ap.add_argument("--max-waves", type=int, default=0)
+    ap.add_argument("--graph", default="grid", choices=["grid", "road"])
+    ap.add_argument("--static-only", action="store_true")
     args = ap.parse_args()
-    us, vs, caps, s, t = gen.grid_graph(args.side, args.side, 0)
-    n = args.side * args.side + 2
+    if args.graph == "road":
+        us, vs, caps, s, t = gen.road_graph(args.side, args.side, 0, 0.21)
+        n = args.side * args.side
+    else:
+        us, vs, caps, s, t = gen.grid_graph(args.side, args.side, 0)
+        n = args.side * args.side + 2
     g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps))
     p = mfx.SolverParams(max_waves=args.max_waves)
     mfx.solve_static(g, s, t, p)
     r = mfx.solve_static(g, s, t, p)
     report("static", r.state, g, r)
+    if args.static_only:
+        rounds_view("static", r.state, g)
+        return
     el = g.to_edge_list()
     bu, bv, bc, _ = gen.fast_batch(n, el.us, el.vs, el.caps, s, t, 10000, "mixed", 0)
     rr = mfx.solve_dynamic(r.state, g, mfx.UpdateBatch(bu, bv, bc), p)
