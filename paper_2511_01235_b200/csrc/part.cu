@@ -341,26 +341,59 @@ __global__ void part_bfs_init_kernel(PeerTab T, int me, int nl, int s, int t, in
   }
 }
 
-__device__ __forceinline__ void part_discover(const PeerTab &T, int me, int i, int L, int cur, int s,
-                                              int t, int forbidden, int rcap) {
-  int v = T.adj[me][i];
-  if (v == forbidden) return;
-  int r = T.pc[me][i] - vol_ld(T.cf[me] + i);  // reverse residual cf[rev i] (pair sum)
-  if (r <= 0) return;
-  int p = owner_of(T, v);
-  int vl = v - T.lo[p];
-  int *hp = T.h[p] + vl;
-  if (vol_ld(hp) != T.n) return;
-  if (atomicCAS_system(hp, T.n, L + 1) != T.n) return;
-  int b = heavy_of(T, p, vl);
-  int pos = atomicAdd_system(T.ctr[p] + PC_FN0 + b, 1);
-  T.F[p][cur ^ 1][b][pos] = vl;
-  atomicAdd_system(T.ctr[p] + PC_REACHED, 1);
-  if (v != s && v != t && vol_ld(T.ex[p] + vl) > 0) {
-    atomicAdd_system(T.ctr[p] + PC_ACTIVE, 1);
-    int q = atomicAdd_system(T.ctr[p] + PC_RT0 + b, 1);
-    if (q < rcap) T.R[p][b][q] = vl;
-    else atomicExch_system(T.ctr[p] + PC_OVF, 1);
+// Discovery through slot i of a frontier row (warp-synchronous: every lane of
+// the warp calls, `valid` lanes hold a slot).  The owner's height is claimed
+// by a system-scope CAS per discovery; the owner-side counters (next-frontier
+// append, reached, active count, round-list append) take ONE system-scope
+// atomic per (owner, degree class) group of the warp instead of one per
+// discovery: over NVLink every remote atomic is a round trip to the owner's
+// L2, and all of a level's discoveries hit the same few counter words.
+__device__ __forceinline__ void part_discover_w(const PeerTab &T, int me, bool valid, int i, int L,
+                                                int cur, int s, int t, int forbidden, int rcap) {
+  const unsigned FULLM = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int p = 0, vl = 0, b = 0;
+  bool disc = false, act = false;
+  if (valid) {
+    const int v = T.adj[me][i];
+    if (v != forbidden && T.pc[me][i] - vol_ld(T.cf[me] + i) > 0) {  // reverse residual cf[rev i]
+      p = owner_of(T, v);
+      vl = v - T.lo[p];
+      int *hp = T.h[p] + vl;
+      if (vol_ld(hp) == T.n && atomicCAS_system(hp, T.n, L + 1) == T.n) {
+        disc = true;
+        b = heavy_of(T, p, vl);
+        act = v != s && v != t && vol_ld(T.ex[p] + vl) > 0;
+      }
+    }
+  }
+  if (!__any_sync(FULLM, disc)) return;
+  const unsigned lt = lanemask_lt();
+  {  // next frontier of the owner, per (owner, class)
+    const unsigned g = __match_any_sync(FULLM, disc ? (unsigned)(p * 2 + b) : ~0u);
+    const int ld = __ffs(g) - 1;
+    int pos = 0;
+    if (disc && lane == ld) pos = atomicAdd_system(T.ctr[p] + PC_FN0 + b, __popc(g));
+    pos = __shfl_sync(FULLM, pos, ld) + __popc(g & lt);
+    if (disc) T.F[p][cur ^ 1][b][pos] = vl;
+  }
+  {  // reached, per owner
+    const unsigned g = __match_any_sync(FULLM, disc ? (unsigned)p : ~0u);
+    if (disc && lane == __ffs(g) - 1) atomicAdd_system(T.ctr[p] + PC_REACHED, __popc(g));
+  }
+  if (!__any_sync(FULLM, act)) return;
+  {  // active: the owner's round list, per (owner, class), and its count, per owner
+    const unsigned g = __match_any_sync(FULLM, act ? (unsigned)(p * 2 + b) : ~0u);
+    const int ld = __ffs(g) - 1;
+    int q = 0;
+    if (act && lane == ld) q = atomicAdd_system(T.ctr[p] + PC_RT0 + b, __popc(g));
+    q = __shfl_sync(FULLM, q, ld) + __popc(g & lt);
+    if (act) {
+      if (q < rcap) T.R[p][b][q] = vl;
+      else atomicExch_system(T.ctr[p] + PC_OVF, 1);
+    }
+    const unsigned g2 = __match_any_sync(FULLM, act ? (unsigned)p : ~0u);
+    if (act && lane == __ffs(g2) - 1) atomicAdd_system(T.ctr[p] + PC_ACTIVE, __popc(g2));
   }
 }
 
@@ -374,14 +407,17 @@ __global__ void part_bfs_expand_kernel(PeerTab T, int me, int L, int cur, int cn
   for (int j = gwarp; j < cnt0; j += gwarps) {  // warp per light row
     int u = F0[j];
     int lo = T.off[me][u], hi = T.off[me][u + 1];
-    for (int i = lo + lane; i < hi; i += 32) part_discover(T, me, i, L, cur, s, t, forbidden, rcap);
+    for (int i0 = lo; i0 < hi; i0 += 32)
+      part_discover_w(T, me, i0 + lane < hi, i0 + lane, L, cur, s, t, forbidden, rcap);
   }
   for (int j = blockIdx.x; j < cnt1; j += gridDim.x) {  // CTA per heavy row
     int u = F1[j];
     int lo = T.off[me][u], hi = T.off[me][u + 1];
     if (hi - lo > kPartHuge) continue;  // hubs: below
-    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
-      part_discover(T, me, i, L, cur, s, t, forbidden, rcap);
+    for (int i0 = lo + (threadIdx.x & ~31); i0 < hi; i0 += blockDim.x) {  // warp-uniform trips
+      const int i = i0 + (threadIdx.x & 31);
+      part_discover_w(T, me, i < hi, i, L, cur, s, t, forbidden, rcap);
+    }
   }
   // hubs of this level (the frontier of a level-synchronous BFS is {h == L}):
   // the whole grid per row
@@ -390,7 +426,10 @@ __global__ void part_bfs_expand_kernel(PeerTab T, int me, int L, int cur, int cn
     const int u = huge[j];
     if (vol_ld(T.h[me] + u) != L) continue;
     const int lo = T.off[me][u], hi = T.off[me][u + 1];
-    for (int i = lo + gtid; i < hi; i += gthreads) part_discover(T, me, i, L, cur, s, t, forbidden, rcap);
+    for (int i0 = lo + (gtid & ~31); i0 < hi; i0 += gthreads) {
+      const int i = i0 + (gtid & 31);
+      part_discover_w(T, me, i < hi, i, L, cur, s, t, forbidden, rcap);
+    }
   }
 }
 
@@ -468,6 +507,33 @@ __device__ __forceinline__ void part_activate(const PeerTab &T, int v, unsigned 
   int q = atomicAdd_system(T.ctr[p] + PC_RT0 + b, 1);
   if (q < rcap) T.R[p][b][q] = vl;
   else atomicExch_system(T.ctr[p] + PC_OVF, 1);
+}
+
+// Warp-synchronous part_activate (every lane calls; `pred` lanes activate v):
+// the per-vertex stamp stays one atomic each, the owner's round-list append
+// is one system-scope atomic per (owner, class) group of the warp.
+__device__ __forceinline__ void part_activate_w(const PeerTab &T, bool pred, int v, unsigned stamp,
+                                                int s, int t, int rcap) {
+  const unsigned FULLM = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int p = 0, vl = 0, b = 0;
+  if (pred && (v == s || v == t)) pred = false;
+  if (pred) {
+    p = owner_of(T, v);
+    vl = v - T.lo[p];
+    pred = atomicMax_system(T.mark[p] + vl, stamp) < stamp;  // not yet in the next wave
+    if (pred) b = heavy_of(T, p, vl);
+  }
+  if (!__any_sync(FULLM, pred)) return;
+  const unsigned g = __match_any_sync(FULLM, pred ? (unsigned)(p * 2 + b) : ~0u);
+  const int ld = __ffs(g) - 1;
+  int q = 0;
+  if (pred && lane == ld) q = atomicAdd_system(T.ctr[p] + PC_RT0 + b, __popc(g));
+  q = __shfl_sync(FULLM, q, ld) + __popc(g & lanemask_lt());
+  if (pred) {
+    if (q < rcap) T.R[p][b][q] = vl;
+    else atomicExch_system(T.ctr[p] + PC_OVF, 1);
+  }
 }
 
 template <int G>
@@ -579,14 +645,15 @@ __device__ void part_push_row(const PeerTab &T, int me, int u, int kc, unsigned 
       }
       long long room = eu - carry - (incl - c);
       long long amt = room <= 0 ? 0 : (room < c ? room : c);
+      long long old = 1;
       if (amt > 0) {
         atomicAdd(cf + i, (int)-amt);
         sys_add(T.cf[p] + rev[i], (int)amt);
-        long long old = sys_add(T.ex[p] + (v - T.lo[p]), amt);
+        old = sys_add(T.ex[p] + (v - T.lo[p]), amt);
         loc[PS_PUSH]++;
         loc[PS_BYTES] += 28;
-        if (old <= 0) part_activate(T, v, stamp, s, t, rcap);
       }
+      part_activate_w(T, amt > 0 && old <= 0, v, stamp, s, t, rcap);  // (warp-uniform loop)
       carry += tot;
     }
     long long moved = carry < eu ? carry : eu;
