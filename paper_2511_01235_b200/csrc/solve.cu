@@ -923,11 +923,16 @@ struct Kern {
     // reverse residual of t's row, pc - cf); with none, only deficits can
     // absorb excess this round (push-phase stop rule, Ctrl::fills)
     if (!PP) {
+      // (only "none" vs "some" matters: a thread stops at its first hit, so
+      // the 2.1 M-slot sink row of C2 costs one pass of loads, not 28; and
+      // only the dynamic rules read it)
       int talive = 0;
-      const int t0 = __ldg(a.off + a.t), t1 = __ldg(a.off + a.t + 1);
-      for (int i = t0 + gtid; i < t1; i += gthreads)
-        talive += __ldg(a.adj + i) != a.forbidden &&
-                  __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i)) > 0;
+      if (a.strand) {
+        const int t0 = __ldg(a.off + a.t), t1 = __ldg(a.off + a.t + 1);
+        for (int i = t0 + gtid; i < t1 && talive == 0; i += gthreads)
+          talive = __ldg(a.adj + i) != a.forbidden &&
+                   __ldg(a.pc + i) - (CapT)ldcg((const CapT *)(a.cf + i)) > 0;
+      }
       talive = warp_sum(talive);
       dbases = warp_sum(dbases);
       if (lane == 0 && talive) atomicAdd(a.ctrl->live + C_TALIVE, talive);
