@@ -331,8 +331,9 @@ def bench_ours(args, cfg, rank, world, dev, pg, backend):
     for i in range(W):
         bu, bv, bc = dbat[i]
         mfx.solve_dynamic_device(st, g, k, bu.data_ptr(), bv.data_ptr(), bc.data_ptr(), params)
-    # snapshot for the e2e replay of the same batches
+    # snapshots for the e2e replay and the O2 push-pull replay of the same batches
     g_snap, st_snap = (None, None) if args.profile else (g.copy(), st.copy())
+    g_pp, st_pp = (None, None) if args.profile else (g.copy(), st.copy())
     torch.cuda.synchronize()
 
     rows = []
@@ -388,6 +389,18 @@ def bench_ours(args, cfg, rank, world, dev, pg, backend):
     L.mfx_transfer_bytes(k, ctypes.byref(h2d), ctypes.byref(d2h))
     out.update(e2e_ms_per_step=e2e_ms / K, e2e_h2d=int(h2d.value), e2e_d2h=int(d2h.value))
     del g_snap, st_snap
+
+    # ---- the reference bench's second dynamic mode (bench.py:150-198):
+    # solve_dynamic_pushpull (O2) on the same batches from the same state
+    pp_ms, pp_flows = [], []
+    for i in range(W, W + K):
+        r = mfx.solve_dynamic_pushpull(st_pp, g_pp, mfx.UpdateBatch(*chain[i]), params)
+        pp_ms.append(r.device["ms_total"])
+        pp_flows.append(r.flow_value)
+        st_pp = r.state
+    assert pp_flows == out["flows"], (pp_flows, out["flows"])
+    out["pushpull_ms"] = pp_ms
+    del g_pp, st_pp
 
     # ---- GPU static re-solve on the updated capacities (the comparison point)
     st2 = mfx.init_residuals(g, s, t)
@@ -462,6 +475,11 @@ def emit_ours(args, out, world):
         "dynamic_speedup_vs_gpu_static_resolve": (round(out["resolve_ms"] / value, 2)
                                                   if "resolve_ms" in out else None),
         "flow_static": out["static_flow"], "flows": out["flows"],
+        "pushpull_ms_per_batch": (round(float(np.mean(out["pushpull_ms"])), 4)
+                                  if "pushpull_ms" in out else None),
+        "pushpull_speedup_vs_gpu_static_resolve": (
+            round(out["resolve_ms"] / float(np.mean(out["pushpull_ms"])), 2)
+            if "pushpull_ms" in out and "resolve_ms" in out else None),
         "per_batch_ms": [round(x, 3) for x in out["solve_ms"]],
         "rounds_per_batch": round(float(np.mean(out["rounds"])), 2),
         "gpu_launches": out["launches"],

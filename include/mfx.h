@@ -206,6 +206,9 @@ int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_p
 
 /* Diagnostics: per-barrier trace of the last solve launch when the process
  * ran with $MFX_TRACE_CAP > 0.  Entry = phase << 60 | items << 32 | ns. */
+/* Diagnostics: the reached-set list the last tracked relabel kept (sparse
+ * relabels seed from it); *count = -1 when the state holds no valid list. */
+int mfx_reached_list(const mfx_state *st, int32_t *out, int64_t cap, int64_t *count);
 int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int64_t cap,
                     int64_t *count);
 /* Host<->device bytes one mfx_solve_dynamic call of k updates moves. */

@@ -113,6 +113,8 @@ StateObj::~StateObj() {
   dfree(ex);
   dfree(h);
   dfree(ctrl);
+  dfree(tl[0]);
+  dfree(tl[1]);
 }
 
 cudaError_t ensure_workspace(Topology &t) {
@@ -631,6 +633,14 @@ int mfx_state_copy(const mfx_state *st, mfx_state **out) {
   if (!e) e = cudaMemcpyAsync(d.ex, st->s.ex, sizeof(long long) * T.n, cudaMemcpyDeviceToDevice, T.stream);
   if (!e) e = cudaMemcpyAsync(d.h, st->s.h, sizeof(int) * T.n, cudaMemcpyDeviceToDevice, T.stream);
   if (!e) e = cudaMemcpyAsync(d.ctrl, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToDevice, T.stream);
+  // the reached-set lists travel with the control block (a snapshot resumes
+  // sparse relabels at once, and its first solve allocates nothing)
+  for (int q = 0; q < 2 && !e && st->s.tl[q]; ++q) {
+    e = cudaMalloc(&d.tl[q], sizeof(int) * (size_t)T.n);
+    if (!e) e = cudaMemcpyAsync(d.tl[q], st->s.tl[q], sizeof(int) * (size_t)T.n,
+                                cudaMemcpyDeviceToDevice, T.stream);
+  }
+  if (!e) d.tl_ok = st->s.tl_ok && d.tl[1] != nullptr;
   if (!e) e = cudaStreamSynchronize(T.stream);
   if (e) {
     delete S;
@@ -656,6 +666,7 @@ int mfx_state_assign(mfx_state *dst, const mfx_state *src) {
   dst->s.excess_consistent = src->s.excess_consistent;
   dst->s.terminated_known = src->s.terminated_known;
   dst->s.cap_id = src->s.cap_id;
+  dst->s.tl_ok = false;
   return MFX_OK;
 }
 
@@ -686,6 +697,7 @@ int mfx_state_upload(mfx_state *st, const int64_t *cf, const int64_t *excess,
   }
   st->s.excess_consistent = false;
   st->s.terminated_known = false;
+  st->s.tl_ok = false;
   st->s.cap_id = 0;  // arbitrary residuals: pair sums are checked at the next use
   return MFX_OK;
 }
@@ -774,6 +786,8 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   cfg.strand = -1;  // auto: on in dynamic solves
   if (const char *sr = getenv("MFX_STRAND")) cfg.strand = atoi(sr);
   if (const char *ee = getenv("MFX_EARLY")) cfg.early = atoi(ee);
+  if (const char *tr = getenv("MFX_TRACK")) cfg.track = atoi(tr);
+  if (const char *sp = getenv("MFX_SPARSE")) cfg.sparse = atoi(sp);
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;
@@ -807,8 +821,11 @@ static void fill_result(const mfx_state *st, mfx_result *r) {
   r->bfs_epochs = (int64_t)c.epochs;
 }
 
-static int solve_status(const mfx_state *st, mfx_result *r) {
+static int solve_status(mfx_state *st, mfx_result *r) {
   const Ctrl &c = *st->host_ctrl;
+  // the reached-set list is valid iff the launch's last relabel kept it and
+  // nothing aborted (an aborted relabel leaves its list partial)
+  st->s.tl_ok = c.status == 0 && c.tl_ok != 0;
   if (c.status == 6)
     return fail(MFX_TIMEOUT, "device watchdog expired after %lld rounds", (long long)c.rounds);
   if (c.status == 3)
@@ -973,6 +990,7 @@ static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const in
   cfg.dyn_bases = 1;
   cfg.forbidden = st->s.s;
   cfg.gate = T.ws.d_err;
+  cfg.batch_k = k;
   // the excess walk ($MFX_WALK_MAX / $MFX_WALK_DEPTH) is off by default since
   // the early-exit relabel and the stranded-excess rule: C4 16.5 (off) vs
   // 19.3 ms/batch (4096 / 1024)
@@ -995,7 +1013,10 @@ static int solve_dynamic_common(mfx_graph *g, mfx_state *st, int64_t k, const in
   CK(cudaEventRecord(T.ev[3], T.stream));
   CK(cudaEventSynchronize(T.ev[3]));
   CK(cudaGetLastError());
-  if ((rc = batch_error(st->host_err, k, h_us, h_vs, h_caps, d_us, d_vs, d_caps))) return rc;
+  if ((rc = batch_error(st->host_err, k, h_us, h_vs, h_caps, d_us, d_vs, d_caps))) {
+    st->s.tl_ok = false;  // (the kernel skipped: conservative, the next relabel seeds in full)
+    return rc;
+  }
   if (k > 0) g->g.cap_id = next_cap_id();
   st->s.cap_id = g->g.cap_id;
   fill_result(st, r);
@@ -1312,6 +1333,23 @@ int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int6
   if (tn > T.ws.trace_cap) tn = T.ws.trace_cap;
   if (tn > 0) CK(cudaMemcpy(out, T.ws.trace, sizeof(uint64_t) * tn, cudaMemcpyDeviceToHost));
   *count = tn;
+  return MFX_OK;
+}
+
+int mfx_reached_list(const mfx_state *st, int32_t *out, int64_t cap, int64_t *count) {
+  Topology &T = *st->s.topo;
+  LOCK_TOPO(T);
+  CK(cudaSetDevice(T.device));
+  *count = -1;
+  if (!st->s.tl_ok) return MFX_OK;
+  Ctrl c;
+  CK(cudaMemcpy(&c, st->s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  long long cnt = c.snap[C_REACHED];
+  if (cnt > cap) return fail(MFX_VALUE_ERROR, "reached list of %lld entries exceeds cap %lld", cnt,
+                             (long long)cap);
+  if (cnt > 0)
+    CK(cudaMemcpy(out, st->s.tl[c.tl_cur & 1], sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+  *count = cnt;
   return MFX_OK;
 }
 

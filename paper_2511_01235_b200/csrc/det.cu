@@ -99,6 +99,7 @@ __global__ void det_round_kernel(const int *__restrict__ off, const int *__restr
 cudaError_t launch_det_round(const GraphObj &g, StateObj &st, int kc, int topology) {
   const Topology &T = *g.topo;
   int *work = T.ws.heavy;  // capacity n; the deterministic loop owns the workspace
+  st.tl_ok = false;
   if (T.cap_bytes == 8)
     det_round_kernel<long long><<<1, 32, 0, T.stream>>>(T.off, T.adj, T.rev, (long long *)st.cf,
                                                         st.ex, st.h, work, T.n, st.s, st.t, kc,

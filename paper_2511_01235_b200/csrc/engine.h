@@ -79,6 +79,12 @@ struct StateObj {
   int *h = nullptr;          // int32[n]
   Ctrl *ctrl = nullptr;      // control block
   bool excess_consistent = true;  // excess == sum_row(cf - cap0) known to hold
+  // Reached-set lists (int32[n] each, allocated by the first tracked solve):
+  // a tracked solve appends every vertex its relabels reach, so
+  // tl[ctrl->tl_cur][0, ctrl->reached) is exactly {h < n}.  tl_ok: that holds
+  // now (cleared by anything else that writes h).
+  int *tl[2] = {nullptr, nullptr};
+  bool tl_ok = false;
   bool terminated_known = false;  // last op was a completed solve
   uint64_t cap_id = 0;            // capacities cf / excess were last consistent with
   ~StateObj();
@@ -122,6 +128,9 @@ struct SolveConfig {
   bool deterministic = false;  // serial round kernel (det.cu), reference deterministic mode
   int strand = 0;  // push phase ends once the sink is cut off and every deficit is filled
   int early = 1;   // solve relabels stop once every excess holder is labelled (0 off)
+  int track = 1;   // WHAT_SOLVE launches keep the reached-set list (StateObj::tl; 0 off)
+  int sparse = 1;  // relabels reset / seed from that list when it is small (0 off)
+  long long batch_k = 0;  // dynamic solves: updates of the batch (their endpoints seed too)
 };
 
 // Dispatch to the solve-kernel build chosen for the graph (Topology::variant).

@@ -98,6 +98,10 @@ struct Ctrl {
   // far; live = appended this epoch, snap = the leader's running totals
   long long x_live[2], x_snap[2];
   long long efill_d;  // total deficit at the last early exit it allowed (must shrink)
+  // reached-set lists (StateObj::tl): which of the two holds the last
+  // global relabel's reached set (tracked solves flip it per relabel)
+  int tl_cur;
+  int tl_ok;  // the last relabel of the last launch kept its list (StateObj::tl_ok)
   unsigned long long epochs;       // grid barriers spent in global relabels
   // push waves run by CTA 0 alone (thin waves): state for the other CTAs
   int tail_base[NBIN];

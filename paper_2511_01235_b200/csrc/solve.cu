@@ -42,6 +42,17 @@ namespace MFX_SOLVE_NS {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// length of the reached-set list at the start of the current BFS epoch
+// (tracked launches; 0 during the seeding pass)
+__shared__ int s_tl_base;
+// which reached-set list holds the last relabel's reach (Ctrl::tl_cur; each
+// CTA's copy, flipped by its thread 0 at the end of every tracked relabel)
+__shared__ int s_tl_cur;
+// the running relabel appends to its list (its predecessor reached < n/16,
+// so it is expected to reach few vertices too); the last relabel's list is
+// valid (launch: the host's StateObj::tl_ok; then: that relabel tracked)
+__shared__ int s_tl_trk, s_tl_ok;
+
 template <typename CapT>
 struct SolveArgs {
   int n;
@@ -69,6 +80,11 @@ struct SolveArgs {
   int strand;        // end a push phase once the sink is cut off and every deficit is filled
   int early;         // solve relabels stop once every excess holder is labelled
   int ring_sleep;    // ns an idle warp sleeps between polls of the BFS ring
+  int track;         // keep the reached-set list: every relabel appends what it reaches
+  int sparse;        // the first relabel may seed from the list (StateObj::tl_ok)
+  int *tl[2];        // the two reached-set lists (n each)
+  const int *buv;    // the batch's (u, v) endpoints (2 * bk), first relabel after a batch
+  long long bk;
   const uint8_t *__restrict__ reg;  // push-pull: 1 = prior cut's A side (pull), 0 = B side
   int *bmark;        // per-vertex epoch stamp: next-frontier dedupe
   int topology;
@@ -118,8 +134,8 @@ struct Local {
 constexpr int kWQ = MFX_WQ;         // per-warp staging capacity (per queue)
 constexpr int kFlush = kWQ - 32;    // publish once this many items are staged
 struct WarpQ {
-  int cnt[2];
-  int item[2][kWQ];
+  int cnt[3];
+  int item[3][kWQ];  // q0 next frontier, q1 round list, q2 reached-set list (track)
 };
 
 // ---------------------------------------------------------------------------
@@ -195,9 +211,7 @@ __device__ __noinline__ void grid_sync(Ctrl *c, Sync &sy, unsigned snap_mask, un
                           d < vc->efill_d;
         if (fire) vc->efill_d = d;
         vc->snap[C_EFILL] = fire;
-      } else if (phase == PH_BFS) {
-        vc->snap[C_EFILL] = 0;
-      }
+      }  // (other BFS barriers -- sparse reset, exit listing -- keep it)
       const unsigned long long now = globaltimer();
       const unsigned long long wdl = vc->wave_deadline;
       vc->snap[C_STOP] = phase == PH_PUSH && ((wdl != 0 && now > wdl) ||
@@ -303,6 +317,9 @@ struct Kern {
   int swarp;  // warp index with CTAs fastest: thin lists spread over every SM
   int *rctr;  // next-wave list counters: the global live ones, or CTA 0's own in tail mode
   int act_cnt;  // active discoveries counted by this lane in the current level
+  // the list the running relabel appends to / the last relabel's
+  __device__ __forceinline__ int *tl_new() const { return s_tl_cur ? a.tl[0] : a.tl[1]; }
+  __device__ __forceinline__ const int *tl_old() const { return s_tl_cur ? a.tl[1] : a.tl[0]; }
   long long *s_sink;  // per-CTA sum of excess pushed into the sink this round
   long long sink_acc; // this thread's share, not yet added to s_sink
 
@@ -638,6 +655,12 @@ struct Kern {
     const bool act = first && u != a.s && u != a.t && (ru == 1 ? eu < 0 : eu > 0);
     act_cnt += act;
     if (!PP && act) hexc += eu;
+    // reached-set list: a vertex joins at its first expansion (exactly once
+    // per relabel: one first-visit item per discovery); an early exit lists
+    // the first-visit items it leaves unexpanded (exit_list).  The append
+    // counter is C_REACHED itself.  (Appending at the discovery instead put
+    // one more inlined append per slot into the hot loop: C2 +8 %.)
+    if (s_tl_trk) stage(2, first, u, a.ctrl->live + C_REACHED, tl_new(), s_tl_base, a.n);
     // queued for the push phase: owned (async) / listed for wave 0 (walk dedupe)
     if (act && (a.async || a.walk_max > 0)) a.mark[u] = ep_next;
     append_binned(1, act && !a.topology, u, bin_of(d), a.ctrl->live + C_RNEXT, a.R, rb_, a.rcap);
@@ -729,8 +752,12 @@ struct Kern {
       if (lane == 0 && x) atomicAdd((unsigned long long *)&a.ctrl->x_live[1], (unsigned long long)x);
       hexc = 0;
     }
-    c = warp_sum(disc_cnt);
-    if (lane == 0 && c) atomicAdd(a.ctrl->live + C_REACHED, c);
+    if (s_tl_trk) {
+      stage_flush(2, a.ctrl->live + C_REACHED, tl_new(), s_tl_base, a.n);
+    } else {
+      c = warp_sum(disc_cnt);
+      if (lane == 0 && c) atomicAdd(a.ctrl->live + C_REACHED, c);
+    }
     disc_cnt = 0;
     int m = max_lab;
 #pragma unroll
@@ -739,6 +766,24 @@ struct Kern {
       m = w > m ? w : m;
     }
     if (lane == 0 && m) atomicMax(a.ctrl->live + C_DEPTH, m);
+  }
+
+  // Early exit of a tracked relabel: the first-visit items of the frontier
+  // it leaves unexpanded (bin 0 of epoch E's list) join the reached-set
+  // list, whose length the barrier then publishes.  Whole grid.
+  __device__ void exit_list(int E, int cnt0) {
+    if (!s_tl_trk) return;
+    __syncthreads();
+    if (threadIdx.x == 0) s_tl_base = sy.s_snap[C_REACHED];
+    __syncthreads();
+    const int *Fc0 = (E & 1) ? a.F1[0] : a.F0[0];
+    for (int j0 = gwarp * 32; j0 < cnt0; j0 += gwarps * 32) {
+      const int j = j0 + lane;
+      const int item = j < cnt0 ? ldcg(Fc0 + j) : 0;
+      stage(2, item < 0, item & kIdMask, a.ctrl->live + C_REACHED, tl_new(), s_tl_base, a.n);
+    }
+    stage_flush(2, a.ctrl->live + C_REACHED, tl_new(), s_tl_base, a.n);
+    grid_sync(a.ctrl, sy, 0, 1u << C_REACHED, 0, PH_BFS);
   }
 
   // Trace mode: per-epoch expansion counts (sum and max over CTAs), recorded
@@ -776,7 +821,16 @@ struct Kern {
   // means no residual out-arc, which nothing adds back: no push or repair
   // can target a vertex at height n.)  Not after a batch: its updates and
   // the source re-saturation change arbitrary arcs.
-  __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels, bool early, bool filt) {
+  //
+  // Reached-set lists (StateObj::tl): a relabel whose predecessor reached
+  // fewer than n/16 vertices appends everything it reaches (bases + first
+  // discoveries) to a list, so {h < n} is exactly that list's entries.  The
+  // next relabel then resets and searches bases over the list (plus the
+  // batch endpoints, where a negative repair can create a deficit, on the
+  // first relabel after a batch) instead of all n vertices: C4's sink side
+  // is a corner, so a relabel there costs its reach, not a 24 M-vertex pass.
+  __device__ int bfs(unsigned ep, unsigned &bstamp, int local_levels, bool early, bool filt,
+                     bool first_after_batch) {
     const int n = a.n;
     int holders = 0;  // vertices (not s, t) with positive excess
     int dbases = 0;   // deficient bases (bases other than the sink)
@@ -793,7 +847,14 @@ struct Kern {
     // level-synchronous mode, which lists every vertex at most once.
     int E_all = 0;  // epochs over the attempts
     if (gtid == 0) a.ctrl->bfs_t0 = globaltimer();  // (push-phase time budget)
+    const int reached_old = sy.s_snap[C_REACHED];  // (the last relabel's; uniform)
+    const bool trk = a.track && !PP && !a.topology && (long long)reached_old * 16 < (long long)n;
+    const bool sparse0 = trk && a.sparse && s_tl_ok;
+    __syncthreads();  // (everyone has read s_tl_ok)
+    if (threadIdx.x == 0) s_tl_trk = trk;
     for (int attempt = 0;; ++attempt) {
+    const bool sparse = sparse0 && attempt == 0;  // (the strict retry seeds in full)
+    if (threadIdx.x == 0) s_tl_base = 0;
     ep_next = ep;
     disc_cnt = 0;
     max_lab = 0;
@@ -838,7 +899,45 @@ struct Kern {
     // flight together and 2 x 16-byte height stores (the pass is a latency
     // chain otherwise); the rare bases are appended only when the warp has one.
     constexpr int V = 8;
-    for (int v0 = gwarp * 32 * V; v0 < n; v0 += gwarps * 32 * V) {
+    if (sparse) {
+      // 1) reset the last relabel's reach (holders among it: the filt rule)
+      const int *Lo = tl_old();
+      for (int j = gtid; j < reached_old; j += gthreads) {
+        const int v = ldcg(Lo + j);
+        if (filt)
+          holders += v != a.s && v != a.t && ldcg(a.h + v) < n && ldcg(a.ex + v) > 0;
+        a.h[v] = n;
+      }
+      if (!filt && gtid == 0) holders = 1 << 29;  // (all holders unknown: EHOLD rule off)
+      lc.bytes += (unsigned long long)((reached_old + gthreads - 1 - gtid) / gthreads) * 8ull;
+      grid_sync(a.ctrl, sy, 0, 0, 0, PH_BFS);  // every reset lands before a base is claimed
+      // 2) bases: deficits can only sit in the old reach (they were bases of
+      // the last relabel) or at a batch endpoint (negative repair); t always
+      const long long nb_ll = (long long)reached_old + (first_after_batch ? 2 * a.bk : 0) + 1;
+      const int nb = nb_ll > (long long)INT_MAX ? INT_MAX : (int)nb_ll;
+      for (int j0 = gwarp * 32; j0 < nb; j0 += gwarps * 32) {
+        const int j = j0 + lane;
+        int v = -1;
+        if (j < reached_old) v = ldcg(Lo + j);
+        else if (j < nb - 1) v = ldcg(a.buv + (j - reached_old));
+        else if (j == nb - 1) v = a.t;
+        bool base = false;
+        long long e = 0;
+        if (v >= 0 && v != a.forbidden) {
+          e = ldcg(a.ex + v);
+          base = v == a.t || (a.dyn_bases && v != a.s && e < 0);
+          if (base) base = atomicCAS(a.h + v, n, 0) == n;  // once per vertex
+        }
+        dbases += base && v != a.t;
+        if (base && v != a.t) dsum -= e;
+        const int b = base ? vbin(v) : 0;
+        append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
+        direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
+        stage(2, base, v, a.ctrl->live + C_REACHED, tl_new(), 0, n);
+      }
+      lc.bytes += (unsigned long long)((nb + gthreads - 1 - gtid) / gthreads) * 16ull;
+    }
+    for (int v0 = gwarp * 32 * V; !sparse && v0 < n; v0 += gwarps * 32 * V) {
       const int vb = v0 + lane * V;
       const bool full = vb + V <= n;
       long long ev[V];
@@ -904,6 +1003,7 @@ struct Kern {
           int b = base ? vbin(v) : 0;
           append_binned(0, base, v, b, a.ctrl->live + C_FNEXT, a.F0, zero, n);
           direct(base, v, a.ctrl->live + C_BASES, a.bases, 0, n);
+          if (trk) stage(2, base, v, a.ctrl->live + C_REACHED, tl_new(), 0, n);
         }
       }
       if (a.topology) {
@@ -943,7 +1043,7 @@ struct Kern {
       if (gtid == 0 && !a.strand) atomicAdd(a.ctrl->live + C_DBASES, 1 << 30);  // rule off
       if (gtid == 0) a.ctrl->fills = 0;
     }
-    lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
+    if (!sparse) lc.bytes += (unsigned long long)((n + gthreads - 1 - gtid) / gthreads) * 12ull;
     const unsigned fmask = 0xFu << C_FNEXT, rmask = 0xFu << C_RNEXT;
     const unsigned amask = (1u << C_ACTIVE) | (1u << C_REACHED) | (1u << C_DEPTH) |
                            (1u << C_EHOLD) | (1u << C_TALIVE) | (1u << C_DBASES);
@@ -973,15 +1073,22 @@ struct Kern {
       // keep h = n, which no push can cross, and the solve's last global
       // relabel (no holder left) always runs to the end, so the certificate
       // still comes from exact distances.
-      if (early && sy.s_snap[C_EHOLD] > 0 && sy.s_snap[C_ACTIVE] >= sy.s_snap[C_EHOLD]) break;
+      if (early && sy.s_snap[C_EHOLD] > 0 && sy.s_snap[C_ACTIVE] >= sy.s_snap[C_EHOLD]) {
+        exit_list(E, cnt[0]);
+        break;
+      }
       // Demand-covered exit (dynamic solves, sink cut off): the holders
       // labelled so far carry at least the total deficit, so this round's
       // pushes can fill every deficit without the far holders (C4: a batch's
       // new deficit is a few hops from the excess its decrease created,
       // while excess stranded near the source lies ~10^4 levels away).  The
       // barrier leader allows it only while the total deficit shrinks.
-      if (early && sy.s_snap[C_EFILL]) break;
+      if (early && sy.s_snap[C_EFILL]) {
+        exit_list(E, cnt[0]);
+        break;
+      }
       if (threadIdx.x < NBIN) rb[threadIdx.x] = sy.s_snap[C_RNEXT + threadIdx.x];
+      if (threadIdx.x == 0) s_tl_base = sy.s_snap[C_REACHED];
       __syncthreads();
       rb_ = rb;
       bst = ++bstamp;
@@ -1067,6 +1174,17 @@ struct Kern {
     filt = false;
     __syncthreads();
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // a tracked relabel's list is the current one now
+      if (trk) s_tl_cur ^= 1;
+      s_tl_ok = trk;
+      s_tl_trk = 0;
+      if (blockIdx.x == 0) {
+        a.ctrl->tl_cur = s_tl_cur;
+        a.ctrl->tl_ok = trk;
+      }
+    }
+    __syncthreads();
     const int depth = sy.s_snap[C_DEPTH] + 1;
     if (sy.trace && threadIdx.x == 0 && sy.trace_n + 1 < sy.trace_cap) {
       // trace: the relabel's exit inputs (phase-8: deficit | labelled excess;
@@ -1949,9 +2067,13 @@ struct Kern {
     // slots; whole grid each) from the back.
     const int reached = sy.s_snap[C_REACHED];
     const bool bside = reached > 0 && 2ll * reached < (long long)n;
+    // tracked launches walk the B side straight from the reached-set list
+    const bool from_list = bside && s_tl_ok;
+    const int *Lc = from_list ? tl_old() : nullptr;  // (flipped: the final relabel's)
     long long c = 0;
-    for (int u = gtid; u < n; u += gthreads) {
-      if ((ldcg(a.h + u) != n) != bside) continue;
+    for (int j = gtid; j < (from_list ? reached : n); j += gthreads) {
+      const int u = from_list ? ldcg(Lc + j) : j;
+      if (!from_list && (ldcg(a.h + u) != n) != bside) continue;
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       if (hi - lo > 64) {
         if (hi - lo > kBin2Max) a.heavy[n - 1 - atomicAdd(a.ctrl->live + C_HUGE, 1)] = u;
@@ -2020,8 +2142,12 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
     sy.trace_cap = a.trace_cap;
     sy.trace_n = 0;
     s_sink = 0;
+    s_tl_cur = vc->tl_cur & 1;
+    s_tl_ok = a.sparse == 1;
+    s_tl_trk = 0;
   }
-  if ((threadIdx.x & 31) == 0) wq[threadIdx.x >> 5].cnt[0] = wq[threadIdx.x >> 5].cnt[1] = 0;
+  if ((threadIdx.x & 31) == 0)
+    wq[threadIdx.x >> 5].cnt[0] = wq[threadIdx.x >> 5].cnt[1] = wq[threadIdx.x >> 5].cnt[2] = 0;
   sy.s_snap = s_snap;
   sy.s_abort = &s_abort;
   __syncthreads();
@@ -2045,7 +2171,7 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
         // dynamic 25 -> 16.5 ms/batch) in solve rounds only: the bit-exact
         // global relabel entry point, WHAT_BFS, never takes it
         const bool early = a.what == WHAT_SOLVE && !a.topology && !PP && (a.early || (a.flags & 4) != 0);
-        L = k.bfs(stamp + 1, bstamp, a.bfs_local, early, early && !first_bfs);
+        L = k.bfs(stamp + 1, bstamp, a.bfs_local, early, early && !first_bfs, first_bfs && a.bk > 0);
         first_bfs = false;
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
@@ -2292,6 +2418,27 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
     a.async = 0;
     a.forbidden = -1;
   }
+  // reached-set tracking (WHAT_SOLVE, ordinary rounds): the lists are
+  // allocated by the first tracked launch; sparse = 1 when the list is valid
+  // right now, 2 when only this launch's own relabels will make it so
+  a.track = cfg.track && cfg.what == WHAT_SOLVE && !cfg.pushpull && !cfg.topology;
+  if (a.track && st.tl[0] == nullptr) {
+    if (cudaMalloc(&st.tl[0], sizeof(int) * (size_t)T.n) != cudaSuccess ||
+        cudaMalloc(&st.tl[1], sizeof(int) * (size_t)T.n) != cudaSuccess) {
+      cudaGetLastError();
+      if (st.tl[0]) cudaFree(st.tl[0]);
+      st.tl[0] = st.tl[1] = nullptr;
+      a.track = 0;  // (no room: the relabels seed in full)
+    }
+  }
+  a.tl[0] = st.tl[0];
+  a.tl[1] = st.tl[1];
+  a.sparse = a.track && cfg.sparse ? (st.tl_ok ? 1 : 2) : 0;
+  if (!a.track && st.tl_ok) a.sparse = 1;  // (an untracked launch may still use the list: finalize)
+  a.buv = W.d_uv;
+  a.bk = cfg.dyn_bases && cfg.gate ? cfg.batch_k : 0;
+  // valid again only when solve_status reads back a clean tracked finish
+  st.tl_ok = false;
 
   ctrl_begin_kernel<<<1, 1, 0, T.stream>>>(st.ctrl, cfg.timeout_s, cfg.ceiling,
                                           cfg.reset_counters ? 1 : 0);

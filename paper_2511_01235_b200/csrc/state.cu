@@ -81,6 +81,7 @@ cudaError_t launch_init_state(const GraphObj &g, StateObj &st) {
   if (e) return e;
   if ((e = cudaMemsetAsync(st.ex, 0, sizeof(long long) * (size_t)T.n, T.stream))) return e;
   e = cudaMemsetAsync(st.h, 0, sizeof(int) * (size_t)T.n, T.stream);
+  st.tl_ok = false;
   st.excess_consistent = true;
   st.terminated_known = false;
   return e;

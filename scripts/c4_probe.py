@@ -69,10 +69,12 @@ def main():
         g, st = g0.copy(), st0.copy()
         rows = []
         for i, (bu, bv, bc) in enumerate(chain):
-            rr = mfx.solve_dynamic(st, g, mfx.UpdateBatch(bu, bv, bc))
+            solve = mfx.solve_dynamic_pushpull if env.get("PP") == "1" else mfx.solve_dynamic
+            rr = solve(st, g, mfx.UpdateBatch(bu, bv, bc))
             d = rr.device
             rows.append(d["ms_total"])
-            if args.quiet:
+            slow = os.environ.get("MFX_TRACE_CAP") and d["ms_total"] > args.trace_ms
+            if args.quiet and not slow:
                 st = rr.state
                 continue
             print(json.dumps({"batch": i, "ms": round(d["ms_total"], 3), "flow": rr.flow_value,
@@ -82,7 +84,7 @@ def main():
                               "push_ms": round(d["ns_push"] / 1e6, 3),
                               "repair_ms": round(d["ns_repair"] / 1e6, 3),
                               "pushes": rr.pushes, "relabels": rr.relabels}), flush=True)
-            if os.environ.get("MFX_TRACE_CAP") and d["ms_total"] > args.trace_ms:
+            if slow:
                 import trace as T
                 ph, items, dt = T.fetch(rr.state, g)
                 raw = (items.astype(np.uint64) << np.uint64(32)) | dt.astype(np.uint64)
