@@ -588,6 +588,26 @@ struct Kern {
     stage(0, glob, item, a.ctrl->live + C_FNEXT, Fn_[0], 0, a.n);
   }
 
+  // Report the relaxations of a row chunk: bit k of `low` set = vv[k] was
+  // lowered to nl (bit k of `fst`: first visit).  Each lane walks its set
+  // bits in order; the warp loops as often as its busiest lane has bits, so
+  // discovered() (ballots, ring reservation, staging) is inlined once and
+  // runs once per actual discovery instead of once per slot of the row (a
+  // thread-per-row pass unrolled over 8 slots otherwise inlines it 8 times:
+  // ~5 K instructions of the kernel's hot code).  Warp-synchronous.
+  template <int K>
+  __device__ __forceinline__ void report(unsigned low, unsigned fst, const int (&vv)[K], int nl) {
+    while (__any_sync(FULL, low != 0)) {
+      const int k = low ? __ffs(low) - 1 : 0;
+      int v = vv[0];
+#pragma unroll
+      for (int q = 1; q < K; ++q) v = k == q ? vv[q] : v;  // (register select, no local array)
+      const bool l = low != 0;
+      discovered(l, l && (fst >> k & 1), v, nl);
+      low &= low - 1;
+    }
+  }
+
   // Discovery through slot i (valid lanes) of a frontier vertex at label
   // nl - 1: the reverse residual cf[rev i] is read as pc[i] - cf[i] from the
   // same row.
@@ -632,7 +652,15 @@ struct Kern {
       low[k] = rr[k] > 0 && (nocheck || hv[k] > nl) && relax(vv[k], nl, fst[k]);
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k) discovered(low[k], fst[k], vv[k], nl);
+    {
+      unsigned lm = 0, fm = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        lm |= (unsigned)low[k] << k;
+        fm |= (unsigned)fst[k] << k;
+      }
+      report<K>(lm, fm, vv, nl);
+    }
   }
 
   // Thread per item: the row (<= kBin0Max slots) is expanded with every load
@@ -720,7 +748,15 @@ struct Kern {
       }
     }
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) discovered(low[k], fst[k], vv[k], nl);
+    {
+      unsigned lm = 0, fm = 0;
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) {
+        lm |= (unsigned)low[k] << k;
+        fm |= (unsigned)fst[k] << k;
+      }
+      report<kBin0Max>(lm, fm, vv, nl);
+    }
   }
 
   // Warp per row over the CTA's heavy-row list (whole CTA calls).
