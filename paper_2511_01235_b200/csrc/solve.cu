@@ -1381,15 +1381,26 @@ struct Kern {
     // claimed it (a head that already held excess, or got none net, is then
     // a no-op item; one that was claimed before is listed already); in the
     // asynchronous phase when it was not holding excess before the push.
+    if (Async) {
 #pragma unroll
-    for (int k = 0; k < kBin0Max; ++k) {
-
-      if (Async) {
+      for (int k = 0; k < kBin0Max; ++k) {
         bool p = (pushed >> k & 1) && oldv[k] <= 0 && vv[k] != a.s && vv[k] != a.t;
         activate(p, vv[k], bb[k], stamp, nbase);
-      } else {
-        append_binned(1, (pushed >> k & 1) && clm[k] < stamp, vv[k], bb[k], rctr, a.R, nbase,
-                      a.rcap);
+      }
+    } else {  // (compacted like report(): one inlined append, run per listed head)
+      unsigned lst = 0;
+#pragma unroll
+      for (int k = 0; k < kBin0Max; ++k) lst |= (unsigned)((pushed >> k & 1) && clm[k] < stamp) << k;
+      while (__any_sync(FULL, lst != 0)) {
+        const int k = lst ? __ffs(lst) - 1 : 0;
+        int v = vv[0], b = bb[0];
+#pragma unroll
+        for (int q = 1; q < kBin0Max; ++q) {
+          v = k == q ? vv[q] : v;
+          b = k == q ? bb[q] : b;
+        }
+        append_binned(1, lst != 0, v, b, rctr, a.R, nbase, a.rcap);
+        lst &= lst - 1;
       }
     }
     if (Async) {
