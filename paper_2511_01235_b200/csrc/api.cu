@@ -788,6 +788,7 @@ static int resolve_config(const Topology &T, const mfx_params *p, SolveConfig &c
   if (const char *ee = getenv("MFX_EARLY")) cfg.early = atoi(ee);
   if (const char *tr = getenv("MFX_TRACK")) cfg.track = atoi(tr);
   if (const char *sp = getenv("MFX_SPARSE")) cfg.sparse = atoi(sp);
+  if (const char *rp = getenv("MFX_RAMP")) cfg.ramp = atoi(rp) > 0 ? atoi(rp) : 4;
   if (p->wave_mult > 0 || p->wave_add > 0) {
     cfg.wave_mult = p->wave_mult;
     cfg.wave_add = p->wave_add;

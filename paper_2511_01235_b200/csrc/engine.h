@@ -129,6 +129,7 @@ struct SolveConfig {
   int strand = 0;  // push phase ends once the sink is cut off and every deficit is filled
   int early = 1;   // solve relabels stop once every excess holder is labelled (0 off)
   int track = 1;   // WHAT_SOLVE launches keep the reached-set list (StateObj::tl; 0 off)
+  int ramp = 4;    // first ring epoch's labels when the demand-covered exit is in reach
   int sparse = 1;  // relabels reset / seed from that list when it is small (0 off)
   long long batch_k = 0;  // dynamic solves: updates of the batch (their endpoints seed too)
 };

@@ -81,6 +81,7 @@ struct SolveArgs {
   int early;         // solve relabels stop once every excess holder is labelled
   int ring_sleep;    // ns an idle warp sleeps between polls of the BFS ring
   int track;         // keep the reached-set list: every relabel appends what it reaches
+  int ramp;          // first ring epoch's labels when the demand-covered exit is in reach
   int sparse;        // the first relabel may seed from the list (StateObj::tl_ok)
   int *tl[2];        // the two reached-set lists (n each)
   const int *buv;    // the batch's (u, v) endpoints (2 * bk), first relabel after a batch
@@ -1094,7 +1095,7 @@ struct Kern {
     // fill) the ring epochs start short and double, so the barrier that can
     // stop the relabel comes a few labels after the holders near the
     // deficits are found, not after a full 128-label epoch (uniform: snap)
-    int ramp = early && a.strand && sy.s_snap[C_TALIVE] == 0 && sy.s_snap[C_DBASES] > 0 ? 8 : 0;
+    int ramp = early && a.strand && sy.s_snap[C_TALIVE] == 0 && sy.s_snap[C_DBASES] > 0 ? a.ramp : 0;
     for (;;) {
       int cnt[NBIN];
       int tot = 0;
@@ -2432,6 +2433,7 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   a.strand = cfg.strand > 0;
   a.early = cfg.early != 0;
   a.ring_sleep = cfg.ring_sleep;
+  a.ramp = cfg.ramp;
   a.coop_kc = cfg.coop_kc > 0 ? (cfg.coop_kc < cfg.kc ? cfg.coop_kc : cfg.kc) : cfg.kc;
   a.tail_cap = cfg.tail_cap;
   a.bmark = W.bmark;

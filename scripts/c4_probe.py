@@ -78,6 +78,7 @@ def main():
                 st = rr.state
                 continue
             print(json.dumps({"batch": i, "ms": round(d["ms_total"], 3), "flow": rr.flow_value,
+                              "update_ms": round(d["ms_update"], 3), "solve_ms": round(d["ms_solve"], 3),
                               "rounds": rr.rounds, "levels": d["bfs_levels"],
                               "epochs": d["bfs_epochs"], "waves": d["waves"],
                               "bfs_ms": round(d["ns_bfs"] / 1e6, 3),
