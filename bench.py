@@ -418,6 +418,9 @@ def bench_ours(args, cfg, rank, world, dev, pg, backend):
     ns = ctypes.c_double()
     _lib.check(L.mfx_bench_barrier(g.handle, st.handle, 2000, 0, ctypes.byref(ns)))
     out["barrier_ns"] = ns.value
+    cns = ctypes.c_double()  # dependent-load latency: the latency roofline's unit
+    _lib.check(L.mfx_bench_chase(g.handle, 1 << 30, 20000, ctypes.byref(cns)))
+    out["chase_ns"] = cns.value
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_sample(g, st, s, t, n, k, args)
@@ -460,6 +463,14 @@ def emit_ours(args, out, world):
     traffic, tsrc = load_traffic(out["cfg"])
     barriers = float(np.mean(out["epochs"] + out["waves"]))
     bar_us = out.get("barrier_ns", 0.0) / 1e3
+    # latency roofline: the critical path of a launch is a chain of dependent
+    # global accesses -- ~4 per BFS label (row offsets/height -> row -> head
+    # heights -> relaxing atomic) and ~5 per push wave (+ the CTA-0 list
+    # hand-off) -- at the measured cache-missing load latency, plus the grid
+    # barriers at their measured cost
+    chain = float(np.mean(4 * out["levels"] + 5 * out["waves"]))
+    load_us = out.get("chase_ns", 0.0) / 1e3
+    lat_floor_ms = (chain * load_us + barriers * bar_us) / 1e3
     value = out["elapsed_ms"] / K
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "ms/batch", "n_gpus": world,
@@ -494,8 +505,15 @@ def emit_ours(args, out, world):
             "latency": {"grid_barriers_per_launch": round(barriers, 1),
                         "barrier_us": round(bar_us, 2),
                         "barrier_floor_ms": round(barriers * bar_us / 1e3, 4),
-                        "frac": round(barriers * bar_us / 1e3 / kernel_ms, 4) if kernel_ms else None,
-                        "bfs_levels_per_launch": round(float(np.mean(out["levels"])), 1)},
+                        "bfs_levels_per_launch": round(float(np.mean(out["levels"])), 1),
+                        "push_waves_per_launch": round(float(np.mean(out["waves"])), 1),
+                        "dependent_loads_per_launch": round(chain, 1),
+                        "load_latency_us": round(load_us, 3),
+                        "floor_ms": round(lat_floor_ms, 4),
+                        "frac": round(lat_floor_ms / kernel_ms, 4) if kernel_ms else None,
+                        "model": "critical path = (4 x BFS labels + 5 x push waves) dependent "
+                                 "loads at the measured pointer-chase latency + grid barriers "
+                                 "at their measured cost; frac = that floor / kernel time"},
         },
         "clocks": out["clocks"],
         "kernel_src_hash": kernel_source_hash(),

@@ -209,6 +209,9 @@ int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_p
 /* Diagnostics: the reached-set list the last tracked relabel kept (sparse
  * relabels seed from it); *count = -1 when the state holds no valid list. */
 int mfx_reached_list(const mfx_state *st, int32_t *out, int64_t cap, int64_t *count);
+/* Dependent global-load latency (ns per load, cache-missing pointer chase over
+ * `bytes` of device memory): the unit of the bench's latency roofline. */
+int mfx_bench_chase(const mfx_graph *g, int64_t bytes, int steps, double *ns_per_load);
 int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int64_t cap,
                     int64_t *count);
 /* Host<->device bytes one mfx_solve_dynamic call of k updates moves. */

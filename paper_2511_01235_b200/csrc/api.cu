@@ -1321,6 +1321,45 @@ int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_p
   return MFX_OK;
 }
 
+// Dependent-load latency (the latency roofline's unit): one thread chases
+// indices through a `words`-entry permutation that jumps ~ a page per step
+// (odd multiplier mod 2^k), so every load misses the caches.
+__global__ void chase_init_kernel(unsigned *p, unsigned long long words) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < words;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    p[i] = (unsigned)((i * 40503ull + 12345ull) & (words - 1));
+}
+__global__ void chase_kernel(const unsigned *p, int steps, unsigned *sink, unsigned long long *ns) {
+  unsigned j = 0;
+  const unsigned long long t0 = globaltimer();
+  for (int s = 0; s < steps; ++s) j = __ldcg(p + j);
+  const unsigned long long t1 = globaltimer();
+  *sink = j;
+  *ns = t1 - t0;
+}
+
+int mfx_bench_chase(const mfx_graph *g, int64_t bytes, int steps, double *ns_per_load) {
+  Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
+  CK(cudaSetDevice(T.device));
+  unsigned long long words = 1;
+  while (words * 2 * sizeof(unsigned) <= (unsigned long long)bytes) words *= 2;
+  unsigned *p = nullptr;
+  unsigned long long *d = nullptr;
+  CK(cudaMalloc(&p, words * sizeof(unsigned) + 64));
+  d = (unsigned long long *)(p + words);
+  chase_init_kernel<<<T.num_sms * 8, 256, 0, T.stream>>>(p, words);
+  chase_kernel<<<1, 1, 0, T.stream>>>(p, 64, (unsigned *)(d + 1), d);  // (warm the TLB path)
+  chase_kernel<<<1, 1, 0, T.stream>>>(p, steps, (unsigned *)(d + 1), d);
+  unsigned long long ns = 0;
+  cudaError_t e = cudaMemcpyAsync(&ns, d, sizeof(ns), cudaMemcpyDeviceToHost, T.stream);
+  if (!e) e = cudaStreamSynchronize(T.stream);
+  cudaFree(p);
+  CK(e);
+  *ns_per_load = (double)ns / (steps > 0 ? steps : 1);
+  return MFX_OK;
+}
+
 int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int64_t cap,
                     int64_t *count) {
   Topology &T = *g->g.topo;
