@@ -1107,6 +1107,7 @@ static int pushpull_common(mfx_graph *g, mfx_state *st, int64_t k, const int64_t
     cfg.reset_counters = false;
     cfg.dyn_bases = 1;
     cfg.forbidden = st->s.s;
+    if (cfg.strand < 0) cfg.strand = 1;  // (the dynamic solve's stop / demand-covered rules)
     CK(launch_solve(g->g, st->s, cfg, &launches));
   }
   CK(cudaEventRecord(T.ev[2], T.stream));

@@ -1011,8 +1011,11 @@ struct Kern {
         const bool valid = v < n;
         bool base;
         if (PP) {  // push side: sink + deficits; pull side: source + overflow
-          base = valid && (region(v) == 0 ? (v == a.t || (v != a.s && ev[r] < 0))
-                                          : (v == a.s || (v != a.t && ev[r] > 0)));
+          const int rg = valid ? region(v) : 0;
+          base = valid && (rg == 0 ? (v == a.t || (v != a.s && ev[r] < 0))
+                                   : (v == a.s || (v != a.t && ev[r] > 0)));
+          // the side's actives (push side: overflow, pull side: deficits)
+          holders += valid && v != a.s && v != a.t && (rg == 0 ? ev[r] > 0 : ev[r] < 0);
         } else {
           base = valid && (v == a.t || (a.dyn_bases && v != a.s && ev[r] < 0));
           holders += valid && v != a.s && v != a.t && ev[r] > 0 && (cand >> r & 1);
@@ -1110,7 +1113,9 @@ struct Kern {
       // keep h = n, which no push can cross, and the solve's last global
       // relabel (no holder left) always runs to the end, so the certificate
       // still comes from exact distances.
-      if (early && sy.s_snap[C_EHOLD] > 0 && sy.s_snap[C_ACTIVE] >= sy.s_snap[C_EHOLD]) {
+      // (push-pull relabels never certify -- the ordinary final pass does --
+      // so with no active vertex on either side they stop at once)
+      if (early && (sy.s_snap[C_EHOLD] > 0 || PP) && sy.s_snap[C_ACTIVE] >= sy.s_snap[C_EHOLD]) {
         exit_list(E, cnt[0]);
         break;
       }
@@ -2218,8 +2223,12 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
         // early exit (stop once every excess holder is labelled; C4
         // dynamic 25 -> 16.5 ms/batch) in solve rounds only: the bit-exact
         // global relabel entry point, WHAT_BFS, never takes it
-        const bool early = a.what == WHAT_SOLVE && !a.topology && !PP && (a.early || (a.flags & 4) != 0);
-        L = k.bfs(stamp + 1, bstamp, a.bfs_local, early, early && !first_bfs, first_bfs && a.bk > 0);
+        // (push-pull: the region relabels stop once every active of both
+        // sides is labelled -- C4's pull side is the whole 24 M-vertex A
+        // side, its few deficits sit next to the excess that feeds them)
+        const bool early = a.what == WHAT_SOLVE && !a.topology && (a.early || (a.flags & 4) != 0);
+        L = k.bfs(stamp + 1, bstamp, a.bfs_local, early, early && !first_bfs && !PP,
+                  first_bfs && a.bk > 0);
         first_bfs = false;
         int act = s_snap[C_ACTIVE];
         if (k.gtid == 0) a.ctrl->active = act;
