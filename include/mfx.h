@@ -164,7 +164,9 @@ int mfx_solve_static(const mfx_graph *g, mfx_state *st, const mfx_params *p, mfx
 int mfx_solve_dynamic(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *us,
                       const int64_t *vs, const int64_t *new_caps, const mfx_params *p,
                       mfx_result *r);
-/* Same with the batch already in device memory (d_* device pointers). */
+/* Same with the batch already in device memory (d_* device pointers).  The
+ * engine reads them on its own (non-blocking) stream: the caller must have
+ * finished writing them (e.g. synchronized its producer stream) first. */
 int mfx_solve_dynamic_device(mfx_graph *g, mfx_state *st, int64_t k, const int64_t *d_us,
                              const int64_t *d_vs, const int64_t *d_caps, const mfx_params *p,
                              mfx_result *r);
