@@ -260,8 +260,13 @@ int mfx_part_info(const mfx_part *p, int64_t *info);
 int mfx_part_export(const mfx_part *p, void *blob, int64_t cap, int64_t *len);
 int mfx_part_attach(mfx_part *p, int peer, const void *blob, int64_t len);
 int mfx_part_attach_local(mfx_part *p, const mfx_part *q);
-/* One phase (args, out: 8 x int64); synchronous at return. */
+/* One phase (args, out: 8 x int64); synchronous at return.  phase |
+ * MFX_PH_ASYNC: only enqueue it on the part's stream (no outputs; phases
+ * whose results the host reads, and LINK / LINK_PC, are refused), so the
+ * parts one process hosts run the phase concurrently; mfx_part_sync waits. */
+#define MFX_PH_ASYNC 0x100
 int mfx_part_phase(mfx_part *p, int phase, const int64_t *args, int64_t *out);
+int mfx_part_sync(mfx_part *p);
 /* This part's share of an update batch; gidx = index in the whole batch,
  * slot_base = global index of the part's first slot (error reports). */
 int mfx_part_stage_batch(mfx_part *p, int64_t k, const int64_t *us, const int64_t *vs,

@@ -132,6 +132,7 @@ SIGNATURES = {
     "mfx_part_attach": (ctypes.c_int, [vp, ctypes.c_int, vp, i64]),
     "mfx_part_attach_local": (ctypes.c_int, [vp, vp]),
     "mfx_part_phase": (ctypes.c_int, [vp, ctypes.c_int, p_i64, p_i64]),
+    "mfx_part_sync": (ctypes.c_int, [vp]),
     "mfx_part_stage_batch": (ctypes.c_int, [vp, i64, p_i64, p_i64, p_i64, p_i64, i64]),
     "mfx_part_download": (ctypes.c_int, [vp, p_i64, p_i64, p_i64, p_i64, p_i64, p_u8, p_i64,
                                          p_i64]),

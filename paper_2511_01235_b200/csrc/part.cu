@@ -1415,7 +1415,20 @@ int mfx_part_attach_local(mfx_part *p, const mfx_part *q) {
 }
 
 // Phases.  args/out are 8 x int64; see include/mfx.h for the meaning.
+int mfx_part_sync(mfx_part *pp) {
+  PartObj &o = pp->o;
+  PCK(cudaSetDevice(o.device));
+  PCK(cudaStreamSynchronize(o.stream));
+  PCK(cudaGetLastError());
+  return MFX_OK;
+}
+
 int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
+  const bool async = (phase & MFX_PH_ASYNC) != 0;
+  phase &= ~MFX_PH_ASYNC;
+  if (async && (phase == MFX_PH_LINK || phase == MFX_PH_LINK_PC || phase == MFX_PH_SWAP ||
+                phase == MFX_PH_FINAL || phase == MFX_PH_ACTIVE || phase == MFX_PH_BATCH_RESOLVE))
+    return part_fail(MFX_VALUE_ERROR, "partition phase %d returns results: no async form", phase);
   PartObj &o = pp->o;
   PCK(cudaSetDevice(o.device));
   cudaStream_t st = o.stream;
@@ -1573,6 +1586,7 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
       return part_fail(MFX_VALUE_ERROR, "unknown partition phase %d", phase);
   }
   PCK(cudaGetLastError());
+  if (async) return MFX_OK;  // (enqueued; mfx_part_sync waits, nothing is read back)
   PCK(cudaStreamSynchronize(st));
   if (phase == MFX_PH_LINK || phase == MFX_PH_LINK_PC) {
     int bad = 0;

@@ -30,6 +30,9 @@ from .solver import SolverError, SolverParams, operation_ceiling
 PH_LINK, PH_LINK_PC, PH_INIT, PH_SATURATE, PH_BFS_INIT, PH_BFS_EXPAND, PH_SWAP, PH_PUSH, \
     PH_REPAIR, PH_FINAL, PH_ACTIVE, PH_BATCH_RESOLVE, PH_BATCH_APPLY, PH_BATCH_FIX = range(14)
 BLOB_BYTES = 15 * 64  # B_NBUF CUDA IPC handles (csrc/part.cu)
+PH_ASYNC = 0x100  # MFX_PH_ASYNC (include/mfx.h): enqueue only
+# phases the host reads nothing back from (their out[] is unused by the round loop)
+ASYNC_PHASES = (PH_BFS_INIT, PH_BFS_EXPAND, PH_PUSH, PH_REPAIR)
 NONE = np.iinfo(np.int64).max
 
 
@@ -241,6 +244,7 @@ class PartitionedGraph:
         # global relabel: levels whose frontier exceeds 1/div of the unreached
         # vertices run bottom-up (0 = always top-down)
         self.bottom_up_div = int(os.environ.get("MFX_PART_BOTTOM_UP", "16"))
+        self.async_phases = os.environ.get("MFX_PART_ASYNC", "1") != "0"
 
     # -- plumbing ------------------------------------------------------------
     def _connect(self):
@@ -272,7 +276,23 @@ class PartitionedGraph:
         return out
 
     def _phase_all(self, phase, args=None):
-        """Run one phase on every local part; args: dict rank -> tuple."""
+        """Run one phase on every local part; args: dict rank -> tuple.
+
+        Phases whose results the host does not read run concurrently when one
+        process hosts several parts: every part's phase is enqueued on its own
+        stream, then all are awaited (the multi-GPU schedule on one process;
+        every cross-part update is an atomic, so any interleaving is valid).
+        $MFX_PART_ASYNC=0 runs them part after part."""
+        if (phase in ASYNC_PHASES and len(self.handles) > 1 and self.async_phases):
+            outs = {}
+            for r in self.handles:
+                outs[r] = self._phase(r, phase | PH_ASYNC, (args or {}).get(r, ()))
+            t0 = time.perf_counter()
+            for r in self.handles:
+                L.check(self.lib.mfx_part_sync(self.handles[r]))
+            self.phase_s[phase | PH_ASYNC] = (self.phase_s.get(phase | PH_ASYNC, 0.0)
+                                              + time.perf_counter() - t0)
+            return outs
         return {r: self._phase(r, phase, (args or {}).get(r, ())) for r in self.handles}
 
     def _sum(self, outs, idx) -> np.ndarray:
