@@ -52,6 +52,9 @@ __shared__ int s_tl_cur;
 // so it is expected to reach few vertices too); the last relabel's list is
 // valid (launch: the host's StateObj::tl_ok; then: that relabel tracked)
 __shared__ int s_tl_trk, s_tl_ok;
+// this round's repair stamp (Workspace::bmark): a vertex listed by several
+// waves of the round is repaired once
+__shared__ unsigned s_rep_stamp;
 
 template <typename CapT>
 struct SolveArgs {
@@ -1624,10 +1627,16 @@ struct Kern {
     }
   }
 
+  // Repair scope: every vertex the round's waves listed (solver.py:233), each
+  // once -- the wave lists repeat a vertex every time it is re-activated, and
+  // on R-MAT the hub rows come back wave after wave (each a 10^5-slot scan).
   __device__ void repair(const int *end) {
+    __shared__ int s_ok;
+    const unsigned rs = s_rep_stamp;
     for (int j = gtid; j < end[0]; j += gthreads) {  // thread per row, loads batched
       int u = ldcg(a.R[0] + j);
       if (u < 0) continue;  // reserved slot never filled (queue overflow)
+      if (atomicMax((unsigned *)a.bmark + u, rs) >= rs) continue;  // (repaired this round)
       int lo = __ldg(a.off + u), d = __ldg(a.off + u + 1) - lo;
       int hu = ldcg(a.h + u);
       const int ru = region(u);
@@ -1659,6 +1668,8 @@ struct Kern {
     for (int j = gwarp; j < end[1]; j += gwarps) {
       int u = ldcg(a.R[1] + j);
       if (u < 0) continue;
+      int fresh = lane == 0 ? atomicMax((unsigned *)a.bmark + u, rs) < rs : 0;
+      if (!__shfl_sync(FULL, fresh, 0)) continue;
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int hu = ldcg(a.h + u);
       if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
@@ -1668,6 +1679,10 @@ struct Kern {
       for (int j = blockIdx.x; j < end[b]; j += gridDim.x) {
         int u = ldcg(a.R[b] + j);
         if (u < 0) continue;  // (uniform across the CTA: same slot)
+        __syncthreads();
+        if (threadIdx.x == 0) s_ok = atomicMax((unsigned *)a.bmark + u, rs) < rs;
+        __syncthreads();
+        if (!s_ok) continue;
         int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
         int hu = ldcg(a.h + u);
         if (threadIdx.x == 0)
@@ -2244,6 +2259,9 @@ __global__ void __launch_bounds__(kBlock, MFX_MIN_BLOCKS)
           grid_sync(a.ctrl, sy, 0, 0xFu << C_RNEXT, 0, PH_PUSH);
         }
       }
+      ++bstamp;  // (every thread: this round's repair stamp)
+      if (threadIdx.x == 0) s_rep_stamp = bstamp;
+      __syncthreads();
       if (a.async) k.push_round_async(stamp, scr);
       else {
         int budget = a.max_waves > 0 ? a.max_waves : a.wave_mult * L / 4 + a.wave_add;
