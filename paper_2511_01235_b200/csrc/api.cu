@@ -191,9 +191,11 @@ cudaError_t launch_solve(const GraphObj &g, StateObj &st, const SolveConfig &cfg
     return v512::launch_solve(g, st, c, launches);
   }
   // short-row graphs: a push phase is cut off once it has run 1.25x the last
-  // global relabel's time (C2: 9.0 -> 8.0 ms/batch, static 30 -> 26.5 ms)
+  // global relabel's time (C2: 9.0 -> 8.0 ms/batch, static 30 -> 26.5 ms);
+  // 0.75x in dynamic solves, whose late rounds bounce a few units of excess
+  // (C2 7.2 -> 6.8 ms/batch; static keeps 1.25x: 0.75x costs it 3 %)
   SolveConfig c = cfg;
-  if (c.wave_time < 0) c.wave_time = 10;
+  if (c.wave_time < 0) c.wave_time = c.dyn_bases && c.what == WHAT_SOLVE && c.strand > 0 ? 6 : 10;
   if (c.bfs_local < 0) c.bfs_local = 128;
   return v256::launch_solve(g, st, c, launches);
 }
