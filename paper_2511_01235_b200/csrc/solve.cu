@@ -55,6 +55,9 @@ __shared__ int s_tl_trk, s_tl_ok;
 // this round's repair stamp (Workspace::bmark): a vertex listed by several
 // waves of the round is repaired once
 __shared__ unsigned s_rep_stamp;
+// deficits this CTA filled during its current run of tail waves (CTA 0 alone
+// pushes then: the stop test reads this instead of Ctrl::fills in L2)
+__shared__ unsigned s_fills;
 
 template <typename CapT>
 struct SolveArgs {
@@ -373,6 +376,11 @@ struct Kern {
   }
 
   __device__ __forceinline__ int vbin(int v) const { return __ldg(a.vbin + v); }
+  // a push took a deficient base's excess to >= 0 (stranded-excess rule)
+  __device__ __forceinline__ void fill_once() const {
+    atomicAdd(&a.ctrl->fills, 1ull);
+    atomicAdd(&s_fills, 1u);
+  }
   __device__ __forceinline__ int region(int v) const { return PP ? (int)__ldg(a.reg + v) : 0; }
 
   // ---- warp-synchronous list appends (every lane of the warp must call) ----
@@ -1290,7 +1298,7 @@ struct Kern {
       // this wave and that holds no deficit any more: filled (a later
       // refill may count it twice, which only ends the phase earlier)
       if (!PP && a.strand && !a.topology && hu == 0 && eu >= 0 && u != a.t && u != a.s)
-        atomicAdd(&a.ctrl->fills, 1ull);
+        fill_once();
     }
     const bool live = eu > 0 && hu < n;
     if (!live) d = 0;
@@ -1554,7 +1562,7 @@ struct Kern {
             atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
             old = add_excess(v, amt);
             if (!PP && a.strand && old < 0 && old + amt >= 0 && v != a.t)
-              atomicAdd(&a.ctrl->fills, 1ull);
+              fill_once();
           }
           act = old <= 0 && v != a.s && v != a.t;
           lc.pushes++;
@@ -1746,7 +1754,7 @@ struct Kern {
         atomic_add(a.ex + u, -take);
         const long long vold = add_excess(v, take);
         if (!PP && a.strand && vold < 0 && vold + take >= 0 && v != a.t)
-          atomicAdd(&a.ctrl->fills, 1ull);
+          fill_once();
         lc.pushes++;
         lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)d * Bytes<CapT>::kSlot +
                     Bytes<CapT>::kPush;
@@ -1776,7 +1784,15 @@ struct Kern {
     __shared__ int s_cnt[NBIN];
     __shared__ int s_go;
     __shared__ int s_rc[NBIN];  // this CTA alone appends: list counters in shared memory
-    if (threadIdx.x == 0) sy.t_tail = globaltimer();
+    // thread 0's stop-test inputs, read once: the push phase's deadline and
+    // the fills so far (only this CTA pushes until the tail waves end)
+    unsigned long long wdl = 0, fills0 = 0;
+    if (threadIdx.x == 0) {
+      sy.t_tail = globaltimer();
+      wdl = ((volatile Ctrl *)a.ctrl)->wave_deadline;
+      fills0 = ((volatile Ctrl *)a.ctrl)->fills;
+      s_fills = 0;
+    }
     if (threadIdx.x < NBIN) s_rc[threadIdx.x] = 0;
     rctr = s_rc;
     for (;;) {
@@ -1814,9 +1830,9 @@ struct Kern {
         const bool go = tot > 0 && tot <= a.tail_local && s_cnt[1] <= kWarps && s_cnt[2] == 0 &&
                         s_cnt[3] == 0 &&
                         (waves < max_waves || (tot <= a.tail_items && waves < a.tail_cap)) &&
-                        !(a.wave_time > 0 && globaltimer() > a.ctrl->wave_deadline) &&
+                        !(a.wave_time > 0 && wdl != 0 && globaltimer() > wdl) &&
                         !(!PP && a.strand && sy.s_snap[C_TALIVE] == 0 &&
-                          ((volatile Ctrl *)a.ctrl)->fills >= (unsigned)sy.s_snap[C_DBASES]);
+                          fills0 + s_fills >= (unsigned)sy.s_snap[C_DBASES]);
         // consumed here: the next wave appends from zero; else the pending
         // wave's counts go to the live counters the grid barrier snapshots
         for (int b = 0; b < NBIN; ++b) {
