@@ -243,7 +243,8 @@ enum {
     MFX_PH_ACTIVE = 10,       /* -> active vertices (state.py:62-67)           */
     MFX_PH_BATCH_RESOLVE = 11,/* -> error block (dynamic.py:63-88)             */
     MFX_PH_BATCH_APPLY = 12,  /* a0 = apply (dynamic.py:103-104)               */
-    MFX_PH_BATCH_FIX = 13     /* pair sums + negative repair (dynamic.py:105-109) */
+    MFX_PH_BATCH_FIX = 13,    /* pair sums + negative repair (dynamic.py:105-109) */
+    MFX_PH_TOPO_SEED = 14     /* topology mode: round list = every non-terminal (solver.py:170-174) */
 };
 /* Edge arrays in device memory of `device` (any edges; those touching the
  * owned range are selected on the device). */

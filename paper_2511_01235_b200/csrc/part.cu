@@ -876,6 +876,20 @@ __global__ void part_heavy_list_kernel(const int *off, int nl, int *list, int *c
   }
 }
 
+// topology mode (solver.py:167-175): the round's worklist is every owned
+// vertex but s and t, binned like the relabel's appends
+__global__ void part_topo_seed_kernel(PeerTab T, int me, int nl, int s, int t, int rcap) {
+  int *ctr = T.ctr[me];
+  PGS_LOOP(v, nl) {
+    const int g = T.lo[me] + (int)v;
+    if (g == s || g == t) continue;
+    const int b = heavy_of(T, me, (int)v);
+    const int q = atomicAdd(ctr + PC_RT0 + b, 1);
+    if (q < rcap) T.R[me][b][q] = (int)v;
+    else atomicExch(ctr + PC_OVF, 1);
+  }
+}
+
 __global__ void part_active_kernel(PeerTab T, int me, int nl, int s, int t,
                                    unsigned long long *stat) {
   unsigned long long a = 0;
@@ -1531,6 +1545,13 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
       PCK(cudaMemsetAsync(o.stat + PS_FLOW, 0, 2 * sizeof(unsigned long long), st));
       part_final_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.S, (int)args[0], o.bases, o.orig, o.src,
                                                   o.stat);
+      count_launch();
+      break;
+    }
+    case MFX_PH_TOPO_SEED: {
+      PCK(cudaMemsetAsync(ctr + PC_RT0, 0, 2 * sizeof(int), st));
+      part_topo_seed_kernel<<<pgrid(o.nl, o.num_sms), kPartBlock, 0, st>>>(T, me, o.nl, o.s, o.t,
+                                                                           o.rcap);
       count_launch();
       break;
     }

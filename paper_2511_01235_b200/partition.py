@@ -28,7 +28,8 @@ from .dynamic import BatchError, UpdateBatch
 from .solver import SolverError, SolverParams, operation_ceiling
 
 PH_LINK, PH_LINK_PC, PH_INIT, PH_SATURATE, PH_BFS_INIT, PH_BFS_EXPAND, PH_SWAP, PH_PUSH, \
-    PH_REPAIR, PH_FINAL, PH_ACTIVE, PH_BATCH_RESOLVE, PH_BATCH_APPLY, PH_BATCH_FIX = range(14)
+    PH_REPAIR, PH_FINAL, PH_ACTIVE, PH_BATCH_RESOLVE, PH_BATCH_APPLY, PH_BATCH_FIX, \
+    PH_TOPO_SEED = range(15)
 BLOB_BYTES = 15 * 64  # B_NBUF CUDA IPC handles (csrc/part.cu)
 PH_ASYNC = 0x100  # MFX_PH_ASYNC (include/mfx.h): enqueue only
 # phases the host reads nothing back from (their out[] is unused by the round loop)
@@ -328,12 +329,19 @@ class PartitionedGraph:
         timeout = params.timeout_s if params.timeout_s > 0 else 600.0
         st = dict(rounds=0, pushes=0, relabels=0, repairs=0, levels=0, waves=0)
         base = self._sum({r: self._stats(r) for r in self.handles}, (0, 1, 2))
+        rnd = 0
         while True:
             outs, depth = self._global_relabel(dyn)
             st["levels"] += depth
+            if params.instrument is not None:  # (solver.py:219-241: the state is this object)
+                params.instrument(self, self, rnd, "bfs")
             active = int(self._sum(outs, (4,))[0])
             if active == 0:
                 break
+            if params.mode == "topology":  # every non-terminal works this round
+                self._phase_all(PH_TOPO_SEED)
+                self.group.barrier()
+                outs = self._phase_all(PH_SWAP)
             budget = params.max_waves if params.max_waves > 0 else 2 * depth // 4 + 4
             begin = {r: (0, 0) for r in outs}
             end = {r: (int(o[2]), int(o[3])) for r, o in outs.items()}
@@ -358,6 +366,9 @@ class PartitionedGraph:
             self.group.barrier()
             st["rounds"] += 1
             st["waves"] += waves
+            if params.instrument is not None:
+                params.instrument(self, self, rnd, "repair")
+            rnd += 1
             if time.perf_counter() - t0 > timeout:
                 raise L.DeviceTimeout(f"partitioned solve exceeded {timeout:.0f} s after "
                                       f"{st['rounds']} rounds")
@@ -389,8 +400,6 @@ class PartitionedGraph:
         """solve_static (solver.py:253-283) over the partition set."""
         params = params or SolverParams()
         params.validate()
-        if params.mode != "data":
-            raise ValueError("the partitioned engine runs the data-driven mode only")
         self.group.barrier()
         t0 = time.perf_counter()
         self._phase_all(PH_INIT)

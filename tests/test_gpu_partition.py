@@ -227,3 +227,34 @@ def test_rmat_large_partition_million_update_batches(part, scale, P):
     """R-MAT 24 (521 M slots) and full C5 (R-MAT 26, 2.1 B slots) on one
     GPU, 10^6-update batches, dynamic == static re-solve."""
     _rmat_chain(part, scale, P, 1_000_000, 2)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("name", ["rand3", "grid64", "rmat12", "road48"])
+def test_topology_mode_and_instrument(mf, part, name, P):
+    """mode="topology" (solver.py:167-175: every non-terminal works each
+    round) gives the reference's flows on the partition too, and the
+    instrument hook sees every round's relabel and repair
+    (solver.py:219-241; the partitioned state is the PartitionedGraph)."""
+    rec = G.rec[name]
+    n, us, vs, caps, s, t = instance(name)
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    pg = part.PartitionedGraph(n, us, vs, caps, s, t, part.LocalGroup(P))
+    seen = []
+
+    def hook(st, gg, rnd, label):
+        assert st is pg and gg is pg
+        seen.append((rnd, label))
+
+    p = mf.SolverParams(mode="topology", instrument=hook)
+    res = pg.solve_static(p)
+    assert res.flow_value == rec["static_flow"] == res.cut_capacity
+    assert seen[0] == (0, "bfs") and seen[-1] == (res.rounds, "bfs")
+    assert [x for x in seen if x[1] == "repair"] == [(r, "repair") for r in range(res.rounds)]
+    cap0 = np.asarray(g.cap0, np.int64).copy()
+    for entry in rec["chain"]:
+        bu, bv, bc = chain_batch(g.src, g.adj, g.is_original, cap0, n, s, t, entry)
+        r = pg.solve_dynamic(mf.UpdateBatch(bu, bv, bc), mf.SolverParams(mode="topology"))
+        assert r.flow_value == entry["flow"] == r.cut_capacity, (name, P, entry["seed"])
+        cap0[g.edge_indices(bu, bv)] = bc
+    pg.close()
