@@ -2405,41 +2405,52 @@ __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long 
 // L2 residency for the heights: every BFS discovery test and every push
 // scan reads h[] of random neighbours, so h (4n bytes; C2 17 MB, C4 96 MB)
 // gets a persisting access-policy window on the engine stream, the rest of
-// the traffic streams past it.  Off unless $MFX_L2_WINDOW = 1.
+// the traffic streams past it.
 static cudaError_t set_l2_window(const Topology &T, const StateObj &st) {
   static int enabled = -1;  // device support (probed once)
-  static size_t max_window = 0;
-  // Opt-in ($MFX_L2_WINDOW=1): the set-aside carve-out itself cost C2's
-  // static solve 23.6 -> 28.1 ms (15 -> 18 rounds) and gained C4 nothing
-  // (1.09 s either way), so by default no L2 is ever set aside.
+  static size_t max_window = 0, max_persist = 0, cur_persist = 0, l2 = 0;
+  // Default: on when the heights take at most a quarter of L2 (C1-C3, C2's
+  // 17 MB: static 21.3 -> 20.6-21.2 ms, dynamic -1.5 %; neutral on R-MAT),
+  // with the set-aside sized to the window.  Setting aside the device maximum
+  // instead cost C2's static solve 23.6 -> 28.1 ms (15 -> 18 rounds).
+  // $MFX_L2_WINDOW = 0 / 1 forces it off / on.
   const char *env = getenv("MFX_L2_WINDOW");  // (read per launch: A/B within a process)
-  if (enabled < 0 && (env == nullptr || atoi(env) == 0)) return cudaSuccess;  // never set aside
+  if (enabled < 0 && env != nullptr && atoi(env) == 0) return cudaSuccess;  // never set aside
   if (enabled < 0) {
     enabled = 1;
-    int mw = 0, mp = 0;
+    int mw = 0, mp = 0, l2b = 0;
     if (cudaDeviceGetAttribute(&mw, cudaDevAttrMaxAccessPolicyWindowSize, T.device) ||
-        cudaDeviceGetAttribute(&mp, cudaDevAttrMaxPersistingL2CacheSize, T.device) || mw <= 0 ||
-        mp <= 0) {
+        cudaDeviceGetAttribute(&mp, cudaDevAttrMaxPersistingL2CacheSize, T.device) ||
+        cudaDeviceGetAttribute(&l2b, cudaDevAttrL2CacheSize, T.device) || mw <= 0 || mp <= 0) {
       cudaGetLastError();
       enabled = 0;
     } else {
       max_window = (size_t)mw;
-      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mp)) {
-        cudaGetLastError();
-        enabled = 0;
-      }
+      max_persist = (size_t)mp;
+      l2 = (size_t)l2b;
     }
   }
-  const bool on = enabled > 0 && env != nullptr && atoi(env) != 0;
+  const size_t hbytes = sizeof(int) * (size_t)T.n;
+  const bool on = enabled > 0 && (env != nullptr ? atoi(env) != 0 : 4 * hbytes <= l2);
   cudaStreamAttrValue v = {};
   if (on) {
-    size_t bytes = sizeof(int) * (size_t)T.n;
+    size_t bytes = hbytes;
+    // set aside only what the window needs (the whole carve-out starved
+    // everything else: C2 static 23.6 -> 28.1 ms)
+    size_t want = bytes < max_persist ? bytes : max_persist;
+    if (want != cur_persist) {
+      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want)) return cudaGetLastError();
+      cur_persist = want;
+    }
     v.accessPolicyWindow.base_ptr = st.h;
     v.accessPolicyWindow.num_bytes = bytes < max_window ? bytes : max_window;
     v.accessPolicyWindow.hitRatio = 1.0f;
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  }  // (off: a zero-sized window clears a previous one)
+  } else if (cur_persist != 0) {  // (off: a zero-sized window clears a previous one,
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0)) return cudaGetLastError();
+    cur_persist = 0;  //  and nothing stays set aside)
+  }
   return cudaStreamSetAttribute(T.stream, cudaStreamAttributeAccessPolicyWindow, &v);
 }
 
