@@ -1119,6 +1119,10 @@ struct Kern {
         tot += cnt[b];
       }
       if (tot == 0 || *sy.s_abort) break;
+      // the sink alone, cut off (no residual slot into it) and no deficit:
+      // nothing can be discovered -- C4's closing relabel after its
+      // deficits are filled skips the epoch that would confirm that
+      if (!PP && E == 0 && a.strand && sy.s_snap[C_TALIVE] == 0 && sy.s_snap[C_DBASES] == 0) break;
       // Early exit (solve rounds only): every vertex holding excess has been
       // expanded, so the round's active list is complete; vertices beyond
       // keep h = n, which no push can cross, and the solve's last global
