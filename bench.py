@@ -71,6 +71,10 @@ CONFIGS = {
     "C4": ("road", (4900,), 10000,
            "C4: road-shaped lattice 4900x4900 (every row link, vertical links p=0.21, "
            "column 0 kept), both directions, caps U[1,100], corner to corner"),
+    # one GPU: the whole graph on the single-device engine (2.10 B slots fit
+    # the int32 layout); N > 1 GPUs: the vertex-range partition (bench_c5)
+    "C5": ("rmat_device", (26,), 1_000_000,
+           "C5: R-MAT scale 26 ef 16 (0.57,0.19,0.19; device generator, seed 0), caps U[1,100]"),
 }
 
 
@@ -94,6 +98,8 @@ def parse():
                          "NVTX range 'timed' (no e2e / re-solve / cpu legs)")
     ap.add_argument("--scale", type=int, default=26, help="C5 R-MAT scale")
     ap.add_argument("--parts", type=int, default=4, help="C5 parts when run as one process")
+    ap.add_argument("--engine", default="single", choices=["single", "part"],
+                    help="C5 on one GPU: the single-device engine, or the partition (--parts)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch plumbing only (ranks, collectives, max-over-ranks, JSON line); "
                          "no engine calls -- runs without a GPU")
@@ -308,11 +314,29 @@ def bench_ours(args, cfg, rank, world, dev, pg, backend):
 
     L = _lib.load()
     k = args.batch or CONFIGS[cfg][2]
-    n, us, vs, caps, s, t = make_instance(cfg, args.side)
-    t0 = time.perf_counter()
-    g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps), device=dev)
-    build_s = time.perf_counter() - t0
-    del us, vs, caps
+    device_graph = CONFIGS[cfg][0] == "rmat_device"
+    if device_graph:  # C5: drawn and built on the device (1.07 B edges)
+        n = 1 << args.scale
+        m = n * 16
+        e = [torch.empty(m, dtype=torch.int64, device=f"cuda:{dev}") for _ in range(3)]
+        s_, t_ = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(L.mfx_rmat_device(args.scale, 16, 0, 0.57, 0.19, 0.19, dev, e[0].data_ptr(),
+                                     e[1].data_ptr(), e[2].data_ptr(), ctypes.byref(s_),
+                                     ctypes.byref(t_)))
+        s, t = s_.value, t_.value
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g = mfx.build_bicsr_device(n, e[0].data_ptr(), e[1].data_ptr(), e[2].data_ptr(), m,
+                                   device=dev)
+        build_s = time.perf_counter() - t0
+        del e
+        torch.cuda.empty_cache()
+    else:
+        n, us, vs, caps, s, t = make_instance(cfg, args.side)
+        t0 = time.perf_counter()
+        g = mfx.build_bicsr(mfx.EdgeListGraph(n, us, vs, caps), device=dev)
+        build_s = time.perf_counter() - t0
+        del us, vs, caps
     params = mfx.SolverParams()
     res = mfx.solve_static(g, s, t, params)  # warm
     static_ms = [res.device["ms_total"]]
@@ -321,9 +345,19 @@ def bench_ours(args, cfg, rank, world, dev, pg, backend):
             res = mfx.solve_static(g, s, t, params)
             static_ms.append(res.device["ms_total"])
     st = res.state
-    el = g.to_edge_list()
     W, K = args.warmup, args.steps
-    chain = make_chain(n, el.us, el.vs, el.caps, s, t, W + K, k, 1000 * rank)
+    if device_graph:  # chained device draws, each from the capacities the last one left
+        from paper_2511_01235_b200 import gen
+        gs, chain = g.copy(), []
+        for i in range(W + K):
+            b = gen.device_sample_batch(gs, s, t, k, "mixed", seed=1000 * rank + i)
+            _lib.check(L.mfx_apply_updates(gs.handle, None, b[0].size, _lib.ptr64(b[0]),
+                                           _lib.ptr64(b[1]), _lib.ptr64(b[2])))  # (capacities only)
+            chain.append(b)
+        del gs
+    else:
+        el = g.to_edge_list()
+        chain = make_chain(n, el.us, el.vs, el.caps, s, t, W + K, k, 1000 * rank)
     dbat = [tuple(torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev}") for a in b)
             for b in chain]
     torch.cuda.synchronize()
@@ -422,8 +456,12 @@ def bench_ours(args, cfg, rank, world, dev, pg, backend):
     _lib.check(L.mfx_bench_chase(g.handle, 1 << 30, 20000, ctypes.byref(cns)))
     out["chase_ns"] = cns.value
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not device_graph:
         out["cpu_baseline"] = cpu_sample(g, st, s, t, n, k, args)
+    elif device_graph:
+        out["cpu_baseline"] = {"value": None, "unit": "ms/batch", "cores": 1, "kind": "port",
+                               "sample": "not run: the C oracle cannot hold the 2.1 B-slot graph "
+                                         "in host memory within the bench's time budget"}
     return out
 
 
@@ -761,7 +799,7 @@ def main():
             else:
                 bench_reference(args, cfg, world)
         return
-    if cfg == "C5":
+    if cfg == "C5" and (world > 1 or args.engine == "part"):
         bench_c5(args, rank, world, dev, pg, backend)
         return
     out = bench_ours(args, cfg, rank, world, dev, pg, backend)

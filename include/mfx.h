@@ -208,6 +208,14 @@ int mfx_bench_barrier(const mfx_graph *g, mfx_state *st, int iters, int blocks_p
 
 /* Diagnostics: per-barrier trace of the last solve launch when the process
  * ran with $MFX_TRACE_CAP > 0.  Entry = phase << 60 | items << 32 | ns. */
+/* Device batch sampler over one graph's original slots (gen.py fast_batch
+ * semantics, the law of mfx_part_sample_batch): k_dec decrements among slots
+ * with capacity, then k_inc increments among the rest, weight `bias` on the
+ * source row and on slots into the sink; host outputs in (u, v) order,
+ * *got = updates produced.  For graphs too large to sample on the host (C5). */
+int mfx_sample_batch(mfx_graph *g, int64_t source, int64_t sink, int64_t k_dec, int64_t k_inc,
+                     uint64_t seed, double bias, int64_t *us, int64_t *vs, int64_t *caps,
+                     int64_t *got);
 /* Diagnostics: the reached-set list the last tracked relabel kept (sparse
  * relabels seed from it); *count = -1 when the state holds no valid list. */
 int mfx_reached_list(const mfx_state *st, int32_t *out, int64_t cap, int64_t *count);

@@ -116,6 +116,8 @@ SIGNATURES = {
     "mfx_trace_fetch": (ctypes.c_int, [vp, vp, ctypes.POINTER(ctypes.c_uint64), i64, p_i64]),
     "mfx_reached_list": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_int32), i64, p_i64]),
     "mfx_bench_chase": (ctypes.c_int, [vp, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+    "mfx_sample_batch": (ctypes.c_int, [vp, i64, i64, i64, i64, ctypes.c_uint64, ctypes.c_double,
+                                        p_i64, p_i64, p_i64, p_i64]),
     "mfx_transfer_bytes": (ctypes.c_int, [i64, p_i64, p_i64]),
     "mfx_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(vp)]),
     "mfx_host_free": (ctypes.c_int, [vp]),

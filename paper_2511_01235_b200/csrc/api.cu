@@ -1379,6 +1379,22 @@ int mfx_trace_fetch(const mfx_state *st, const mfx_graph *g, uint64_t *out, int6
   return MFX_OK;
 }
 
+int mfx_sample_batch(mfx_graph *g, int64_t source, int64_t sink, int64_t k_dec, int64_t k_inc,
+                     uint64_t seed, double bias, int64_t *us, int64_t *vs, int64_t *caps,
+                     int64_t *got) {
+  Topology &T = *g->g.topo;
+  LOCK_TOPO(T);
+  if (source < 0 || source >= T.n || sink < 0 || sink >= T.n)
+    return fail(MFX_VALUE_ERROR, "source / sink out of range [0, %d)", T.n);
+  if (k_dec < 0 || k_inc < 0) return fail(MFX_VALUE_ERROR, "negative update counts");
+  CK(cudaSetDevice(T.device));
+  long long n_got = 0;
+  CK(sample_batch(g->g, (int)source, (int)sink, k_dec, k_inc, seed, bias, (long long *)us,
+                  (long long *)vs, (long long *)caps, &n_got));
+  *got = n_got;
+  return MFX_OK;
+}
+
 int mfx_reached_list(const mfx_state *st, int32_t *out, int64_t cap, int64_t *count) {
   Topology &T = *st->s.topo;
   LOCK_TOPO(T);

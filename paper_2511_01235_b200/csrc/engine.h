@@ -155,6 +155,10 @@ cudaError_t ensure_batch_capacity(Topology &t, int64_t k);
 // ---- state / batch kernels (state.cu) -------------------------------------
 cudaError_t launch_init_state(const GraphObj &g, StateObj &st);
 cudaError_t launch_vbin(const Topology &t, uint8_t *vbin);
+// device batch sampler (state.cu; gen.py fast_batch semantics, host outputs)
+cudaError_t sample_batch(const GraphObj &g, int s, int t, long long k_dec, long long k_inc,
+                         unsigned long long seed, double bias, long long *us, long long *vs,
+                         long long *caps, long long *got);
 // gate: optional batch error block; the kernel is a no-op if the batch failed
 cudaError_t launch_saturate(const GraphObj &g, StateObj &st, const long long *gate = nullptr);
 cudaError_t launch_refresh_pc(const GraphObj &g);

@@ -15,6 +15,9 @@
 //   saturate  the source row (state.py:42-59)
 #include <limits.h>
 
+#include <algorithm>
+#include <vector>
+
 #include <cub/cub.cuh>
 
 #include "engine.h"
@@ -612,6 +615,183 @@ cudaError_t launch_cap_check(const Topology &T, const int64_t *d_cap, unsigned l
       (const long long *)d_cap, T.rev, T.S, T.cap_bytes == 4, d_out);
   count_launch();
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// device batch sampler on one graph (gen.py fast_batch semantics, the law of
+// the partitioned engine's mfx_part_sample_batch): k_dec decrements among the
+// original slots with capacity (new in [0, old)), then k_inc increments among
+// the rest (new in [old + 1, 2 old + 10]), drawn without replacement by
+// exponential-race keys with weight `bias` on the source row and on slots
+// into the sink; emitted in slot order = (u, v) order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long smix_s(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void sample_weight_kernel(const int *__restrict__ adj, const uint8_t *__restrict__ orig,
+                                     long long S, long long s_lo, long long s_hi, int t, double bias,
+                                     unsigned long long *acc) {
+  unsigned long long w = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < S;
+       i += (long long)gridDim.x * blockDim.x)
+    if (orig[i]) w += (adj[i] == t || (i >= s_lo && i < s_hi)) ? (unsigned long long)bias : 1ull;
+  w = warp_sum(w);
+  if ((threadIdx.x & 31) == 0 && w) atomicAdd(acc, w);
+}
+
+template <typename CapT>
+__global__ void sample_kernel(const int *__restrict__ adj, const uint8_t *__restrict__ orig,
+                              const CapT *__restrict__ cap0, const uint8_t *taken, long long S,
+                              long long s_lo, long long s_hi, int t, double bias,
+                              unsigned long long seed, int dec, double tau, int cap,
+                              unsigned long long *cand, int *cnt) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < S;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (!orig[i] || taken[i] || (dec && cap0[i] <= 0)) continue;
+    const unsigned long long h = smix_s(seed ^ smix_s((unsigned long long)i));
+    const double u = ((double)(h >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double w = (adj[i] == t || (i >= s_lo && i < s_hi)) ? bias : 1.0;
+    const double key = -log(u) / w;
+    if (key < tau) {
+      const int q = atomicAdd(cnt, 1);
+      if (q < cap) cand[q] = ((unsigned long long)__float_as_uint((float)key) << 32) | (unsigned)i;
+    }
+  }
+}
+
+template <typename CapT>
+__global__ void sample_emit_kernel(const int *__restrict__ off, int n, const int *__restrict__ adj,
+                                   const CapT *__restrict__ cap0, const int *slots, int k, int dec,
+                                   unsigned long long seed, uint8_t *taken, long long *ou,
+                                   long long *ov, long long *oc) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    const int i = slots[j];
+    taken[i] = 1;
+    const long long old = (long long)cap0[i];
+    const unsigned long long h = smix_s(seed ^ 0xD1B54A32D192ED03ull ^ smix_s((unsigned long long)i + 1));
+    int a = 0, b = n;  // row of slot i
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (off[mid] <= i) a = mid;
+      else b = mid;
+    }
+    ou[j] = a;
+    ov[j] = adj[i];
+    oc[j] = dec ? (long long)(h % (unsigned long long)old)
+                : old + 1 + (long long)(h % (unsigned long long)(old + 10));
+  }
+}
+
+cudaError_t sample_batch(const GraphObj &g, int s, int t, long long k_dec, long long k_inc,
+                         unsigned long long seed, double bias, long long *us, long long *vs,
+                         long long *caps, long long *got) {
+  const Topology &T = *g.topo;
+  cudaStream_t st = T.stream;
+  *got = 0;
+  const long long S = T.S;
+  if (S == 0 || k_dec + k_inc == 0) return cudaSuccess;
+  int s_lo = 0, s_hi = 0;
+  cudaError_t e = cudaMemcpyAsync(&s_lo, T.off + s, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (!e) e = cudaMemcpyAsync(&s_hi, T.off + s + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+  uint8_t *taken = nullptr;
+  unsigned long long *acc = nullptr;
+  if (!e) e = cudaMalloc(&taken, (size_t)S);
+  if (!e) e = cudaMalloc(&acc, sizeof(unsigned long long));
+  if (!e) e = cudaMemsetAsync(taken, 0, (size_t)S, st);
+  if (!e) e = cudaMemsetAsync(acc, 0, sizeof(unsigned long long), st);
+  if (!e) e = cudaStreamSynchronize(st);
+  const int grid = grid_for(S, T.num_sms);
+  unsigned long long W = 0;
+  if (!e) {
+    sample_weight_kernel<<<grid, kBlock, 0, st>>>(T.adj, T.orig, S, s_lo, s_hi, t, bias, acc);
+    count_launch();
+    e = cudaMemcpyAsync(&W, acc, sizeof(W), cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+  }
+  long long done = 0;
+  for (int kind = 0; kind < 2 && !e; ++kind) {
+    const long long want = kind == 0 ? k_dec : k_inc;
+    if (want <= 0) continue;
+    const int cap = (int)(8 * want + 4096 < S ? 8 * want + 4096 : S);
+    unsigned long long *cand = nullptr, *sorted = nullptr;
+    int *cnt = nullptr, *d_slots = nullptr;
+    long long *d_out = nullptr;
+    void *tmp = nullptr;
+    e = cudaMalloc(&cand, sizeof(unsigned long long) * cap);
+    if (!e) e = cudaMalloc(&sorted, sizeof(unsigned long long) * cap);
+    if (!e) e = cudaMalloc(&cnt, sizeof(int));
+    double tau = 3.0 * (double)want / (double)(W > 0 ? W : 1) + 1e-12;
+    int c = 0;
+    for (int it = 0; it < 60 && !e; ++it) {
+      e = cudaMemsetAsync(cnt, 0, sizeof(int), st);
+      if (T.cap_bytes == 8)
+        sample_kernel<long long><<<grid, kBlock, 0, st>>>(
+            T.adj, T.orig, (const long long *)g.cap0, taken, S, s_lo, s_hi, t, bias,
+            seed * 2 + kind, kind == 0, tau, cap, cand, cnt);
+      else
+        sample_kernel<int><<<grid, kBlock, 0, st>>>(T.adj, T.orig, (const int *)g.cap0, taken, S,
+                                                    s_lo, s_hi, t, bias, seed * 2 + kind,
+                                                    kind == 0, tau, cap, cand, cnt);
+      count_launch();
+      if (!e) e = cudaMemcpyAsync(&c, cnt, sizeof(int), cudaMemcpyDeviceToHost, st);
+      if (!e) e = cudaStreamSynchronize(st);
+      if (c > cap) tau *= 0.5;                       // too many candidates
+      else if (c < want && tau < 1e30) tau *= 4.0;  // too few: widen (or nothing left)
+      else break;
+      if (c < want && tau >= 1e30) break;
+    }
+    if (c > cap) c = cap;
+    size_t tb = 0;
+    if (!e) e = cub::DeviceRadixSort::SortKeys(nullptr, tb, cand, sorted, c, 0, 64, st);
+    if (!e) e = cudaMalloc(&tmp, tb > 0 ? tb : 1);
+    if (!e) e = cub::DeviceRadixSort::SortKeys(tmp, tb, cand, sorted, c, 0, 64, st);
+    std::vector<unsigned long long> h((size_t)c);
+    if (!e && c > 0)
+      e = cudaMemcpyAsync(h.data(), sorted, sizeof(unsigned long long) * (size_t)c,
+                          cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    const long long take = want < c ? want : c;
+    std::vector<int> slots((size_t)(take > 0 ? take : 0));
+    for (long long j = 0; j < take; ++j) slots[j] = (int)(h[j] & 0xFFFFFFFFull);
+    std::sort(slots.begin(), slots.end());
+    if (!e) e = cudaMalloc(&d_slots, sizeof(int) * (size_t)(take > 0 ? take : 1));
+    if (!e) e = cudaMalloc(&d_out, sizeof(long long) * 3 * (size_t)(take > 0 ? take : 1));
+    if (!e && take > 0) {
+      e = cudaMemcpyAsync(d_slots, slots.data(), sizeof(int) * take, cudaMemcpyHostToDevice, st);
+      const int eg = grid_for(take, T.num_sms);
+      if (T.cap_bytes == 8)
+        sample_emit_kernel<long long><<<eg, kBlock, 0, st>>>(
+            T.off, T.n, T.adj, (const long long *)g.cap0, d_slots, (int)take, kind == 0,
+            seed * 2 + kind, taken, d_out, d_out + take, d_out + 2 * take);
+      else
+        sample_emit_kernel<int><<<eg, kBlock, 0, st>>>(T.off, T.n, T.adj, (const int *)g.cap0,
+                                                       d_slots, (int)take, kind == 0,
+                                                       seed * 2 + kind, taken, d_out, d_out + take,
+                                                       d_out + 2 * take);
+      count_launch();
+      if (!e) e = cudaMemcpyAsync(us + done, d_out, sizeof(long long) * take, cudaMemcpyDeviceToHost, st);
+      if (!e) e = cudaMemcpyAsync(vs + done, d_out + take, sizeof(long long) * take,
+                                  cudaMemcpyDeviceToHost, st);
+      if (!e) e = cudaMemcpyAsync(caps + done, d_out + 2 * take, sizeof(long long) * take,
+                                  cudaMemcpyDeviceToHost, st);
+      if (!e) e = cudaStreamSynchronize(st);
+    }
+    if (!e) done += take > 0 ? take : 0;
+    cudaFree(tmp);
+    cudaFree(cand);
+    cudaFree(sorted);
+    cudaFree(cnt);
+    cudaFree(d_slots);
+    cudaFree(d_out);
+  }
+  cudaFree(taken);
+  cudaFree(acc);
+  *got = done;
+  return e;
 }
 
 }  // namespace mfx

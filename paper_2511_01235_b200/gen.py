@@ -360,3 +360,25 @@ def source_edges(name: str, args):
     if name == "random_graph":
         return random_edges(*args)
     return globals()[name](*args)
+
+
+def device_sample_batch(g, s: int, t: int, k: int, kind: str = "mixed", seed: int = 0,
+                        bias: float = 10.0):
+    """:func:`fast_batch` semantics drawn on the device from ``g``'s own
+    capacities (csrc/state.cu sample_batch; the partitioned engine's sampler
+    law): for graphs whose edge list is too large to sample on the host (C5:
+    1.07 B edges).  Returns host arrays (us, vs, new_caps) in (u, v) order."""
+    import ctypes
+
+    from . import _lib as L
+    kind_ = KINDS[kind]
+    k_dec = k if kind_ == "dec" else 0 if kind_ == "inc" else k // 2
+    k_inc = k - k_dec
+    us, vs, cs = (np.empty(k, np.int64) for _ in range(3))
+    got = ctypes.c_int64()
+    L.check(L.load().mfx_sample_batch(g.handle, int(s), int(t), k_dec, k_inc, int(seed),
+                                      float(bias), L.ptr64(us), L.ptr64(vs), L.ptr64(cs),
+                                      ctypes.byref(got)))
+    n = got.value
+    order = np.lexsort((vs[:n], us[:n]))  # (the two kinds come out one after the other)
+    return us[:n][order], vs[:n][order], cs[:n][order]

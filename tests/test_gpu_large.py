@@ -98,3 +98,61 @@ def test_c2_terminal_hub_rows(mf):
     row = slice(off[s], off[s + 1])
     assert int(st.excess[s]) == -int(g.cap0[row].sum())
     assert np.all(st.cf[row] == 0)
+
+
+def _single_device_rmat(mf, scale):
+    import ctypes
+
+    import torch
+
+    from paper_2511_01235_b200 import _lib
+    n = 1 << scale
+    m = n * 16
+    e = [torch.empty(m, dtype=torch.int64, device="cuda:0") for _ in range(3)]
+    s, t = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.load().mfx_rmat_device(scale, 16, 0, 0.57, 0.19, 0.19, 0, e[0].data_ptr(),
+                                           e[1].data_ptr(), e[2].data_ptr(), ctypes.byref(s),
+                                           ctypes.byref(t)))
+    g = mf.build_bicsr_device(n, e[0].data_ptr(), e[1].data_ptr(), e[2].data_ptr(), m)
+    del e
+    torch.cuda.empty_cache()
+    return g, s.value, t.value
+
+
+def _c5_single_chain(mf, scale, batches, k, static_flow=None):
+    """The C5 generator on the single-device engine (the 2.1 B slots of
+    scale 26 fit its int32 layout): the static flow equals the partitioned
+    engine's on the same device-drawn graph, and every chained batch of
+    device-sampled mixed updates equals a static re-solve, flow == cut."""
+    from paper_2511_01235_b200 import gen, partition
+    g, s, t = _single_device_rmat(mf, scale)
+    res = mf.solve_static(g, s, t)
+    assert res.flow_value == res.certificate.cut_capacity > 0
+    if static_flow is None:  # (both engines at once do not fit one GPU at scale 26)
+        pg = partition.PartitionedGraph.rmat(scale, 16, 0, partition.LocalGroup(2))
+        assert pg.solve_static().flow_value == res.flow_value
+        pg.close()
+    else:
+        assert res.flow_value == static_flow
+    st = res.state
+    for b in range(batches):
+        bu, bv, bc = gen.device_sample_batch(g, s, t, k, "mixed", seed=b)
+        assert bu.size == k
+        r = mf.solve_dynamic(st, g, mf.UpdateBatch(bu, bv, bc))
+        assert r.flow_value == r.certificate.cut_capacity
+        rs = mf.resolve_static(g, mf.init_residuals(g, s, t))
+        assert rs.flow_value == r.flow_value, (scale, b)
+        st = r.state
+
+
+def test_c5_generator_single_device_scale22(mf):
+    _c5_single_chain(mf, 22, 2, 1_000_000)
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.environ.get("MFX_SLOW"), reason="opt-in (minutes): MFX_SLOW=1")
+def test_c5_full_single_device(mf):
+    """Full C5 (R-MAT 26, 2,103,824,774 slots) on one B200; 13,488,105 is the
+    partitioned engine's static flow on the same device-drawn graph
+    (profiles/round2/bench_lines.jsonl, C5 with 4 parts)."""
+    _c5_single_chain(mf, 26, 2, 1_000_000, static_flow=13488105)
