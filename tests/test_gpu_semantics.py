@@ -244,3 +244,39 @@ def test_bfs_ring_stress_bit_exact(mf, kind, arg, monkeypatch):
         assert np.array_equal(st0.height, want0), (i, kind)
         mf.backward_bfs_dynamic(st1, gd)
         assert np.array_equal(st1.height, want1), (i, kind)
+
+
+def test_device_sample_batch_law(mf):
+    """gen.device_sample_batch (mfx_sample_batch): k distinct original edges
+    in (u, v) order, the first half decrements (new in [0, old)) of edges with
+    capacity, the rest increments (new in [old + 1, 2 old + 10]) -- the
+    fast_batch / partitioned-sampler law -- and the batch applies cleanly."""
+    import numpy as np
+
+    from paper_2511_01235_b200 import gen
+    us, vs, caps, s, t = gen.rmat_graph(12, 16, 3)
+    n = 1 << 12
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    el = g.to_edge_list()
+    old = {(int(u), int(v)): int(c) for u, v, c in zip(el.us, el.vs, el.caps)}
+    k = 2000
+    bu, bv, bc = gen.device_sample_batch(g, s, t, k, "mixed", seed=7)
+    assert bu.size == k
+    keys = bu * n + bv
+    assert np.all(np.diff(keys) > 0)  # distinct, (u, v) order
+    dec = inc = 0
+    for u, v, c in zip(bu, bv, bc):
+        o = old[(int(u), int(v))]  # an original edge
+        if c < o:
+            dec += 1
+        else:
+            assert o + 1 <= c <= 2 * o + 10
+            inc += 1
+    assert dec == k // 2 and inc == k - k // 2
+    res = mf.solve_static(g, s, t)
+    r = mf.solve_dynamic(res.state, g, mf.UpdateBatch(bu, bv, bc))
+    assert r.flow_value == r.certificate.cut_capacity
+    # deterministic in the seed
+    bu2, bv2, bc2 = gen.device_sample_batch(mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps)),
+                                            s, t, k, "mixed", seed=7)
+    assert np.array_equal(bu, bu2) and np.array_equal(bv, bv2) and np.array_equal(bc, bc2)
