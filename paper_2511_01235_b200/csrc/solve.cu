@@ -2411,8 +2411,18 @@ __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long 
 // gets a persisting access-policy window on the engine stream, the rest of
 // the traffic streams past it.
 static cudaError_t set_l2_window(const Topology &T, const StateObj &st) {
-  static int enabled = -1;  // device support (probed once)
-  static size_t max_window = 0, max_persist = 0, cur_persist = 0, l2 = 0;
+  // per device (the persisting set-aside is a device-wide limit)
+  static int enabled_d[64];
+  static size_t max_window_d[64], max_persist_d[64], cur_persist_d[64], l2_d[64];
+  static bool init_d = false;
+  if (!init_d) {
+    for (int i = 0; i < 64; ++i) enabled_d[i] = -1;
+    init_d = true;
+  }
+  const int dv = T.device & 63;
+  int &enabled = enabled_d[dv];
+  size_t &max_window = max_window_d[dv], &max_persist = max_persist_d[dv],
+         &cur_persist = cur_persist_d[dv], &l2 = l2_d[dv];
   // Default: on when the heights take at most a quarter of L2 (C1-C3, C2's
   // 17 MB: static 21.3 -> 20.6-21.2 ms, dynamic -1.5 %; neutral on R-MAT),
   // with the set-aside sized to the window.  Setting aside the device maximum
