@@ -57,7 +57,8 @@ enum PartCtr {
   PC_OVF = 6,      // round-list overflow
   PC_BASES = 7,
   PC_BAD = 8,      // link: slots without a reverse
-  PC_N = 16
+  PC_OB0 = 16,     // outbox fill toward part q: PC_OB0 + q (reset by q once applied)
+  PC_N = 24
 };
 // per-part 64-bit statistics (local writes only)
 enum PartStat { PS_PUSH = 0, PS_RELABEL, PS_REPAIR, PS_BYTES, PS_FLOW, PS_CUT, PS_ACTIVE, PS_N = 8 };
@@ -79,6 +80,9 @@ struct PeerTab {
   int *F[kMaxParts][2][2];  // [part][buffer][bin]
   int *R[kMaxParts][2];     // [part][bin]
   int *ctr[kMaxParts];
+  int4 *out[kMaxParts];  // cut-slot push outboxes, obox_cap(nl) entries per destination
+  int obox;              // 1: cut-slot pushes go through the outboxes
+  int ostride;           // entries per destination: obox_cap(largest part), same on every part
   // own part only: vertices relabeled in the current round (the repair scope);
   // rl_cnt[1] counts the hub rows (> kPartHuge slots) among them, listed in rl_hub
   int *rl_list, *rl_flag, *rl_cnt, *rl_hub;
@@ -87,8 +91,17 @@ struct PeerTab {
 // device buffers of one part; the order here is the IPC export order
 enum PartBuf {
   B_OFF = 0, B_ADJ, B_CAP0, B_PC, B_CF, B_EX, B_H, B_MARK, B_F00, B_F01, B_F10, B_F11, B_R0, B_R1,
-  B_CTR, B_NBUF
+  B_CTR, B_OUT, B_NBUF
 };
+
+// Outbox entries per destination part: pushes along cut slots in one push
+// phase are buffered as (reverse slot, local vertex, amount) in the pushing
+// part's own memory and applied by the owner after the phase barrier (one
+// coalesced peer read per entry instead of two remote atomics and a remote
+// activation per push).  A full outbox falls back to the direct remote update.
+__host__ __device__ __forceinline__ int obox_cap(int nl) {
+  return nl < 1024 ? 1024 : (nl > (1 << 22) ? (1 << 22) : nl);
+}
 
 struct PartObj {
   int device = 0;
@@ -127,6 +140,8 @@ struct PartObj {
   int bk = 0;
   PeerTab tab;
   bool opened[kMaxParts][B_NBUF] = {};  // IPC mappings to close
+  bool inbox_pending = false;  // a push phase ran since the last swap
+  unsigned push_stamp = 0;
   ~PartObj();
 };
 
@@ -152,6 +167,7 @@ PartObj::~PartObj() {
           case B_R0: ptr = tab.R[p][0]; break;
           case B_R1: ptr = tab.R[p][1]; break;
           case B_CTR: ptr = tab.ctr[p]; break;
+          case B_OUT: ptr = tab.out[p]; break;
         }
         if (ptr) cudaIpcCloseMemHandle(ptr);
       }
@@ -182,6 +198,7 @@ static void tab_set_self(PartObj &o, int p) {
   T.R[p][0] = (int *)o.buf[B_R0];
   T.R[p][1] = (int *)o.buf[B_R1];
   T.ctr[p] = (int *)o.buf[B_CTR];
+  T.out[p] = (int4 *)o.buf[B_OUT];
 }
 
 // ---------------------------------------------------------------------------
@@ -648,10 +665,17 @@ __device__ void part_push_row(const PeerTab &T, int me, int u, int kc, unsigned 
       long long old = 1;
       if (amt > 0) {
         atomicAdd(cf + i, (int)-amt);
-        sys_add(T.cf[p] + rev[i], (int)amt);
-        old = sys_add(T.ex[p] + (v - T.lo[p]), amt);
+        int q = INT_MAX;
+        if (p != me && T.obox) q = atomicAdd(T.ctr[me] + PC_OB0 + p, 1);
+        if (q < T.ostride) {  // applied (and v activated) by p after the barrier
+          T.out[me][(size_t)p * T.ostride + q] = make_int4(rev[i], v - T.lo[p], (int)amt, 0);
+          loc[PS_BYTES] += 16;
+        } else {
+          sys_add(T.cf[p] + rev[i], (int)amt);
+          old = sys_add(T.ex[p] + (v - T.lo[p]), amt);
+          loc[PS_BYTES] += 28;
+        }
         loc[PS_PUSH]++;
-        loc[PS_BYTES] += 28;
       }
       part_activate_w(T, amt > 0 && old <= 0, v, stamp, s, t, rcap);  // (warp-uniform loop)
       carry += tot;
@@ -662,6 +686,39 @@ __device__ void part_push_row(const PeerTab &T, int me, int u, int kc, unsigned 
   }
   if (G > 32) __syncthreads();
   if (tid == 0 && hu < n && vol_ld(T.ex[me] + u) > 0) part_activate(T, ug, stamp, s, t, rcap);
+}
+
+// The owner's half of the buffered cut-slot pushes (after the push phase's
+// barrier): every peer's outbox toward `me`, read over P2P in entry order.
+__global__ void part_inbox_kernel(PeerTab T, int me, unsigned stamp, int s, int t, int rcap,
+                                  unsigned long long *stat) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned long long bytes = 0;
+  for (int p = 0; p < T.P; ++p) {
+    if (p == me) continue;
+    const int cnt = min(vol_ld(T.ctr[p] + PC_OB0 + me), T.ostride);
+    const int4 *box = T.out[p] + (size_t)me * T.ostride;
+    for (int j0 = gw * 32; j0 < cnt; j0 += nw * 32) {  // (warp-uniform trip count)
+      const int j = j0 + lane;
+      long long old = 1;
+      int v = 0;
+      if (j < cnt) {
+        const int4 e = __ldcv(box + j);
+        v = e.y;
+        sys_add(T.cf[me] + e.x, e.z);
+        old = sys_add(T.ex[me] + v, (long long)e.z);
+        bytes += 16 + 16;
+      }
+      part_activate_w(T, j < cnt && old <= 0, T.lo[me] + v, stamp, s, t, rcap);
+    }
+  }
+  bytes = warp_sum(bytes);
+  if (lane == 0 && bytes) atomicAdd(stat + PS_BYTES, bytes);
+}
+__global__ void part_inbox_reset_kernel(PeerTab T, int me) {
+  const int p = threadIdx.x;
+  if (p < T.P && p != me) atomicExch_system(T.ctr[p] + PC_OB0 + me, 0);
 }
 
 __global__ void part_push_kernel(PeerTab T, int me, int b0, int e0, int b1, int e1, int kc,
@@ -1178,7 +1235,8 @@ static int part_build(PartObj &o, long long m, const int64_t *d_us, const int64_
                           sizeof(int) * NL, sizeof(unsigned) * NL, sizeof(int) * NL,
                           sizeof(int) * NL, sizeof(int) * NL, sizeof(int) * NL,
                           sizeof(int) * (size_t)o.rcap, sizeof(int) * (size_t)o.rcap,
-                          sizeof(int) * PC_N};
+                          sizeof(int) * PC_N,
+                          sizeof(int4) * (size_t)o.tab.ostride * (o.P > 1 ? o.P : 1)};
   for (int b = 0; b < B_NBUF; ++b) {
     o.bytes[b] = sizes[b];
     PCK(cudaMalloc(&o.buf[b], sizes[b]));
@@ -1267,6 +1325,16 @@ int mfx_part_create(int64_t n, int nparts, int rank, const int64_t *bounds, int6
   memset(&o.tab, 0, sizeof(o.tab));
   o.tab.P = nparts;
   o.tab.n = (int)n;
+  {
+    // MFX_PART_OUTBOX: 0 = every cut-slot push updates the peer directly;
+    // k >= 2 = outboxes of k entries (tests: overflow into the direct path)
+    const char *ob = getenv("MFX_PART_OUTBOX");
+    const int obv = ob ? atoi(ob) : 1;
+    o.tab.obox = obv != 0;
+    long long big = 0;
+    for (int p = 0; p < nparts; ++p) big = std::max<long long>(big, bounds[p + 1] - bounds[p]);
+    o.tab.ostride = obv >= 2 ? obv : obox_cap((int)big);
+  }
   for (int p = 0; p <= nparts; ++p) o.tab.lo[p] = (int)bounds[p];
   for (int p = nparts + 1; p <= kMaxParts; ++p) o.tab.lo[p] = (int)n;
   cudaError_t e = cudaStreamCreateWithFlags(&o.stream, cudaStreamNonBlocking);
@@ -1395,6 +1463,7 @@ int mfx_part_attach(mfx_part *p, int peer, const void *blob, int64_t len) {
   T.R[peer][0] = (int *)ptr[B_R0];
   T.R[peer][1] = (int *)ptr[B_R1];
   T.ctr[peer] = (int *)ptr[B_CTR];
+  T.out[peer] = (int4 *)ptr[B_OUT];
   return MFX_OK;
 }
 
@@ -1425,6 +1494,7 @@ int mfx_part_attach_local(mfx_part *p, const mfx_part *q) {
     T.R[k][a] = R.R[k][a];
   }
   T.ctr[k] = R.ctr[k];
+  T.out[k] = R.out[k];
   return MFX_OK;
 }
 
@@ -1505,6 +1575,12 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
       break;
     }
     case MFX_PH_SWAP: {  // -> out: next frontier per bin, round-list tails, active, reached, ovf, bases
+      if (o.inbox_pending && o.P > 1) {  // the last push phase's buffered cut-slot pushes
+        part_inbox_kernel<<<G, kPartBlock, 0, st>>>(T, me, o.push_stamp, o.s, o.t, o.rcap, o.stat);
+        part_inbox_reset_kernel<<<1, 32, 0, st>>>(T, me);
+        count_launch(2);
+      }
+      o.inbox_pending = false;
       int h[PC_N];
       PCK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
       PCK(cudaStreamSynchronize(st));
@@ -1515,6 +1591,8 @@ int mfx_part_phase(mfx_part *pp, int phase, const int64_t *args, int64_t *out) {
     case MFX_PH_PUSH: {  // args: b0, e0, b1, e1, kc, stamp
       int b0 = (int)args[0], e0 = (int)std::min<int64_t>(args[1], o.rcap);
       int b1 = (int)args[2], e1 = (int)std::min<int64_t>(args[3], o.rcap);
+      o.inbox_pending = true;  // (peers may buffer pushes toward this part)
+      o.push_stamp = (unsigned)args[5];
       if (e0 > b0 || e1 > b1) {
         PCK(cudaMemsetAsync(o.hub_cnt, 0, sizeof(int), st));
         part_push_kernel<<<G, kPartBlock, 0, st>>>(T, me, b0, e0, b1, e1, (int)args[4],

@@ -30,7 +30,7 @@ from .solver import SolverError, SolverParams, operation_ceiling
 PH_LINK, PH_LINK_PC, PH_INIT, PH_SATURATE, PH_BFS_INIT, PH_BFS_EXPAND, PH_SWAP, PH_PUSH, \
     PH_REPAIR, PH_FINAL, PH_ACTIVE, PH_BATCH_RESOLVE, PH_BATCH_APPLY, PH_BATCH_FIX, \
     PH_TOPO_SEED = range(15)
-BLOB_BYTES = 15 * 64  # B_NBUF CUDA IPC handles (csrc/part.cu)
+BLOB_BYTES = 16 * 64  # B_NBUF CUDA IPC handles (csrc/part.cu)
 PH_ASYNC = 0x100  # MFX_PH_ASYNC (include/mfx.h): enqueue only
 # phases the host reads nothing back from (their out[] is unused by the round loop)
 ASYNC_PHASES = (PH_BFS_INIT, PH_BFS_EXPAND, PH_PUSH, PH_REPAIR)

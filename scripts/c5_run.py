@@ -39,8 +39,11 @@ def main():
     pg.phase_s.clear()
     r = pg.solve_static()
     names = ["link", "link_pc", "init", "saturate", "bfs_init", "bfs_expand", "swap", "push",
-             "repair", "final", "active", "resolve", "apply", "fix"]
-    print(json.dumps({"static_phase_s": {names[k]: round(v, 4) for k, v in pg.phase_s.items()}}))
+             "repair", "final", "active", "resolve", "apply", "fix", "topo_seed"]
+
+    def name(k):  # (PH_ASYNC entries: enqueue time of the concurrent form)
+        return names[k & 0xFF] + ("/enqueue" if k & partition.PH_ASYNC else "")
+    print(json.dumps({"static_phase_s": {name(k): round(v, 4) for k, v in pg.phase_s.items()}}))
     out = {"static_flow": r.flow_value, "static_s": round(r.seconds, 3), "rounds": r.rounds,
            "levels": r.bfs_levels, "waves": r.waves, "pushes": r.pushes,
            "static_edges_per_s": round(pg.m_original / r.seconds, 1)}
@@ -51,7 +54,7 @@ def main():
         gen_s = time.perf_counter() - t1
         pg.phase_s.clear()
         d = pg.solve_dynamic(batch)
-        print(json.dumps({"dynamic_phase_s": {names[k]: round(v, 4) for k, v in pg.phase_s.items()}}))
+        print(json.dumps({"dynamic_phase_s": {name(k): round(v, 4) for k, v in pg.phase_s.items()}}))
         row = {"batch": b, "k": len(batch), "sample_s": round(gen_s, 2), "dyn_flow": d.flow_value,
                "dyn_s": round(d.seconds, 3), "rounds": d.rounds, "levels": d.bfs_levels,
                "waves": d.waves}

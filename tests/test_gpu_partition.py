@@ -119,6 +119,30 @@ def test_static_and_chained_dynamic_flows(mf, part, name, P):
     pg.close()
 
 
+@pytest.mark.parametrize("outbox", ["0", "2", "64"])
+@pytest.mark.parametrize("name", ["grid64", "rmat12"])
+def test_cut_slot_outboxes(mf, part, name, outbox, monkeypatch):
+    """Cut-slot pushes buffered per destination part and applied by the owner
+    after the push phase (part.cu part_inbox_kernel): off (direct remote
+    updates), tiny outboxes that overflow into the direct path mid-phase, and
+    a small one; the golden static and chained flows hold in every mode."""
+    monkeypatch.setenv("MFX_PART_OUTBOX", outbox)
+    rec = G.rec[name]
+    n, us, vs, caps, s, t = instance(name)
+    g = mf.build_bicsr(mf.EdgeListGraph(n, us, vs, caps))
+    pg = part.PartitionedGraph(n, us, vs, caps, s, t, part.LocalGroup(3))
+    res = pg.solve_static()
+    assert res.flow_value == rec["static_flow"] == res.cut_capacity
+    cap0 = np.asarray(g.cap0, np.int64).copy()
+    for entry in rec["chain"][:3]:
+        bu, bv, bc = chain_batch(g.src, g.adj, g.is_original, cap0, n, s, t, entry)
+        r = pg.solve_dynamic(mf.UpdateBatch(bu, bv, bc))
+        assert r.flow_value == entry["flow"] == r.cut_capacity
+        assert pg.active_count() == 0
+        cap0[g.edge_indices(bu, bv)] = bc
+    pg.close()
+
+
 def test_batch_errors_match_reference_and_leave_state(mf, part):
     """The reference's error cases (tests/golden/make_golden.py) on the
     diamond, split over 2 parts: same exception text, state untouched."""
