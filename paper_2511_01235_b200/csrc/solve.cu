@@ -620,20 +620,6 @@ struct Kern {
     }
   }
 
-  // Discovery through slot i (valid lanes) of a frontier vertex at label
-  // nl - 1: the reverse residual cf[rev i] is read as pc[i] - cf[i] from the
-  // same row.
-  __device__ __forceinline__ void discover_slot(bool valid, int i, int nl, int ru = 0) {
-    int v = valid ? __ldg(a.adj + i) : 0;
-    bool low = false, first = false;
-    if (valid && v != a.forbidden && (!PP || region(v) == ru)) {
-      CapT f = (CapT)ldcg((const CapT *)(a.cf + i));
-      CapT r = (PP && ru == 1) ? f : __ldg(a.pc + i) - f;  // pull side: forward residual
-      if (r > 0 && (nocheck || ldcg(a.h + v) > nl)) low = relax(v, nl, first);
-    }
-    discovered(low, first, v, nl);
-  }
-
   // K slots i, i + stride, ... (< hi) per lane of a long row: every load of
   // the K slots is issued before any result is consumed, so a row scan is
   // not a chain of one-slot round trips.  Warp-uniform trip count.
@@ -783,7 +769,7 @@ struct Kern {
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int nl = ldcg(a.h + u) + 1;
       if (lane == 0) lc.bytes += (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-      for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl, region(u));
+      for (int i0 = lo; i0 < hi; i0 += 4 * 32) discover_slots<4>(i0 + lane, 32, hi, nl, region(u));  // (4 gathers in flight)
     }
     __syncthreads();
     if (threadIdx.x == 0) *hq_cnt = 0;
@@ -1186,7 +1172,7 @@ struct Kern {
         xc += lane == 0;
         if (lane == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kBfsSlot;
-        for (int i0 = lo; i0 < hi; i0 += 32) discover_slot(i0 + lane < hi, i0 + lane, nl, region(u));
+        for (int i0 = lo; i0 < hi; i0 += 4 * 32) discover_slots<4>(i0 + lane, 32, hi, nl, region(u));  // (4 gathers in flight)
       }
       // bin 2: CTA per row
       for (int j = blockIdx.x; j < cnt[2]; j += gridDim.x) {
@@ -1520,23 +1506,44 @@ struct Kern {
         }
         continue;
       }
-      // ---- pass 2: push along slots at height bh, ordered by slot
+      // ---- pass 2: push along slots at height bh, ordered by slot.  Each
+      // thread takes 4 consecutive slots (all loads in flight together), so
+      // a chunk of 4G slots costs one ordered scan of the per-thread sums
+      // (hub rows: a quarter of the dependent gathers and CTA barriers)
       int first = lo + (int)(best & 0xFFFFFFFFu);
       long long carry = 0;  // residual of admissible slots before this chunk
-      for (int i0 = first - ((first - lo) % G); i0 < hi && carry < eu; i0 += G) {
-        int i = i0 + tid;
-        long long c = 0;
-        int v = 0, vb = 0;
-        if (i < hi && i >= first) {
-          c = (long long)ldcg((const CapT *)(a.cf + i));
-          if (pull) c = (long long)__ldg(a.pc + i) - c;
-          if (c > 0) {
-            v = __ldg(a.adj + i);
-            vb = vbin(v);  // in flight with the height
-            if (ldcg(a.h + v) != bh || (PP && region(v) != ru)) c = 0;
+      for (int i0 = first - ((first - lo) % (4 * G)); i0 < hi && carry < eu; i0 += 4 * G) {
+        const int ib = i0 + 4 * tid;
+        long long c[4];
+        int v[4], vb[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = ib + r;
+          c[r] = 0;
+          v[r] = 0;
+          vb[r] = 0;
+          if (i < hi && i >= first) {
+            c[r] = (long long)ldcg((const CapT *)(a.cf + i));
+            if (pull) c[r] = (long long)__ldg(a.pc + i) - c[r];
+            v[r] = __ldg(a.adj + i);
           }
         }
-        long long incl = warp_incl_scan(c, lane), tot;
+        int hv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          hv[r] = -1;
+          if (c[r] > 0) {
+            vb[r] = vbin(v[r]);  // in flight with the height
+            hv[r] = ldcg(a.h + v[r]);
+          }
+        }
+        long long tsum = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (hv[r] != bh || (PP && region(v[r]) != ru)) c[r] = 0;
+          tsum += c[r];
+        }
+        long long incl = warp_incl_scan(tsum, lane), tot;
         if (G > 32) {
           __syncthreads();
           if (lane == 31) s_red[wib] = incl;
@@ -1552,28 +1559,34 @@ struct Kern {
         } else {
           tot = __shfl_sync(FULL, incl, 31);
         }
-        long long room = eu - carry - (incl - c);
-        long long amt = room <= 0 ? 0 : (room < c ? room : c);
-        bool act = false;
-        if (amt > 0) {
-          long long old;
-          if (pull) {  // pull amt along (v, u)
-            atomic_add(a.cf + __ldg(a.rev + i), (CapT)(-amt));
-            atomic_add(a.cf + i, (CapT)amt);
-            old = -atomic_add(a.ex + v, -amt);
-          } else {
-            atomic_add(a.cf + i, (CapT)(-amt));
-            atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
-            old = add_excess(v, amt);
-            if (!PP && a.strand && old < 0 && old + amt >= 0 && v != a.t)
-              fill_once();
+        long long pre = incl - tsum;  // admissible residual before this thread's slots
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = ib + r;
+          long long room = eu - carry - pre;
+          long long amt = room <= 0 ? 0 : (room < c[r] ? room : c[r]);
+          pre += c[r];
+          bool act = false;
+          if (amt > 0) {
+            long long old;
+            if (pull) {  // pull amt along (v, u)
+              atomic_add(a.cf + __ldg(a.rev + i), (CapT)(-amt));
+              atomic_add(a.cf + i, (CapT)amt);
+              old = -atomic_add(a.ex + v[r], -amt);
+            } else {
+              atomic_add(a.cf + i, (CapT)(-amt));
+              atomic_add(a.cf + __ldg(a.rev + i), (CapT)amt);
+              old = add_excess(v[r], amt);
+              if (!PP && a.strand && old < 0 && old + amt >= 0 && v[r] != a.t)
+                fill_once();
+            }
+            act = old <= 0 && v[r] != a.s && v[r] != a.t;
+            lc.pushes++;
+            lc.bytes += Bytes<CapT>::kPush;
+            if (Async && act) __threadfence();  // push visible before the hand-off
           }
-          act = old <= 0 && v != a.s && v != a.t;
-          lc.pushes++;
-          lc.bytes += Bytes<CapT>::kPush;
-          if (Async && act) __threadfence();  // push visible before the hand-off
+          activate(act, v[r], vb[r], stamp, nbase);
         }
-        activate(act, v, vb, stamp, nbase);
         carry += tot;
       }
       long long moved = carry < eu ? carry : eu;
@@ -1603,15 +1616,26 @@ struct Kern {
   // =========================================================================
   // repair (kernels.py:70-93): saturate steep residual edges h(u) > h(v)+1
   // =========================================================================
-  __device__ __forceinline__ void repair_slot(int u, int hu, int i, int ru = 0) {
-    CapT f = (CapT)ldcg((const CapT *)(a.cf + i));
-    const bool pull = PP && ru == 1;
-    if (pull) f = __ldg(a.pc + i) - f;  // cf(v -> u)
-    if (f > 0) {
-      int v = __ldg(a.adj + i);
-      if ((!PP || region(v) == ru) && hu > ldcg(a.h + v) + 1) {
-        if (pull) repair_pull(u, v, i);
-        else repair_push(u, v, i, i);
+  // slots i, i + stride, ... i + 3 stride (< hi) of u with every load in
+  // flight before any is consumed (one round trip per 4 slots, not per slot)
+  __device__ __forceinline__ void repair_slots4(int u, int hu, int i, int stride, int hi, int ru) {
+    CapT f[4];
+    int v[4], hv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = i + k * stride;
+      f[k] = j < hi ? (CapT)ldcg((const CapT *)(a.cf + j)) : (CapT)0;
+      if (PP && ru == 1 && j < hi) f[k] = __ldg(a.pc + j) - f[k];  // cf(v -> u)
+      v[k] = j < hi ? __ldg(a.adj + j) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hv[k] = f[k] > 0 ? ldcg(a.h + v[k]) : INT_MAX - 1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = i + k * stride;
+      if (f[k] > 0 && (!PP || region(v[k]) == ru) && hu > hv[k] + 1) {
+        if (PP && ru == 1) repair_pull(u, v[k], j);
+        else repair_push(u, v[k], j, j);
       }
     }
   }
@@ -1685,7 +1709,7 @@ struct Kern {
       int lo = __ldg(a.off + u), hi = __ldg(a.off + u + 1);
       int hu = ldcg(a.h + u);
       if (lane == 0) lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-      for (int i = lo + lane; i < hi; i += 32) repair_slot(u, hu, i, region(u));
+      for (int i = lo + lane; i < hi; i += 4 * 32) repair_slots4(u, hu, i, 32, hi, region(u));
     }
     for (int b = 2; b < NBIN; ++b) {
       for (int j = blockIdx.x; j < end[b]; j += gridDim.x) {
@@ -1699,7 +1723,8 @@ struct Kern {
         int hu = ldcg(a.h + u);
         if (threadIdx.x == 0)
           lc.bytes += Bytes<CapT>::kVertex + (unsigned long long)(hi - lo) * Bytes<CapT>::kSlot;
-        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) repair_slot(u, hu, i, region(u));
+        for (int i = lo + threadIdx.x; i < hi; i += 4 * blockDim.x)
+          repair_slots4(u, hu, i, blockDim.x, hi, region(u));
       }
     }
   }
