@@ -40,7 +40,10 @@ print(f"build {time.perf_counter() - t0:.1f} s: n {g.n} slots {g.m} (int32 limit
 print(f"device memory in use {torch.cuda.memory_allocated() / 1e9:.1f} GB (torch)", flush=True)
 for rep in range(2):
     r = mfx.solve_static(g, s.value, t.value)
-    print(f"static: flow {r.flow_value} rounds {r.rounds} {r.device['ms_total']:.1f} ms", flush=True)
+    d = r.device
+    print(f"static: flow {r.flow_value} rounds {r.rounds} {d['ms_total']:.1f} ms (bfs "
+          f"{d['ns_bfs'] / 1e6:.1f} in {d['bfs_levels']} levels, push {d['ns_push'] / 1e6:.1f} in "
+          f"{d['waves']} waves, repair {d['ns_repair'] / 1e6:.1f})", flush=True)
 st = r.state
 us, vs = e[0], e[1]
 keep = us != vs
@@ -64,7 +67,9 @@ for mode in ("plain", "pushpull"):
                                                                       bc.cpu().numpy()))
         d = rr.device
         print(f"{mode} batch {b}: flow {rr.flow_value} rounds {rr.rounds} {d['ms_total']:.1f} ms "
-              f"(update {d['ms_update']:.1f})", flush=True)
+              f"(update {d['ms_update']:.1f}, bfs {d['ns_bfs'] / 1e6:.1f} in {d['bfs_levels']} levels, "
+              f"push {d['ns_push'] / 1e6:.1f} in {d['waves']} waves, repair {d['ns_repair'] / 1e6:.1f})",
+              flush=True)
         st2 = rr.state
     rs = mfx.resolve_static(g2, mfx.init_residuals(g2, s.value, t.value))
     print(f"{mode}: static re-solve flow {rs.flow_value} {rs.device['ms_total']:.1f} ms "
