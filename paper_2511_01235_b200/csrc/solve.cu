@@ -1506,18 +1506,20 @@ struct Kern {
         }
         continue;
       }
-      // ---- pass 2: push along slots at height bh, ordered by slot.  Each
-      // thread takes 4 consecutive slots (all loads in flight together), so
-      // a chunk of 4G slots costs one ordered scan of the per-thread sums
-      // (hub rows: a quarter of the dependent gathers and CTA barriers)
+      // ---- pass 2: push along slots at height bh, ordered by slot.  In a
+      // CTA row each thread takes R = 4 consecutive slots (all loads in
+      // flight together), so a chunk of 4G slots costs one ordered scan of
+      // the per-thread sums (hub rows: a quarter of the dependent gathers and
+      // CTA barriers); warp rows are short and keep one slot per lane
+      constexpr int R = G > 32 ? 4 : 1;
       int first = lo + (int)(best & 0xFFFFFFFFu);
       long long carry = 0;  // residual of admissible slots before this chunk
-      for (int i0 = first - ((first - lo) % (4 * G)); i0 < hi && carry < eu; i0 += 4 * G) {
-        const int ib = i0 + 4 * tid;
-        long long c[4];
-        int v[4], vb[4];
+      for (int i0 = first - ((first - lo) % (R * G)); i0 < hi && carry < eu; i0 += R * G) {
+        const int ib = i0 + R * tid;
+        long long c[R];
+        int v[R], vb[R];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < R; ++r) {
           const int i = ib + r;
           c[r] = 0;
           v[r] = 0;
@@ -1528,9 +1530,9 @@ struct Kern {
             v[r] = __ldg(a.adj + i);
           }
         }
-        int hv[4];
+        int hv[R];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < R; ++r) {
           hv[r] = -1;
           if (c[r] > 0) {
             vb[r] = vbin(v[r]);  // in flight with the height
@@ -1539,7 +1541,7 @@ struct Kern {
         }
         long long tsum = 0;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < R; ++r) {
           if (hv[r] != bh || (PP && region(v[r]) != ru)) c[r] = 0;
           tsum += c[r];
         }
@@ -1561,7 +1563,7 @@ struct Kern {
         }
         long long pre = incl - tsum;  // admissible residual before this thread's slots
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < R; ++r) {
           const int i = ib + r;
           long long room = eu - carry - pre;
           long long amt = room <= 0 ? 0 : (room < c[r] ? room : c[r]);
