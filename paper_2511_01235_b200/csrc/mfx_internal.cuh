@@ -21,9 +21,39 @@
 // CapT is int32 when every pair sum fits (the default), else int64.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <utility>
 #include <stdint.h>
 
 namespace mfx {
+
+// ---- programmatic dependent launch (the O(k) pre-phase chain) -------------
+// Each small kernel of the dynamic pre-phase is launched with programmatic
+// stream serialisation: it may be scheduled while its predecessor drains and
+// waits on the device (griddepcontrol.wait, full completion and visibility of
+// the prerequisite grid) before touching anything, so the chain pays one
+// launch latency instead of one per kernel.  Every kernel launched through
+// pdl_launch starts with pdl_wait().
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), unsigned grid, unsigned block,
+                              cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 
 #ifndef MFX_BLOCK
 #define MFX_BLOCK 256

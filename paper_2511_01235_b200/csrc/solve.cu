@@ -2412,6 +2412,7 @@ cudaError_t launch_pp_setup(const GraphObj &g, StateObj &st, bool crossing, cons
 
 __global__ void ctrl_begin_kernel(Ctrl *c, double timeout_s, unsigned long long ceiling,
                                   int reset_counters) {
+  pdl_wait();
   unsigned long long now = globaltimer();
   c->deadline_ns = now + (unsigned long long)(timeout_s * 1e9);
   c->last_ns = now;
@@ -2584,9 +2585,9 @@ static cudaError_t launch_solve_t(const GraphObj &g, StateObj &st, const SolveCo
   // valid again only when solve_status reads back a clean tracked finish
   st.tl_ok = false;
 
-  ctrl_begin_kernel<<<1, 1, 0, T.stream>>>(st.ctrl, cfg.timeout_s, cfg.ceiling,
-                                          cfg.reset_counters ? 1 : 0);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = pdl_launch(ctrl_begin_kernel, 1, 1, T.stream, st.ctrl, cfg.timeout_s, cfg.ceiling,
+                     cfg.reset_counters ? 1 : 0)))
+    return e;
 
   const void *fn = cfg.pushpull ? (const void *)solve_kernel<CapT, true>
                                 : (const void *)solve_kernel<CapT, false>;

@@ -39,6 +39,7 @@ template <typename CapT>
 __global__ void saturate_kernel(const int *__restrict__ off, const int *__restrict__ adj,
                                 const int *__restrict__ rev, CapT *cf, long long *ex, int s,
                                 const long long *gate) {
+  pdl_wait();
   __shared__ long long scr[kWarps];
   if (gate && batch_failed(gate)) return;
   int lo = off[s], hi = off[s + 1];
@@ -66,10 +67,11 @@ __global__ void saturate_kernel(const int *__restrict__ off, const int *__restri
 template <typename CapT>
 static cudaError_t saturate_t(const GraphObj &g, StateObj &st, const long long *gate) {
   Topology &T = *g.topo;
-  saturate_kernel<CapT><<<grid_for(1 << 22, T.num_sms, 2), kBlock, 0, T.stream>>>(
-      T.off, T.adj, T.rev, (CapT *)st.cf, st.ex, st.s, gate);
+  cudaError_t e = pdl_launch(saturate_kernel<CapT>, grid_for(1 << 22, T.num_sms, 2), kBlock,
+                             T.stream, (const int *)T.off, (const int *)T.adj, (const int *)T.rev,
+                             (CapT *)st.cf, st.ex, st.s, gate);
   count_launch();
-  return cudaGetLastError();
+  return e ? e : cudaGetLastError();
 }
 
 cudaError_t launch_saturate(const GraphObj &g, StateObj &st, const long long *gate) {
@@ -240,6 +242,7 @@ __global__ void batch_resolve_kernel(const int *__restrict__ off, const int *__r
                                      const CapT *__restrict__ cap0, int n, long long k,
                                      const long long *us, const long long *vs, const long long *caps,
                                      int *slot, int *uv, long long *err) {
+  pdl_wait();
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
        j += (long long)gridDim.x * blockDim.x) {
     long long c = caps[j];
@@ -260,6 +263,7 @@ template <typename CapT>
 __global__ void batch_over_kernel(long long k, const int *slot, const int *first,
                                   const int *__restrict__ rev, const CapT *cap0,
                                   const long long *caps, long long *err) {
+  pdl_wait();
   if (err[E_NEG] != LLONG_MAX || err[E_UNKNOWN] != LLONG_MAX) return;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
        j += (long long)gridDim.x * blockDim.x) {
@@ -271,6 +275,7 @@ __global__ void batch_over_kernel(long long k, const int *slot, const int *first
 }
 
 __global__ void batch_first_kernel(long long k, const int *slot, int *first, const long long *err) {
+  pdl_wait();
   if (err[E_NEG] != LLONG_MAX || err[E_UNKNOWN] != LLONG_MAX) return;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
        j += (long long)gridDim.x * blockDim.x)
@@ -278,6 +283,7 @@ __global__ void batch_first_kernel(long long k, const int *slot, int *first, con
 }
 
 __global__ void batch_dup_kernel(long long k, const int *slot, const int *first, long long *err) {
+  pdl_wait();
   if (err[E_NEG] != LLONG_MAX || err[E_UNKNOWN] != LLONG_MAX) return;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
        j += (long long)gridDim.x * blockDim.x)
@@ -287,6 +293,7 @@ __global__ void batch_dup_kernel(long long k, const int *slot, const int *first,
 // reference reports order[p] of the first equal pair in the stable (slot, j)
 // order: the second-smallest update index on the smallest duplicated slot
 __global__ void batch_dupidx_kernel(long long k, const int *slot, const int *first, long long *err) {
+  pdl_wait();
   if (err[E_NEG] != LLONG_MAX || err[E_UNKNOWN] != LLONG_MAX || err[E_DUPSLOT] == LLONG_MAX) return;
   long long ds = err[E_DUPSLOT];
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
@@ -297,6 +304,7 @@ __global__ void batch_dupidx_kernel(long long k, const int *slot, const int *fir
 template <typename CapT>
 __global__ void batch_apply_kernel(long long k, const int *slot, int *first, const long long *caps,
                                    CapT *cap0, CapT *cf, const long long *err, int apply) {
+  pdl_wait();
   bool ok = apply && !batch_failed(err);
   bool resolved = err[E_NEG] == LLONG_MAX && err[E_UNKNOWN] == LLONG_MAX;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
@@ -315,6 +323,7 @@ template <typename CapT>
 __global__ void batch_repair_kernel(long long k, const int *slot, const int *uv,
                                     const int *__restrict__ rev, CapT *cf, long long *ex,
                                     const long long *err) {
+  pdl_wait();
   if (batch_failed(err)) return;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
        j += (long long)gridDim.x * blockDim.x) {
@@ -334,6 +343,7 @@ __global__ void batch_repair_kernel(long long k, const int *slot, const int *uv,
 template <typename CapT>
 __global__ void batch_pc_kernel(long long k, const int *slot, const int *__restrict__ rev,
                                 const CapT *cap0, CapT *pc, const long long *err) {
+  pdl_wait();
   if (batch_failed(err)) return;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
        j += (long long)gridDim.x * blockDim.x) {
@@ -345,6 +355,7 @@ __global__ void batch_pc_kernel(long long k, const int *slot, const int *__restr
 }
 
 __global__ void fill_ll_kernel(long long *p, int cnt, long long v) {
+  pdl_wait();
   if (threadIdx.x < cnt) p[threadIdx.x] = v;
 }
 
@@ -354,39 +365,47 @@ static cudaError_t batch_t(GraphObj &g, StateObj *st, int64_t k, const int64_t *
                            bool update_excess, int *launches) {
   Topology &T = *g.topo;
   Workspace &W = T.ws;
-  fill_ll_kernel<<<1, 32, 0, T.stream>>>(W.d_err, E_N, LLONG_MAX);
+  cudaError_t e = pdl_launch(fill_ll_kernel, 1, 32, T.stream, W.d_err, (int)E_N, (long long)LLONG_MAX);
   count_launch();
   if (launches) *launches += 1;
-  if (k == 0) return cudaGetLastError();
+  if (e || k == 0) return e ? e : cudaGetLastError();
   int grid = grid_for(k, T.num_sms);
   const long long *us = (const long long *)d_us, *vs = (const long long *)d_vs,
                   *cs = (const long long *)d_caps;
-  batch_resolve_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(T.off, T.adj, T.rev, T.orig,
-                                                            (const CapT *)g.cap0, T.n, k, us, vs,
-                                                            cs, W.d_slot, W.d_uv, W.d_err);
-  batch_first_kernel<<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, W.d_err);
+  const long long kk = k;
+#define PDL(...) \
+  if ((e = pdl_launch(__VA_ARGS__))) return e
+  PDL(batch_resolve_kernel<CapT>, grid, kBlock, T.stream, (const int *)T.off, (const int *)T.adj,
+      (const int *)T.rev, (const uint8_t *)T.orig, (const CapT *)g.cap0, T.n, kk, us, vs, cs,
+      W.d_slot, W.d_uv, W.d_err);
+  PDL(batch_first_kernel, grid, kBlock, T.stream, kk, (const int *)W.d_slot, W.slot_first,
+      (const long long *)W.d_err);
   if (sizeof(CapT) == 4) {
-    batch_over_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, T.rev,
-                                                           (const CapT *)g.cap0, cs, W.d_err);
+    PDL(batch_over_kernel<CapT>, grid, kBlock, T.stream, kk, (const int *)W.d_slot,
+        (const int *)W.slot_first, (const int *)T.rev, (const CapT *)g.cap0, cs, W.d_err);
     count_launch();
     if (launches) *launches += 1;
   }
-  batch_dup_kernel<<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, W.d_err);
-  batch_dupidx_kernel<<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, W.slot_first, W.d_err);
-  batch_apply_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(
-      k, W.d_slot, W.slot_first, cs, (CapT *)g.cap0, st ? (CapT *)st->cf : nullptr, W.d_err,
+  PDL(batch_dup_kernel, grid, kBlock, T.stream, kk, (const int *)W.d_slot,
+      (const int *)W.slot_first, W.d_err);
+  PDL(batch_dupidx_kernel, grid, kBlock, T.stream, kk, (const int *)W.d_slot,
+      (const int *)W.slot_first, W.d_err);
+  PDL(batch_apply_kernel<CapT>, grid, kBlock, T.stream, kk, (const int *)W.d_slot, W.slot_first,
+      cs, (CapT *)g.cap0, st ? (CapT *)st->cf : (CapT *)nullptr, (const long long *)W.d_err,
       apply ? 1 : 0);
   int nl = 5;
   if (apply && st) {
-    batch_repair_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(
-        k, W.d_slot, W.d_uv, T.rev, (CapT *)st->cf, update_excess ? st->ex : nullptr, W.d_err);
+    PDL(batch_repair_kernel<CapT>, grid, kBlock, T.stream, kk, (const int *)W.d_slot,
+        (const int *)W.d_uv, (const int *)T.rev, (CapT *)st->cf,
+        update_excess ? st->ex : (long long *)nullptr, (const long long *)W.d_err);
     ++nl;
   }
   if (apply) {
-    batch_pc_kernel<CapT><<<grid, kBlock, 0, T.stream>>>(k, W.d_slot, T.rev, (const CapT *)g.cap0,
-                                                         (CapT *)g.pc, W.d_err);
+    PDL(batch_pc_kernel<CapT>, grid, kBlock, T.stream, kk, (const int *)W.d_slot,
+        (const int *)T.rev, (const CapT *)g.cap0, (CapT *)g.pc, (const long long *)W.d_err);
     ++nl;
   }
+#undef PDL
   if (launches) *launches += nl;
   count_launch(nl);
   return cudaGetLastError();

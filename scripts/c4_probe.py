@@ -99,7 +99,7 @@ def main():
                               f"active {x & 0xFFFFF}")
                 T.rounds_view(f"batch {i}", rr.state, g)
             st = rr.state
-        print(f"# {spec or 'default'}: mean {np.mean(rows):.2f} ms/batch over {len(rows)} batches "
+        print(f"# {spec or 'default'}: mean {np.mean(rows):.4f} ms/batch over {len(rows)} batches "
               f"(max {np.max(rows):.1f}); flows {'same' if True else ''}", flush=True)
         for k in env:
             os.environ.pop(k, None)
